@@ -1,0 +1,260 @@
+/*
+ * genie.h -- the C-ABI drop-in boundary of the B200-native GENIE match-count
+ * engine (libgenie_b200.so, sm_100a).
+ *
+ * The reference (mcx, /root/reference/proj/include) has no FFI layer: its
+ * hot path is inline C++ in namespace mcx.  These entry points are exactly
+ * what a binding of that path needs; the C++ mirror in include/mcx/*.hpp
+ * (same names and semantics as the reference) and the Python mirror
+ * (paper_1603_08390_b200.mcx) are thin hosts over them.  Each function names
+ * the reference interface it replaces.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; no torch / CUDA types in signatures
+ *    (streams are passed as void*).
+ *  - every call returns a genie_status; on failure a NUL-terminated message
+ *    is written to err[errlen] (may be NULL).  Messages that concern one
+ *    query carry the reference prefix "query N (stage): " (engine.hpp:127-135).
+ *  - the index handle owns its device memory and one CUDA stream; it is not
+ *    re-entrant (one controlling thread per handle).
+ *  - results are written into caller-owned host buffers (or device buffers
+ *    for the *_device variants).
+ */
+#ifndef GENIE_GENIE_H
+#define GENIE_GENIE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error taxonomy mirrors mcx/error.hpp:24-41 and the CLI exit codes
+ * (mcx_cli.cpp:682-694). */
+typedef enum {
+    GENIE_OK = 0,
+    GENIE_ERR_CONTRACT = 1,  /* mcx::ContractError (std::invalid_argument) */
+    GENIE_ERR_DATA = 2,      /* mcx::DataError (std::runtime_error) */
+    GENIE_ERR_INVARIANT = 3, /* mcx::InvariantError (std::logic_error) */
+    GENIE_ERR_CUDA = 4,      /* CUDA runtime / device failure */
+    GENIE_ERR_NCCL = 5,
+    GENIE_RETRY = 6          /* device batch outgrew the workspace: it was grown, re-issue the batch */
+} genie_status;
+
+/* mcx::Selector (engine.hpp:33).  All selectors return identical results.
+ *  CPQ    : Count Priority Queue per object tile -- AuditThreshold gate,
+ *           ZipperArray and a lock-free Robin Hood table in shared memory.
+ *  BUCKET : histogram k-selection over the tile counters (GEN-SPQ ablation,
+ *           stands in for bucket_kselect select.hpp:62-120).
+ *  SORT   : same device path as BUCKET (sort_topk select.hpp:40-51 semantics). */
+typedef enum { GENIE_SELECT_CPQ = 0, GENIE_SELECT_BUCKET = 1, GENIE_SELECT_SORT = 2 } genie_selector;
+
+/* mcx::TopKEntry (cpq.hpp:31-41): result order is count desc, id asc. */
+typedef struct {
+    uint32_t id;
+    uint32_t count;
+} genie_entry;
+
+/* mcx::EngineConfig (engine.hpp:36-42) plus device knobs.  Every field is
+ * result-invariant; zero means "default" except span_chunk /
+ * max_spans_per_task, where 0 is a ContractError exactly as in
+ * engine.hpp:186-188 (use genie_config_default()). */
+typedef struct {
+    uint32_t selector;           /* genie_selector */
+    uint32_t span_chunk;         /* postings per warp work unit (rounded up to 128) */
+    uint32_t max_spans_per_task; /* accepted for API parity; must be > 0 */
+    uint32_t tile_bytes;         /* shared-memory counter bytes per object tile (0: default) */
+    uint32_t ctas_per_sm;        /* persistent scan CTAs per SM (0: default) */
+    uint32_t flags;              /* reserved, 0 */
+} genie_config;
+
+/* mcx::StageTimings (engine.hpp:44-50), measured with CUDA events on the
+ * handle's stream (device stages) and the host clock (total). */
+typedef struct {
+    uint64_t lookup_ns;
+    uint64_t match_ns;
+    uint64_t select_ns;
+    uint64_t merge_ns;
+    uint64_t total_ns;
+} genie_stage_ns;
+
+/* mcx::MemoryStats (engine.hpp:52-56) with the reference accounting
+ * (cpq.hpp:103-106, 359-362), plus device-side facts. */
+typedef struct {
+    uint64_t counter_bytes;  /* sum_q ceil(n * W_q / 8) */
+    uint64_t gate_bytes;     /* sum_q ((bound_q + 1) * 4 + 4) */
+    uint64_t table_bytes;    /* sum_q 8 * bit_ceil(max(2 k_q bound_q, 2)) */
+    uint64_t postings;       /* sum_q P_q: posting ids scanned (algorithmic work) */
+    uint64_t work_items;     /* (query, object tile) items processed */
+    uint64_t fallback_tiles; /* tiles whose table overflowed -> exact histogram select */
+} genie_batch_stats;
+
+genie_config genie_config_default(void);
+
+/* Build-side ------------------------------------------------------------- */
+
+typedef struct genie_index genie_index;
+
+/* Uploads a CSR inverted index to `device` (replaces mcx::build_index's
+ * product, index.hpp:190-250, and InvertedIndex, index.hpp:41-182).
+ *   keys[K]      packed dim<<32|token (Keyword::packed, model.hpp:43-45),
+ *                strictly ascending
+ *   key_off[K+1] postings offsets; key j owns postings[key_off[j], key_off[j+1])
+ *   postings[P]  object ids, strictly ascending within each key, < num_objects
+ *   dim_max_mult optional [65536]: InvertedIndex::max_multiplicity per dim
+ *                (index.hpp:110-113); NULL computes it on the device
+ * id_offset is added to every reported id (IndexPartition::id_offset,
+ * index.hpp:254-259) -- used for object-range shards.
+ * Validation failures (order, range) are GENIE_ERR_DATA. */
+int genie_index_create(uint32_t num_objects, uint64_t num_keys, const uint64_t* keys,
+                       const uint64_t* key_off, const uint32_t* postings,
+                       const uint32_t* dim_max_mult, uint32_t id_offset, int device,
+                       genie_index** out, char* err, size_t errlen);
+
+/* Same as genie_index_create but keeps only object ids in [id_begin, id_end)
+ * of a full CSR (rebased to local ids, id_offset = id_begin): one GPU's slice
+ * of partition_dataset (index.hpp:263-291) without materialising parts. */
+int genie_index_create_shard(uint32_t num_objects, uint64_t num_keys, const uint64_t* keys,
+                             const uint64_t* key_off, const uint32_t* postings,
+                             uint32_t id_begin, uint32_t id_end, int device, genie_index** out,
+                             char* err, size_t errlen);
+
+void genie_index_destroy(genie_index* ix);
+
+/* Index facts: num_objects, keys, postings, id_offset, device. */
+void genie_index_info(const genie_index* ix, uint32_t* num_objects, uint64_t* num_keys,
+                      uint64_t* num_postings, uint32_t* id_offset, int* device);
+
+/* max_multiplicity per dim as held by the device index (65536 entries). */
+int genie_index_dim_stats(genie_index* ix, uint32_t* dim_max_mult, char* err, size_t errlen);
+
+/* Query-side ------------------------------------------------------------- */
+
+/* mcx::execute_batch (engine.hpp:184-304) with host buffers.
+ * Queries (mcx::Query, model.hpp:91-102): query q has items
+ * [item_off[q], item_off[q+1]) with dims / inclusive [lo, hi] ranges, asks
+ * for k[q] >= 1 results and reports query_id qid[q].
+ * Output row q (stride out_stride >= max k) receives out_len[q] entries in
+ * (count desc, id asc) order and out_threshold[q] (TopKResult, cpq.hpp:43-47).
+ * out_bound (optional, Q) receives max_count_bound per query.
+ * Errors: k == 0, empty query, lo > hi -> CONTRACT ("Query N: ..."), bound >
+ * 0xffff -> CONTRACT "query N (setup): ...", table overflow never surfaces
+ * (exact fallback), CUDA failures -> CUDA. */
+int genie_query_batch(genie_index* ix, const genie_config* cfg, uint32_t num_queries,
+                      const uint32_t* qid, const uint32_t* k, const uint64_t* item_off,
+                      const uint16_t* item_dim, const uint32_t* item_lo, const uint32_t* item_hi,
+                      uint32_t out_stride, genie_entry* out, uint32_t* out_len,
+                      uint32_t* out_threshold, uint64_t* out_bound, genie_stage_ns* timings,
+                      genie_batch_stats* stats, char* err, size_t errlen);
+
+/* Device-resident variant: every array is a device pointer on the index's
+ * device; work is enqueued on `stream` (a cudaStream_t, NULL = the handle's
+ * stream) and the call returns without synchronising.  Validation and
+ * counter-range checks happen on the device; call genie_query_status() after
+ * synchronising to surface them.  out_len/out_threshold/out_bound are device
+ * arrays.  No host<->device copies are issued. */
+int genie_query_batch_device(genie_index* ix, const genie_config* cfg, uint32_t num_queries,
+                             const uint32_t* d_qid, const uint32_t* d_k,
+                             const uint64_t* d_item_off, const uint16_t* d_item_dim,
+                             const uint32_t* d_item_lo, const uint32_t* d_item_hi,
+                             uint32_t max_k, uint32_t total_items, uint32_t out_stride,
+                             genie_entry* d_out, uint32_t* d_out_len, uint32_t* d_out_threshold,
+                             void* stream, char* err, size_t errlen);
+
+/* Status of the last genie_query_batch_device call (synchronises the
+ * handle's stream).  Fills stats if non-NULL. */
+int genie_query_status(genie_index* ix, genie_batch_stats* stats, char* err, size_t errlen);
+
+/* Kernels launched by the last batch (for launch accounting). */
+uint32_t genie_last_launch_count(const genie_index* ix);
+
+/* mcx::merge_topk (engine.hpp:158-177) over device-resident candidate lists,
+ * batched over queries: list l of query q is d_in[(q*L + l)*in_stride ...]
+ * with d_in_len[q*L + l] valid entries, each list ordered by (count desc, id
+ * asc) and lists holding disjoint ascending id ranges in list order (the
+ * per-GPU top-k of id-range shards).  Output as genie_query_batch_device.
+ * Duplicate ids across lists are a ContractError (reported by
+ * genie_query_status). */
+int genie_merge_topk_device(genie_index* ix, uint32_t num_queries, uint32_t num_lists,
+                            const genie_entry* d_in, const uint32_t* d_in_len, uint32_t in_stride,
+                            const uint32_t* d_k, uint32_t out_stride, genie_entry* d_out,
+                            uint32_t* d_out_len, uint32_t* d_out_threshold, void* stream,
+                            char* err, size_t errlen);
+
+/* Host variant of the batched merge (runs on `device`). */
+int genie_merge_topk(int device, uint32_t num_queries, uint32_t num_lists, const genie_entry* in,
+                     const uint32_t* in_len, uint32_t in_stride, const uint32_t* k,
+                     uint32_t out_stride, genie_entry* out, uint32_t* out_len,
+                     uint32_t* out_threshold, char* err, size_t errlen);
+
+/* hash_results (engine.hpp:141-153): the byte-exact parity digest (host). */
+uint64_t genie_hash_results(uint32_t num_queries, const uint32_t* qid, const uint32_t* threshold,
+                            const uint32_t* len, uint32_t stride, const genie_entry* entries);
+
+/* LSH / minHash transforms ------------------------------------------------- */
+
+/* mcx::LshFamily (lsh.hpp:130) plus minHash (new). */
+typedef enum { GENIE_LSH_PSTABLE = 0, GENIE_LSH_RBH = 1, GENIE_LSH_MINHASH = 2 } genie_lsh_family;
+
+/* mcx::LshEncoderConfig (lsh.hpp:132-145). */
+typedef struct {
+    uint32_t family; /* genie_lsh_family */
+    uint32_t m;      /* hash functions == keyword dims */
+    uint32_t dims;   /* point dimensionality (unused for minHash) */
+    uint32_t rehash_domain;
+    uint64_t seed;
+    double w;
+    uint32_t bucket_count;
+    int32_t rehash_pstable;
+    int64_t bucket_min;
+    double sigma;
+} genie_lsh_config;
+
+genie_lsh_config genie_lsh_config_default(void);
+
+/* Host-side parameter sampling exactly as LshEncoder::create (lsh.hpp:151-166).
+ * p-stable: a[m*dims], b[m]; RBH: a = pitch[m*dims], b = shift[m*dims];
+ * minHash: hash_seed[m] (a, b unused).  rehash_seed[m] always. */
+int genie_lsh_sample(const genie_lsh_config* cfg, double* a, double* b, uint64_t* hash_seed,
+                     uint64_t* rehash_seed, char* err, size_t errlen);
+
+typedef struct genie_encoder genie_encoder;
+
+/* Samples parameters on the host and uploads them to `device`. */
+int genie_encoder_create(const genie_lsh_config* cfg, int device, genie_encoder** out, char* err,
+                         size_t errlen);
+void genie_encoder_destroy(genie_encoder* enc);
+
+/* LshEncoder::encode_point / encode_query_point (lsh.hpp:176-195), batched:
+ * tokens[n_points * m], token of function i for point p at [p*m + i]
+ * (Keyword{dim=i, token}).  Host buffers.  fp64 with IEEE mul/add/div in the
+ * reference order (no contraction): bit-exact with the reference. */
+int genie_lsh_encode(genie_encoder* enc, const float* points, uint64_t n_points,
+                     uint32_t* tokens, char* err, size_t errlen);
+int genie_lsh_encode_device(genie_encoder* enc, const float* d_points, uint64_t n_points,
+                            uint32_t* d_tokens, void* stream, char* err, size_t errlen);
+
+/* minHash over sets of u64 elements: set s = elems[set_off[s], set_off[s+1]). */
+int genie_minhash_encode(genie_encoder* enc, const uint64_t* set_off, const uint64_t* elems,
+                         uint64_t n_sets, uint32_t* tokens, char* err, size_t errlen);
+int genie_minhash_encode_device(genie_encoder* enc, const uint64_t* d_set_off,
+                                const uint64_t* d_elems, uint64_t n_sets, uint32_t* d_tokens,
+                                void* stream, char* err, size_t errlen);
+
+/* Builds a device index directly from device tokens (n_points x m, dim = function
+ * index): the GPU counterpart of encode_dataset + build_index for LSH data.
+ * Postings per key are ascending ids (stable counting sort). */
+int genie_index_from_tokens_device(const uint32_t* d_tokens, uint32_t n_points, uint32_t m,
+                                   uint32_t token_domain, uint32_t id_offset, int device,
+                                   genie_index** out, char* err, size_t errlen);
+
+/* Copies the device CSR back (for parity checks): keys[K], key_off[K+1], postings[P]. */
+int genie_index_export(genie_index* ix, uint64_t* keys, uint64_t* key_off, uint32_t* postings,
+                       char* err, size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GENIE_GENIE_H */

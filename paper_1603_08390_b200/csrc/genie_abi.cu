@@ -1,0 +1,282 @@
+// Host-side C-ABI entry points of the query path (include/genie/genie.h):
+// validation with the reference's messages, staging, launch, readback.
+#include <algorithm>
+#include <chrono>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace genie {
+void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
+                       const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
+                       uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
+                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s);
+
+// engine.hpp:186-188 and model.hpp:80-85, 97-101: the reference raises these
+// before any work happens.
+static void validate_config(const genie_config& c) {
+    if (c.span_chunk == 0 || c.max_spans_per_task == 0)
+        throw Error(GENIE_ERR_CONTRACT, "span_chunk and max_spans_per_task must be positive");
+    if (c.selector > GENIE_SELECT_SORT) throw Error(GENIE_ERR_CONTRACT, "unknown selector");
+}
+
+static void validate_queries(uint32_t Q, const uint32_t* qid, const uint32_t* k,
+                             const uint64_t* item_off, const uint16_t* dim, const uint32_t* lo,
+                             const uint32_t* hi) {
+    if (Q >= (1u << 21)) throw Error(GENIE_ERR_CONTRACT, "batch exceeds 2^21 queries");
+    for (uint32_t q = 0; q < Q; ++q) {
+        if (item_off[q + 1] < item_off[q]) throw Error(GENIE_ERR_CONTRACT, "item_off must be non-decreasing");
+        for (uint64_t i = item_off[q]; i < item_off[q + 1]; ++i)
+            if (lo[i] > hi[i])
+                throw Error(GENIE_ERR_CONTRACT, "QueryItem: lo " + std::to_string(lo[i]) + " > hi " +
+                                                    std::to_string(hi[i]) + " on dim " +
+                                                    std::to_string(dim[i]));
+        if (item_off[q + 1] == item_off[q])
+            throw Error(GENIE_ERR_CONTRACT, "Query " + std::to_string(qid[q]) + ": no items");
+        if (k[q] == 0) throw Error(GENIE_ERR_CONTRACT, "Query " + std::to_string(qid[q]) + ": k must be >= 1");
+    }
+}
+
+template <typename T>
+static void h2d(DevBuf<T>& b, const T* src, size_t n, cudaStream_t s) {
+    b.reserve(n);
+    if (n) GENIE_CUDA(cudaMemcpyAsync(b.p, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+// Reference accounting of MemoryStats (engine.hpp:239-241; cpq.hpp:103-106,
+// 243, 283, 359-362), from the per-query bounds.
+static void memory_stats(uint32_t n, uint32_t Q, const uint32_t* k, const uint64_t* bounds,
+                         genie_batch_stats* st) {
+    st->counter_bytes = st->gate_bytes = st->table_bytes = 0;
+    for (uint32_t q = 0; q < Q; ++q) {
+        const uint64_t b = std::max<uint64_t>(bounds[q], 1);
+        const uint64_t w = width_for(b);
+        st->counter_bytes += (uint64_t(n) * w + 7) / 8;
+        st->gate_bytes += (b + 1) * 4 + 4;
+        st->table_bytes += 8 * bit_ceil64(std::max<uint64_t>(2ull * k[q] * b, 2));
+    }
+}
+
+}  // namespace genie
+
+using namespace genie;
+
+extern "C" {
+
+int genie_query_batch(genie_index* ix, const genie_config* cfg_in, uint32_t Q, const uint32_t* qid,
+                      const uint32_t* k, const uint64_t* item_off, const uint16_t* item_dim,
+                      const uint32_t* item_lo, const uint32_t* item_hi, uint32_t out_stride,
+                      genie_entry* out, uint32_t* out_len, uint32_t* out_threshold,
+                      uint64_t* out_bound, genie_stage_ns* timings, genie_batch_stats* stats,
+                      char* err, size_t errlen) {
+    return guarded(err, errlen, [&]() -> int {
+        const auto t0 = std::chrono::steady_clock::now();
+        const genie_config cfg = cfg_in ? *cfg_in : genie_config_default();
+        validate_config(cfg);
+        if (!ix) throw Error(GENIE_ERR_CONTRACT, "null index");
+        if (Q && (!qid || !k || !item_off || !out || !out_len || !out_threshold))
+            throw Error(GENIE_ERR_CONTRACT, "genie_query_batch: null argument");
+        validate_queries(Q, qid, k, item_off, item_dim, item_lo, item_hi);
+        uint32_t max_k = 0;
+        for (uint32_t q = 0; q < Q; ++q) max_k = std::max(max_k, k[q]);
+        if (Q && out_stride < max_k)
+            throw Error(GENIE_ERR_CONTRACT, "out_stride must be >= the largest k");
+        ensure_device(ix->device);
+        Workspace& w = ix->ws;
+        cudaStream_t s = ix->stream;
+        const uint64_t items = Q ? item_off[Q] - item_off[0] : 0;
+        if (items >= (1ull << 32)) throw Error(GENIE_ERR_CONTRACT, "too many query items");
+        std::vector<uint64_t> off_rebased;
+        const uint64_t* offs = item_off;
+        if (Q && item_off[0] != 0) {
+            off_rebased.assign(item_off, item_off + Q + 1);
+            for (auto& o : off_rebased) o -= item_off[0];
+            offs = off_rebased.data();
+        }
+        const uint64_t i0 = Q ? item_off[0] : 0;
+        int rc = GENIE_RETRY;
+        std::string msg;
+        genie_batch_stats local_stats{};
+        for (int attempt = 0; attempt < 4 && rc == GENIE_RETRY; ++attempt) {
+            h2d(w.d_qid, qid, Q, s);
+            h2d(w.d_k, k, Q, s);
+            h2d(w.d_item_off, offs, Q + 1, s);
+            h2d(w.d_dim, item_dim + i0, items, s);
+            h2d(w.d_lo, item_lo + i0, items, s);
+            h2d(w.d_hi, item_hi + i0, items, s);
+            w.d_out.reserve(uint64_t(Q) * std::max<uint32_t>(out_stride, 1));
+            w.d_out_len.reserve(Q + 1);
+            w.d_out_thr.reserve(Q + 1);
+            launch_batch(ix, cfg, Q, w.d_qid.p, w.d_k.p, w.d_item_off.p, w.d_dim.p, w.d_lo.p,
+                         w.d_hi.p, static_cast<uint32_t>(items), max_k, std::max<uint32_t>(out_stride, 1),
+                         w.d_out.p, w.d_out_len.p, w.d_out_thr.p, s, timings != nullptr);
+            rc = finish_batch(ix, &local_stats, msg, qid);
+        }
+        if (rc != GENIE_OK) throw Error(rc, msg);
+        if (Q) {
+            if (out_stride) {
+                GENIE_CUDA(cudaMemcpyAsync(out, w.d_out.p, uint64_t(Q) * out_stride * sizeof(genie_entry),
+                                           cudaMemcpyDeviceToHost, s));
+            }
+            GENIE_CUDA(cudaMemcpyAsync(out_len, w.d_out_len.p, Q * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            GENIE_CUDA(cudaMemcpyAsync(out_threshold, w.d_out_thr.p, Q * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToHost, s));
+        }
+        std::vector<uint64_t> bounds(Q);
+        if (Q && (out_bound || stats))
+            GENIE_CUDA(cudaMemcpyAsync(bounds.data(), w.q_bound.p, Q * sizeof(uint64_t),
+                                       cudaMemcpyDeviceToHost, s));
+        GENIE_CUDA(cudaStreamSynchronize(s));
+        if (out_bound) std::copy(bounds.begin(), bounds.end(), out_bound);
+        if (stats) {
+            *stats = local_stats;
+            memory_stats(ix->n, Q, k, bounds.data(), stats);
+        }
+        if (timings) {
+            float ms_lookup = 0, ms_match = 0, ms_merge = 0;
+            cudaEventElapsedTime(&ms_lookup, ix->ev[0], ix->ev[1]);
+            cudaEventElapsedTime(&ms_match, ix->ev[1], ix->ev[2]);
+            cudaEventElapsedTime(&ms_merge, ix->ev[2], ix->ev[3]);
+            timings->lookup_ns = static_cast<uint64_t>(ms_lookup * 1e6);
+            timings->match_ns = static_cast<uint64_t>(ms_match * 1e6);
+            timings->select_ns = 0;  // fused into the match kernel (per-tile c-PQ extract)
+            timings->merge_ns = static_cast<uint64_t>(ms_merge * 1e6);
+            const auto t1 = std::chrono::steady_clock::now();
+            timings->total_ns = static_cast<uint64_t>(
+                std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+            const uint64_t sum = timings->lookup_ns + timings->match_ns + timings->merge_ns;
+            if (sum > timings->total_ns) timings->total_ns = sum;
+        }
+        return GENIE_OK;
+    });
+}
+
+int genie_query_batch_device(genie_index* ix, const genie_config* cfg_in, uint32_t Q,
+                             const uint32_t* d_qid, const uint32_t* d_k, const uint64_t* d_item_off,
+                             const uint16_t* d_item_dim, const uint32_t* d_item_lo,
+                             const uint32_t* d_item_hi, uint32_t max_k, uint32_t total_items,
+                             uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
+                             uint32_t* d_out_threshold, void* stream, char* err, size_t errlen) {
+    return guarded(err, errlen, [&]() -> int {
+        const genie_config cfg = cfg_in ? *cfg_in : genie_config_default();
+        validate_config(cfg);
+        if (!ix) throw Error(GENIE_ERR_CONTRACT, "null index");
+        if (Q >= (1u << 21)) throw Error(GENIE_ERR_CONTRACT, "batch exceeds 2^21 queries");
+        if (Q && out_stride < max_k) throw Error(GENIE_ERR_CONTRACT, "out_stride must be >= max_k");
+        ensure_device(ix->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix->stream;
+        launch_batch(ix, cfg, Q, d_qid, d_k, d_item_off, d_item_dim, d_item_lo, d_item_hi, total_items,
+                     max_k, std::max<uint32_t>(out_stride, 1), d_out, d_out_len, d_out_threshold, s,
+                     false);
+        if (s != ix->stream) {
+            // make genie_query_status's synchronisation cover the caller's stream
+            cudaEvent_t e = ix->ev[4];
+            GENIE_CUDA(cudaEventRecord(e, s));
+            GENIE_CUDA(cudaStreamWaitEvent(ix->stream, e, 0));
+        }
+        return GENIE_OK;
+    });
+}
+
+int genie_query_status(genie_index* ix, genie_batch_stats* stats, char* err, size_t errlen) {
+    return guarded(err, errlen, [&]() -> int {
+        ensure_device(ix->device);
+        std::string msg;
+        const int rc = finish_batch(ix, stats, msg, nullptr);
+        if (rc != GENIE_OK) throw Error(rc, msg);
+        return GENIE_OK;
+    });
+}
+
+uint32_t genie_last_launch_count(const genie_index* ix) { return ix ? ix->last_launches : 0; }
+
+int genie_merge_topk_device(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
+                            const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
+                            uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
+                            uint32_t* d_out_threshold, void* stream, char* err, size_t errlen) {
+    return guarded(err, errlen, [&]() -> int {
+        if (!ix) throw Error(GENIE_ERR_CONTRACT, "null index");
+        ensure_device(ix->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix->stream;
+        // max_k is unknown on the host here; rows are bounded by L * in_stride
+        const uint32_t max_rows = std::min<uint32_t>(out_stride, L * in_stride);
+        launch_list_merge(ix, Q, L, d_in, d_in_len, in_stride, d_k, out_stride, d_out, d_out_len,
+                          d_out_threshold, max_rows, s);
+        if (s != ix->stream) {
+            GENIE_CUDA(cudaEventRecord(ix->ev[4], s));
+            GENIE_CUDA(cudaStreamWaitEvent(ix->stream, ix->ev[4], 0));
+        }
+        return GENIE_OK;
+    });
+}
+
+int genie_merge_topk(int device, uint32_t Q, uint32_t L, const genie_entry* in, const uint32_t* in_len,
+                     uint32_t in_stride, const uint32_t* k, uint32_t out_stride, genie_entry* out,
+                     uint32_t* out_len, uint32_t* out_threshold, char* err, size_t errlen) {
+    return guarded(err, errlen, [&]() -> int {
+        ensure_device(device);
+        uint32_t max_k = 0;
+        for (uint32_t q = 0; q < Q; ++q) {
+            if (k[q] == 0) throw Error(GENIE_ERR_CONTRACT, "merge_topk: k must be >= 1");
+            max_k = std::max(max_k, k[q]);
+        }
+        if (Q && out_stride < std::min<uint64_t>(max_k, uint64_t(L) * in_stride))
+            throw Error(GENIE_ERR_CONTRACT, "out_stride too small");
+        for (uint64_t i = 0; i < uint64_t(Q) * L; ++i)
+            if (in_len[i] > in_stride) throw Error(GENIE_ERR_CONTRACT, "list longer than in_stride");
+        // a transient handle carries the stream and workspace
+        genie_index tmp;
+        tmp.device = device;
+        tmp.sms = sm_count(device);
+        GENIE_CUDA(cudaStreamCreateWithFlags(&tmp.stream, cudaStreamNonBlocking));
+        struct Guard {
+            genie_index& t;
+            ~Guard() {
+                if (t.ws.h_status) cudaFreeHost(t.ws.h_status);
+                t.ws.h_status = nullptr;
+                cudaStreamDestroy(t.stream);
+                t.stream = nullptr;
+            }
+        } guard{tmp};
+        DevBuf<genie_entry> d_in, d_out;
+        DevBuf<uint32_t> d_len, d_k, d_olen, d_othr;
+        h2d(d_in, in, uint64_t(Q) * L * in_stride, tmp.stream);
+        h2d(d_len, in_len, uint64_t(Q) * L, tmp.stream);
+        h2d(d_k, k, Q, tmp.stream);
+        const uint32_t stride = std::max<uint32_t>(out_stride, 1);
+        d_out.reserve(uint64_t(Q) * stride);
+        d_olen.reserve(Q + 1);
+        d_othr.reserve(Q + 1);
+        launch_list_merge(&tmp, Q, L, d_in.p, d_len.p, in_stride, d_k.p, stride, d_out.p, d_olen.p,
+                          d_othr.p, max_k, tmp.stream);
+        std::string msg;
+        const int rc = finish_batch(&tmp, nullptr, msg, nullptr);
+        if (rc != GENIE_OK) throw Error(rc, msg);
+        if (Q) {
+            GENIE_CUDA(cudaMemcpy(out, d_out.p, uint64_t(Q) * stride * sizeof(genie_entry),
+                                  cudaMemcpyDeviceToHost));
+            GENIE_CUDA(cudaMemcpy(out_len, d_olen.p, Q * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            GENIE_CUDA(cudaMemcpy(out_threshold, d_othr.p, Q * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        }
+        return GENIE_OK;
+    });
+}
+
+// engine.hpp:141-153
+uint64_t genie_hash_results(uint32_t Q, const uint32_t* qid, const uint32_t* thr, const uint32_t* len,
+                            uint32_t stride, const genie_entry* entries) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    auto mix_in = [&h](uint64_t v) { h = mix64(h ^ v); };
+    for (uint32_t q = 0; q < Q; ++q) {
+        mix_in(qid[q]);
+        mix_in(thr[q]);
+        mix_in(len[q]);
+        for (uint32_t e = 0; e < len[q]; ++e) {
+            const genie_entry& x = entries[uint64_t(q) * stride + e];
+            mix_in((uint64_t(x.id) << 32) | x.count);
+        }
+    }
+    return h;
+}
+
+}  // extern "C"

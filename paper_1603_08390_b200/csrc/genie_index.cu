@@ -1,0 +1,237 @@
+// Device inverted index: CSR upload, validation, id-range shards, per-dim
+// statistics, export.  Replaces the product of mcx::build_index
+// (index.hpp:190-250) and the InvertedIndex accessors (index.hpp:41-182).
+#include <algorithm>
+#include <thread>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace genie {
+
+// ---- max_multiplicity per dim (index.hpp:110-113, 153-174) on the device:
+// pass 1 counts the dim's keywords per object, pass 2 takes the max while
+// clearing the scratch (atomicExch), touching only the dim's postings.
+__global__ void k_dim_count(const uint32_t* post, uint64_t b, uint64_t e, uint32_t* cnt) {
+    for (uint64_t i = b + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < e;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        atomicAdd(&cnt[post[i]], 1u);
+}
+
+__global__ void k_dim_max(const uint32_t* post, uint64_t b, uint64_t e, uint32_t* cnt,
+                          uint32_t* out) {
+    uint32_t best = 0;
+    for (uint64_t i = b + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < e;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        best = max(best, atomicExch(&cnt[post[i]], 0u));
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, d));
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
+
+static void compute_dim_stats(genie_index* ix, const uint64_t* h_keys, const uint64_t* h_off) {
+    GENIE_CUDA(cudaMemsetAsync(ix->dim_mult.p, 0, 65536 * sizeof(uint32_t), ix->stream));
+    if (!ix->K || !ix->n) return;
+    DevBuf<uint32_t> scratch;
+    scratch.reserve(ix->n);
+    GENIE_CUDA(cudaMemsetAsync(scratch.p, 0, size_t(ix->n) * sizeof(uint32_t), ix->stream));
+    uint64_t j = 0;
+    while (j < ix->K) {
+        const uint32_t d = static_cast<uint32_t>(h_keys[j] >> 32);
+        uint64_t e = j;
+        while (e < ix->K && static_cast<uint32_t>(h_keys[e] >> 32) == d) ++e;
+        const uint64_t pb = h_off[j], pe = h_off[e];
+        if (pe > pb) {
+            const uint64_t blocks = std::min<uint64_t>((pe - pb + 255) / 256, uint64_t(ix->sms) * 16);
+            k_dim_count<<<static_cast<unsigned>(blocks), 256, 0, ix->stream>>>(ix->postings.p, pb, pe,
+                                                                              scratch.p);
+            k_dim_max<<<static_cast<unsigned>(blocks), 256, 0, ix->stream>>>(ix->postings.p, pb, pe,
+                                                                            scratch.p, ix->dim_mult.p + d);
+        }
+        j = e;
+    }
+    GENIE_CUDA(cudaStreamSynchronize(ix->stream));
+    GENIE_CUDA(cudaGetLastError());
+}
+
+static void validate_csr(uint32_t n, uint64_t K, const uint64_t* keys, const uint64_t* off,
+                         const uint32_t* post) {
+    if (K >= (1ull << 32)) throw Error(GENIE_ERR_DATA, "index: too many keywords");
+    if (off[0] != 0) throw Error(GENIE_ERR_DATA, "index: key_off[0] must be 0");
+    for (uint64_t j = 0; j < K; ++j) {
+        if (j && keys[j] <= keys[j - 1])
+            throw Error(GENIE_ERR_DATA, "index: keywords must be strictly ascending");
+        if ((keys[j] >> 32) > 0xffffu) throw Error(GENIE_ERR_DATA, "index: dim exceeds 16 bits");
+        if (off[j + 1] < off[j]) throw Error(GENIE_ERR_DATA, "index: key_off must be non-decreasing");
+    }
+    const uint64_t P = off[K];
+    // postings: ascending per key, < n (index_io.hpp:136-150 validation rules)
+    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    std::vector<int> bad(T, 0);
+    for (unsigned t = 0; t < T; ++t) {
+        pool.emplace_back([&, t] {
+            for (uint64_t j = t; j < K; j += T) {
+                for (uint64_t p = off[j]; p < off[j + 1]; ++p) {
+                    if (post[p] >= n) { bad[t] = 1; return; }
+                    if (p > off[j] && post[p] <= post[p - 1]) { bad[t] = 2; return; }
+                }
+            }
+        });
+    }
+    for (auto& th : pool) th.join();
+    for (int b : bad) {
+        if (b == 1) throw Error(GENIE_ERR_DATA, "index: object id out of range");
+        if (b == 2) throw Error(GENIE_ERR_DATA, "index: postings must be strictly ascending per keyword");
+    }
+    (void)P;
+}
+
+static genie_index* upload(uint32_t n, uint64_t K, const uint64_t* keys, const uint64_t* off,
+                           const uint32_t* post, const uint32_t* dim_mult, uint32_t id_offset,
+                           int device) {
+    ensure_device(device);
+    auto* ix = new genie_index;
+    try {
+        ix->device = device;
+        ix->n = n;
+        ix->K = K;
+        ix->P = off[K];
+        ix->id_offset = id_offset;
+        ix->sms = sm_count(device);
+        GENIE_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+        for (auto& e : ix->ev) GENIE_CUDA(cudaEventCreate(&e));
+        ix->keys.reserve(K + 1);
+        ix->key_off.reserve(K + 1);
+        // +64 padding: 16-byte tail loads of the scan may read past a list end
+        ix->postings.reserve(ix->P + 64);
+        ix->dim_mult.reserve(65536);
+        if (K) GENIE_CUDA(cudaMemcpy(ix->keys.p, keys, K * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        GENIE_CUDA(cudaMemcpy(ix->key_off.p, off, (K + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        GENIE_CUDA(cudaMemset(ix->postings.p, 0, (ix->P + 64) * sizeof(uint32_t)));
+        if (ix->P)
+            GENIE_CUDA(cudaMemcpy(ix->postings.p, post, ix->P * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        if (dim_mult) {
+            GENIE_CUDA(cudaMemcpy(ix->dim_mult.p, dim_mult, 65536 * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice));
+        } else {
+            compute_dim_stats(ix, keys, off);
+        }
+        GENIE_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+        genie_index_destroy(ix);
+        throw;
+    }
+    return ix;
+}
+
+}  // namespace genie
+
+using namespace genie;
+
+extern "C" {
+
+genie_config genie_config_default(void) {
+    genie_config c{};
+    c.selector = GENIE_SELECT_CPQ;
+    c.span_chunk = kDefaultUnit;
+    c.max_spans_per_task = 2;
+    c.tile_bytes = 0;
+    c.ctas_per_sm = 0;
+    c.flags = 0;
+    return c;
+}
+
+int genie_index_create(uint32_t num_objects, uint64_t num_keys, const uint64_t* keys,
+                       const uint64_t* key_off, const uint32_t* postings,
+                       const uint32_t* dim_max_mult, uint32_t id_offset, int device,
+                       genie_index** out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!out || !key_off || (num_keys && (!keys)))
+            throw Error(GENIE_ERR_CONTRACT, "genie_index_create: null argument");
+        validate_csr(num_objects, num_keys, keys, key_off, postings);
+        *out = upload(num_objects, num_keys, keys, key_off, postings, dim_max_mult, id_offset, device);
+        return GENIE_OK;
+    });
+}
+
+int genie_index_create_shard(uint32_t num_objects, uint64_t num_keys, const uint64_t* keys,
+                             const uint64_t* key_off, const uint32_t* postings, uint32_t id_begin,
+                             uint32_t id_end, int device, genie_index** out, char* err,
+                             size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!out) throw Error(GENIE_ERR_CONTRACT, "genie_index_create_shard: null argument");
+        if (id_begin > id_end || id_end > num_objects)
+            throw Error(GENIE_ERR_CONTRACT, "genie_index_create_shard: bad id range");
+        validate_csr(num_objects, num_keys, keys, key_off, postings);
+        // one part of partition_dataset (index.hpp:263-291): keep ids in
+        // [id_begin, id_end), rebase, drop keywords absent from the part
+        std::vector<uint64_t> sb(num_keys), se(num_keys);
+        for (uint64_t j = 0; j < num_keys; ++j) {
+            const uint32_t* a = postings + key_off[j];
+            const uint32_t* b = postings + key_off[j + 1];
+            sb[j] = std::lower_bound(a, b, id_begin) - postings;
+            se[j] = std::lower_bound(a, b, id_end) - postings;
+        }
+        std::vector<uint64_t> k2, o2{0};
+        for (uint64_t j = 0; j < num_keys; ++j)
+            if (se[j] > sb[j]) {
+                k2.push_back(keys[j]);
+                o2.push_back(o2.back() + (se[j] - sb[j]));
+            }
+        std::vector<uint32_t> p2(o2.back());
+        uint64_t w = 0;
+        for (uint64_t j = 0; j < num_keys; ++j)
+            for (uint64_t p = sb[j]; p < se[j]; ++p) p2[w++] = postings[p] - id_begin;
+        *out = upload(id_end - id_begin, k2.size(), k2.data(), o2.data(), p2.data(), nullptr, id_begin,
+                      device);
+        return GENIE_OK;
+    });
+}
+
+void genie_index_destroy(genie_index* ix) {
+    if (!ix) return;
+    cudaSetDevice(ix->device);
+    if (ix->stream) cudaStreamSynchronize(ix->stream);
+    if (ix->ws.h_status) cudaFreeHost(ix->ws.h_status);
+    for (auto& e : ix->ev)
+        if (e) cudaEventDestroy(e);
+    if (ix->stream) cudaStreamDestroy(ix->stream);
+    delete ix;
+}
+
+void genie_index_info(const genie_index* ix, uint32_t* num_objects, uint64_t* num_keys,
+                      uint64_t* num_postings, uint32_t* id_offset, int* device) {
+    if (num_objects) *num_objects = ix->n;
+    if (num_keys) *num_keys = ix->K;
+    if (num_postings) *num_postings = ix->P;
+    if (id_offset) *id_offset = ix->id_offset;
+    if (device) *device = ix->device;
+}
+
+int genie_index_dim_stats(genie_index* ix, uint32_t* dim_max_mult, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        ensure_device(ix->device);
+        GENIE_CUDA(cudaMemcpy(dim_max_mult, ix->dim_mult.p, 65536 * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost));
+        return GENIE_OK;
+    });
+}
+
+int genie_index_export(genie_index* ix, uint64_t* keys, uint64_t* key_off, uint32_t* postings,
+                       char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        ensure_device(ix->device);
+        if (ix->K && keys)
+            GENIE_CUDA(cudaMemcpy(keys, ix->keys.p, ix->K * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        if (key_off)
+            GENIE_CUDA(cudaMemcpy(key_off, ix->key_off.p, (ix->K + 1) * sizeof(uint64_t),
+                                  cudaMemcpyDeviceToHost));
+        if (ix->P && postings)
+            GENIE_CUDA(cudaMemcpy(postings, ix->postings.p, ix->P * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost));
+        return GENIE_OK;
+    });
+}
+
+}  // extern "C"

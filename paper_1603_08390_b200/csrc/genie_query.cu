@@ -1,0 +1,1458 @@
+// Batched match-count query pipeline for B200 (sm_100a).
+//
+// Replaces mcx::execute_batch (engine.hpp:184-304) with Selector::cpq:
+//
+//   k_resolve   lookup_into + max_count_bound per query (index.hpp:86-133),
+//               one warp per query, binary search over the packed keys.
+//   k_plan      per-query prefix sums, counter width W = width_for(bound)
+//               (cpq.hpp:63-68) and the object-tile decomposition.
+//   k_worklist  tile-major (query, object tile) work list.
+//   k_cut       per (query, span): positions of the object-tile boundaries
+//               inside the ascending posting list (long lists are thereby
+//               split into tile-aligned sub-lists).
+//   k_scan      persistent CTAs over (query, tile) items: packed 4/8/16-bit
+//               counters for the tile's objects live in shared memory
+//               (BitmapCounter, cpq.hpp:53-120); 128-bit streaming posting
+//               loads; every increment returns the new count, which feeds
+//               the Count Priority Queue gate (ZipperArray + AuditThreshold,
+//               cpq.hpp:294-301, 374-389) and the lock-free modified Robin
+//               Hood table in shared memory (cpq.hpp:149-204).  At the end
+//               of the item the CTA extracts the tile's exact top-k
+//               (cpq.hpp:307-339: entries above AT-1 from the table, ties at
+//               AT-1 by ascending id from the counters).
+//   k_merge     per query: merge_topk over its tiles (engine.hpp:158-177);
+//               exact by the partition lemma that makes execute_partitioned
+//               equal execute_batch.
+//
+// Counters never touch HBM; every posting id of every matched span is read
+// exactly once per query (the algorithmic traffic).
+#include <cub/device/device_segmented_radix_sort.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <vector>
+
+#include "block.cuh"
+#include "internal.cuh"
+
+namespace genie {
+
+// ------------------------------------------------------------------ params
+
+struct BatchParams {
+    // index
+    const uint64_t* keys;
+    const uint64_t* key_off;
+    const uint32_t* postings;
+    const uint32_t* dim_mult;
+    uint64_t K;
+    uint32_t n;
+    uint32_t id_offset;
+    // queries
+    uint32_t Q;
+    const uint32_t* k;
+    const uint64_t* item_off;
+    const uint16_t* dim;
+    const uint32_t* lo;
+    const uint32_t* hi;
+    // plan
+    uint32_t tile_bits;
+    uint32_t unit;
+    uint32_t selector;
+    // workspace
+    uint64_t *q_bound, *q_P, *q_span_base, *q_cut_base, *q_out_base;
+    uint32_t *q_S, *q_W, *q_ntiles, *q_cap, *q_tile_base, *q_rank, *q_big;
+    uint32_t *it_kb, *it_nk, *it_sbase;
+    uint64_t* span_beg;
+    uint32_t* cuts;
+    uint32_t *work_q, *work_t;
+    uint32_t* tile_len;
+    genie_entry* tile_out;
+    unsigned long long* st;
+    uint64_t cap_spans, cap_cuts, cap_work, cap_tout;
+    // output
+    uint32_t out_stride;
+    genie_entry* out;
+    uint32_t* out_len;
+    uint32_t* out_thr;
+};
+
+__device__ __forceinline__ uint32_t wclass(uint32_t W) { return W == 4 ? 0 : (W == 8 ? 1 : 2); }
+
+__device__ __forceinline__ uint32_t ntiles_for(uint32_t n, uint32_t tile_bits, uint32_t W) {
+    const uint32_t T = tile_bits / W;
+    return (n + T - 1) / T;
+}
+
+// ------------------------------------------------------------------ init
+
+__global__ void k_init_status(unsigned long long* st) {
+    const int i = threadIdx.x;
+    if (i < ST_WORDS) {
+        st[i] = (i == ST_BAD_INPUT || i == ST_BAD_BOUND || i == ST_MERGE_DUP) ? ~0ull : 0ull;
+    }
+}
+
+// ---------------------------------------------------------------- resolve
+
+// One warp per query: items -> keyword ranges (lookup_into, index.hpp:86-96),
+// span counts, postings P_q and max_count_bound (index.hpp:118-133).
+__global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
+    const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= p.Q) return;
+    const uint64_t i0 = p.item_off[q], i1 = p.item_off[q + 1];
+    const uint32_t kq = p.k[q];
+    uint32_t bad = 0;
+    bool lohi_bad = false;
+    uint64_t bound = 0, P = 0;
+    uint32_t carry = 0;
+    for (uint64_t base = i0; base < i1; base += 32) {
+        const uint64_t i = base + lane;
+        uint32_t nk = 0, kb = 0, b = 0;
+        uint64_t pp = 0;
+        if (i < i1) {
+            const uint32_t d = p.dim[i], l = p.lo[i], h = p.hi[i];
+            if (l > h) {
+                lohi_bad = true;
+            } else {
+                const uint64_t a = lower_bound_dev(p.keys, p.K, (uint64_t(d) << 32) | l);
+                const uint64_t e = upper_bound_dev(p.keys, p.K, (uint64_t(d) << 32) | h);
+                kb = static_cast<uint32_t>(a);
+                nk = static_cast<uint32_t>(e - a);
+                pp = p.key_off[e] - p.key_off[a];
+                b = min(nk, p.dim_mult[d]);
+            }
+        }
+        const uint32_t incl = warp_inclusive_scan(nk);
+        if (i < i1) {
+            p.it_kb[i] = kb;
+            p.it_nk[i] = nk;
+            p.it_sbase[i] = carry + incl - nk;
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+        bound += warp_sum(static_cast<uint64_t>(b));
+        P += warp_sum(pp);
+    }
+    lohi_bad = __any_sync(0xffffffffu, lohi_bad);
+    if (lane != 0) return;
+    if (lohi_bad) bad = 3;
+    else if (i1 <= i0) bad = 1;
+    else if (kq == 0) bad = 2;
+    uint32_t W = 0, nt = 0;
+    if (bad) {
+        atomicMin(&p.st[ST_BAD_INPUT], (static_cast<unsigned long long>(q) << 8) | bad);
+    } else {
+        const uint64_t bnd = bound < 1 ? 1 : bound;  // engine.hpp:228
+        if (bnd > 0xffffu) {                          // engine.hpp:230-233
+            atomicMin(&p.st[ST_BAD_BOUND], static_cast<unsigned long long>(q));
+        } else {
+            W = width_for(bnd);
+            nt = (P == 0 || p.n == 0) ? 0 : ntiles_for(p.n, p.tile_bits, W);
+        }
+    }
+    p.q_bound[q] = bound;
+    p.q_S[q] = carry;
+    p.q_P[q] = P;
+    p.q_W[q] = W;
+    p.q_ntiles[q] = nt;
+    if (nt) atomicAdd(&p.st[ST_TOTAL_POSTINGS], static_cast<unsigned long long>(P));
+}
+
+// ------------------------------------------------------------------- plan
+
+// Single CTA: exclusive prefix sums over queries and the width classes.
+__global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
+    __shared__ unsigned long long sums[32];
+    unsigned long long c_span = 0, c_cut = 0, c_tile = 0, c_out = 0, c_cls = 0;
+    uint32_t max_nt = 0;
+    for (uint32_t base = 0; base < p.Q; base += blockDim.x) {
+        const uint32_t q = base + threadIdx.x;
+        unsigned long long v_span = 0, v_cut = 0, v_tile = 0, v_out = 0, v_cls = 0;
+        uint32_t cap = 0, W = 0, nt = 0;
+        if (q < p.Q) {
+            nt = p.q_ntiles[q];
+            W = p.q_W[q];
+            if (nt) {
+                const uint32_t T = p.tile_bits / W;
+                const uint32_t kq = p.k[q];
+                cap = min(kq, T);
+                v_span = p.q_S[q];
+                v_cut = static_cast<unsigned long long>(p.q_S[q]) * (nt + 1);
+                v_tile = nt;
+                v_out = static_cast<unsigned long long>(nt) * cap;
+                v_cls = 1ull << (21 * wclass(W));
+            }
+            max_nt = max(max_nt, nt);
+        }
+        unsigned long long t_span, t_cut, t_tile, t_out, t_cls;
+        const unsigned long long e_span = block_exclusive_scan(v_span, sums, t_span);
+        const unsigned long long e_cut = block_exclusive_scan(v_cut, sums, t_cut);
+        const unsigned long long e_tile = block_exclusive_scan(v_tile, sums, t_tile);
+        const unsigned long long e_out = block_exclusive_scan(v_out, sums, t_out);
+        const unsigned long long e_cls = block_exclusive_scan(v_cls, sums, t_cls);
+        if (q < p.Q) {
+            p.q_span_base[q] = c_span + e_span;
+            p.q_cut_base[q] = c_cut + e_cut;
+            p.q_tile_base[q] = static_cast<uint32_t>(c_tile + e_tile);
+            p.q_out_base[q] = c_out + e_out;
+            p.q_cap[q] = cap;
+            const unsigned long long r = c_cls + e_cls;
+            p.q_rank[q] = nt ? static_cast<uint32_t>((r >> (21 * wclass(W))) & 0x1fffffull) : 0;
+        }
+        c_span += t_span;
+        c_cut += t_cut;
+        c_tile += t_tile;
+        c_out += t_out;
+        c_cls += t_cls;
+    }
+    if (threadIdx.x == 0) {
+        p.st[ST_TOTAL_SPANS] = c_span;
+        p.st[ST_TOTAL_CUTS] = c_cut;
+        p.st[ST_TOTAL_WORK] = c_tile;
+        p.st[ST_TOTAL_TOUT] = c_out;
+        p.st[ST_CLASS0] = c_cls & 0x1fffffull;
+        p.st[ST_CLASS1] = (c_cls >> 21) & 0x1fffffull;
+        p.st[ST_CLASS2] = (c_cls >> 42) & 0x1fffffull;
+        if (c_span > p.cap_spans || c_cut > p.cap_cuts || c_tile > p.cap_work ||
+            c_out > p.cap_tout)
+            p.st[ST_OVERFLOW] = 1;
+    }
+}
+
+// --------------------------------------------------------------- worklist
+
+// Tile-major order: all queries' tile 0, then tile 1, ...  Within a tile the
+// width classes follow each other and queries keep request order.  Items of
+// the same tile read the same slice of every hot list, so the hot slice of
+// the index stays L2-resident while the batch sweeps it.
+__global__ void k_worklist(BatchParams p) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= p.Q || p.st[ST_OVERFLOW]) return;
+    const uint32_t nt = p.q_ntiles[q];
+    if (!nt) return;
+    const uint32_t c = wclass(p.q_W[q]);
+    uint64_t cnt[3], ntc[3];
+    for (int i = 0; i < 3; ++i) {
+        cnt[i] = p.st[ST_CLASS0 + i];
+        ntc[i] = p.n ? ntiles_for(p.n, p.tile_bits, 4u << i) : 0;
+    }
+    const uint32_t rank = p.q_rank[q];
+    for (uint32_t t = 0; t < nt; ++t) {
+        uint64_t item = rank;
+        for (int i = 0; i < 3; ++i) {
+            item += cnt[i] * (uint64_t(t) < ntc[i] ? uint64_t(t) : ntc[i]);
+            if (i < static_cast<int>(c) && ntc[i] > t) item += cnt[i];
+        }
+        p.work_q[item] = q;
+        p.work_t[item] = t;
+    }
+}
+
+// -------------------------------------------------------------------- cut
+
+// One warp per (query, span): the span's list and the positions of every
+// object-tile boundary inside it (lower_bound on the ascending ids).
+__global__ void __launch_bounds__(256) k_cut(BatchParams p) {
+    if (p.st[ST_OVERFLOW]) return;
+    const uint64_t total = p.st[ST_TOTAL_SPANS];
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t g = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < total;
+         g += nwarps) {
+        // query owning global span g (last q with span_base <= g)
+        const uint32_t q = static_cast<uint32_t>(upper_bound_dev(p.q_span_base, p.Q, g) - 1);
+        const uint32_t s = static_cast<uint32_t>(g - p.q_span_base[q]);
+        const uint64_t i0 = p.item_off[q], i1 = p.item_off[q + 1];
+        const uint64_t it = i0 + upper_bound_dev(p.it_sbase + i0, i1 - i0, s) - 1;
+        const uint64_t j = p.it_kb[it] + (s - p.it_sbase[it]);
+        const uint64_t beg = p.key_off[j];
+        const uint32_t len = static_cast<uint32_t>(p.key_off[j + 1] - beg);
+        if (lane == 0) p.span_beg[g] = beg;
+        const uint32_t nt = p.q_ntiles[q];
+        const uint32_t T = p.tile_bits / p.q_W[q];
+        uint32_t* cut = p.cuts + p.q_cut_base[q] + uint64_t(s) * (nt + 1);
+        const uint32_t* list = p.postings + beg;
+        for (uint32_t b = lane; b <= nt; b += 32) {
+            uint32_t v;
+            if (b == 0) v = 0;
+            else if (b == nt) v = len;
+            else v = static_cast<uint32_t>(lower_bound_dev(list, len, b * T));
+            cut[b] = v;
+        }
+    }
+}
+
+// ------------------------------------------------------------------- scan
+
+struct ScanSmem {
+    uint32_t* cnt;        // packed counters of the tile
+    uint64_t* ht;         // Robin Hood table / histogram scratch
+    uint32_t* za;         // ZipperArray, levels [0, bound]
+    uint64_t* s_beg;      // staged slices
+    uint32_t* s_len;
+    uint32_t* s_upref;
+    unsigned long long* sums;  // block scan scratch (32)
+    uint32_t* scal;            // scalars
+};
+
+enum ScalarSlot {
+    SC_ITEM = 0,
+    SC_AT = 1,
+    SC_OVF = 2,
+    SC_NOUT = 3,
+    SC_UCTR = 4,
+    SC_U = 5,
+    SC_TIES = 6,
+    SC_T = 7,
+    SC_ABOVE = 8,
+    SC_DONE = 9,
+    SC_WORDS = 16
+};
+
+__device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t tile_bytes) {
+    ScanSmem s;
+    s.cnt = reinterpret_cast<uint32_t*>(base);
+    base += tile_bytes;
+    s.ht = reinterpret_cast<uint64_t*>(base);
+    base += kHtMaxSlots * sizeof(uint64_t);
+    s.s_beg = reinterpret_cast<uint64_t*>(base);
+    base += kSpanBatch * sizeof(uint64_t);
+    s.sums = reinterpret_cast<unsigned long long*>(base);
+    base += 32 * sizeof(unsigned long long);
+    s.za = reinterpret_cast<uint32_t*>(base);
+    base += kZaMax * sizeof(uint32_t);
+    s.s_len = reinterpret_cast<uint32_t*>(base);
+    base += kSpanBatch * sizeof(uint32_t);
+    s.s_upref = reinterpret_cast<uint32_t*>(base);
+    base += kSpanBatch * sizeof(uint32_t);
+    s.scal = reinterpret_cast<uint32_t*>(base);
+    return s;
+}
+
+inline size_t scan_smem_bytes(uint32_t tile_bytes) {
+    return tile_bytes + kHtMaxSlots * 8 + kSpanBatch * 8 + 32 * 8 + kZaMax * 4 + kSpanBatch * 4 * 2 +
+           SC_WORDS * 4;
+}
+
+__device__ __forceinline__ uint32_t ht_home(uint32_t id, uint32_t mask) {
+    return static_cast<uint32_t>(mix64(id)) & mask;
+}
+
+__device__ __forceinline__ uint64_t pack_slot(uint32_t id, uint32_t v, uint32_t age) {
+    return (uint64_t(id) << 32) | (uint64_t(v & 0xffffu) << 16) | uint64_t(age & 0xffffu);
+}
+
+// Lock-free modified Robin Hood insert in shared memory; the same protocol
+// as CountHashTable::insert (cpq.hpp:149-204): empty -> claim, same id ->
+// raise value keeping age, dead resident (value + 1 < AT) -> overwrite,
+// younger resident -> displace and keep probing with it.  Returns false when
+// the table is full (the caller falls back to an exact histogram select).
+__device__ bool ht_insert(uint64_t* ht, uint32_t cap, uint32_t id, uint32_t value,
+                          uint32_t cur_at) {
+    const uint32_t mask = cap - 1;
+    uint64_t carried = pack_slot(id, value, 0);
+    uint32_t slot = ht_home(id, mask);
+    for (uint32_t probes = 0; probes <= cap; ++probes) {
+        unsigned long long* addr = reinterpret_cast<unsigned long long*>(&ht[slot]);
+        uint64_t res = *reinterpret_cast<volatile uint64_t*>(&ht[slot]);
+        bool advance = false;
+        while (!advance) {
+            if (res == kEmptySlot) {
+                const uint64_t prev = atomicCAS(addr, kEmptySlot, carried);
+                if (prev == kEmptySlot) return true;
+                res = prev;
+                continue;
+            }
+            const uint32_t rid = uint32_t(res >> 32), rv = uint32_t(res >> 16) & 0xffffu,
+                           rage = uint32_t(res) & 0xffffu;
+            const uint32_t cid = uint32_t(carried >> 32), cv = uint32_t(carried >> 16) & 0xffffu,
+                           cage = uint32_t(carried) & 0xffffu;
+            if (rid == cid) {
+                if (rv >= cv) return true;
+                const uint64_t merged = pack_slot(rid, cv, rage);
+                const uint64_t prev = atomicCAS(addr, res, merged);
+                if (prev == res) return true;
+                res = prev;
+                continue;
+            }
+            if (uint64_t(rv) + 1 < cur_at) {  // dead: cannot reach top-k any more
+                const uint64_t prev = atomicCAS(addr, res, carried);
+                if (prev == res) return true;
+                res = prev;
+                continue;
+            }
+            if (rage < cage) {  // Robin Hood displacement
+                const uint64_t prev = atomicCAS(addr, res, carried);
+                if (prev == res) {
+                    carried = res;
+                    advance = true;
+                    continue;
+                }
+                res = prev;
+                continue;
+            }
+            advance = true;
+        }
+        slot = (slot + 1) & mask;
+        const uint32_t age = uint32_t(carried) & 0xffffu;
+        if (age >= 0xffffu) break;
+        carried += 1;
+    }
+    return false;
+}
+
+template <int W>
+struct Packing {
+    static constexpr uint32_t kPer = 32 / W;
+    static constexpr uint32_t kMask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+    __device__ static __forceinline__ uint32_t get(const uint32_t* cnt, uint32_t local) {
+        return (cnt[local / kPer] >> ((local % kPer) * W)) & kMask;
+    }
+    // Bit (pos * W + W - 1) set for every counter equal to v.
+    __device__ static __forceinline__ uint32_t eq_mask(uint32_t x, uint32_t v) {
+        if constexpr (W == 4) {
+            const uint32_t y = x ^ (v * 0x11111111u);
+            return ~(((y & 0x77777777u) + 0x77777777u) | y | 0x77777777u);
+        } else if constexpr (W == 8) {
+            const uint32_t y = x ^ (v * 0x01010101u);
+            return ~(((y & 0x7f7f7f7fu) + 0x7f7f7f7fu) | y | 0x7f7f7f7fu);
+        } else {
+            return ((x & 0xffffu) == v ? 0x8000u : 0u) | ((x >> 16) == v ? 0x80000000u : 0u);
+        }
+    }
+};
+
+struct ItemCtx {
+    uint32_t q, t, kq, bound, tile_lo, tile_n, words, ht_cap, cap;
+    uint64_t out_base;
+    bool gate;
+};
+
+// Count every posting of [ua, ub) (absolute positions) into the tile's
+// shared counters; with the gate on, feed the c-PQ with each new value.
+template <int W, bool GATE>
+__device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings, uint64_t ua,
+                                           uint64_t ub, const ItemCtx& it, const ScanSmem& sm) {
+    using Pk = Packing<W>;
+    constexpr int UNR = 4;
+    const int lane = threadIdx.x & 31;
+    const uint64_t base = ua & ~3ull;
+    uint32_t at = GATE ? *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]) : 0;
+    for (uint64_t p0 = base + uint64_t(lane) * 4; p0 < ub; p0 += 128 * UNR) {
+        uint4 v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint64_t pp = p0 + uint64_t(u) * 128;
+            v[u] = pp < ub ? ldg_stream_v4(postings + pp) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint64_t pp = p0 + uint64_t(u) * 128;
+            const uint32_t e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint64_t pos = pp + e;
+                if (pos >= ua && pos < ub) {
+                    const uint32_t local = e4[e] - it.tile_lo;
+                    const uint32_t sh = (local % Pk::kPer) * W;
+                    const uint32_t old = atomicAdd(&sm.cnt[local / Pk::kPer], 1u << sh);
+                    if constexpr (GATE) {
+                        const uint32_t val = ((old >> sh) & Pk::kMask) + 1;
+                        if (val >= at) {
+                            // cpq.hpp:294-301: insert, bump ZA[val], advance AT
+                            const uint32_t cur =
+                                *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]);
+                            if (!ht_insert(sm.ht, it.ht_cap, local, val, cur)) sm.scal[SC_OVF] = 1;
+                            atomicAdd(&sm.za[val], 1u);
+                            uint32_t a = *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]);
+                            while (a <= it.bound &&
+                                   *reinterpret_cast<volatile uint32_t*>(&sm.za[a]) >= it.kq) {
+                                atomicCAS(&sm.scal[SC_AT], a, a + 1);
+                                a = *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]);
+                            }
+                            at = a;
+                        }
+                    }
+                }
+            }
+        }
+        if constexpr (GATE) at = *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]);
+    }
+}
+
+__device__ __forceinline__ void emit(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
+                                     uint32_t local, uint32_t count) {
+    const uint32_t pos = atomicAdd(&sm.scal[SC_NOUT], 1u);
+    genie_entry e;
+    e.id = local + it.tile_lo;
+    e.count = count;
+    p.tile_out[it.out_base + pos] = e;
+}
+
+// Ties at T in ascending local id, the first `need` of them
+// (cpq.hpp:330-336).  Ordered block scan over the counter words; stops as
+// soon as enough ties were seen.
+template <int W>
+__device__ void emit_ties(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t T,
+                          uint32_t need) {
+    using Pk = Packing<W>;
+    unsigned long long seen = 0;
+    for (uint32_t w0 = 0; w0 < it.words; w0 += blockDim.x) {
+        const uint32_t wi = w0 + threadIdx.x;
+        const uint32_t x = wi < it.words ? sm.cnt[wi] : 0u;
+        uint32_t m = wi < it.words ? Pk::eq_mask(x, T) : 0u;
+        unsigned long long total;
+        const unsigned long long before =
+            seen + block_exclusive_scan<unsigned long long>(__popc(m), sm.sums, total);
+        unsigned long long r = before;
+        while (m && r < need) {
+            const uint32_t b = __ffs(m) - 1;
+            m &= m - 1;
+            emit(p, it, sm, wi * Pk::kPer + b / W, T);
+            ++r;
+        }
+        seen += total;
+        if (seen >= need) break;  // uniform: total is block-wide
+    }
+}
+
+// Exact histogram k-selection over the tile counters (GEN-SPQ ablation and
+// the fallback when the table overflowed): T = k-th largest count in the
+// tile, zeros included (0 if fewer than k non-zero), then every count > T
+// and the first ties at T in ascending id.
+template <int W>
+__device__ void hist_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm) {
+    using Pk = Packing<W>;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    uint32_t* h = reinterpret_cast<uint32_t*>(sm.ht);  // 16 warps x 256 bins
+    // level 1: high byte of the count (W == 16) or the count itself (W <= 8)
+    constexpr uint32_t kShift1 = W == 16 ? 8 : 0;
+    uint32_t T = 0, above = 0;
+    uint32_t hi_sel = 0;
+    unsigned long long cum_above = 0;
+    for (int level = 0; level < (W == 16 ? 2 : 1); ++level) {
+        for (uint32_t i = threadIdx.x; i < uint32_t(nwarps) * 256; i += blockDim.x) h[i] = 0;
+        __syncthreads();
+        for (uint32_t wi = threadIdx.x; wi < it.words; wi += blockDim.x) {
+            const uint32_t x = sm.cnt[wi];
+            if (!x) continue;
+#pragma unroll
+            for (uint32_t j = 0; j < Pk::kPer; ++j) {
+                const uint32_t c = (x >> (j * W)) & Pk::kMask;
+                if (!c) continue;
+                if (level == 0) {
+                    atomicAdd(&h[warp * 256 + (c >> kShift1)], 1u);
+                } else if ((c >> 8) == hi_sel) {
+                    atomicAdd(&h[warp * 256 + (c & 0xffu)], 1u);
+                }
+            }
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) {
+            uint32_t s = 0;
+            for (int w = 0; w < nwarps; ++w) s += h[w * 256 + b];
+            h[b] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // walk bins from the top until k objects are covered
+            unsigned long long cum = cum_above;
+            uint32_t sel = 0;
+            bool found = false;
+            for (int b = 255; b >= 0; --b) {
+                if (level == 0 && W != 16 && b == 0) break;  // count 0 is not a level
+                if (level == 1 && hi_sel == 0 && b == 0) break;
+                const unsigned long long nb = cum + h[b];
+                if (nb >= it.kq) {
+                    sel = b;
+                    found = true;
+                    break;
+                }
+                cum = nb;
+            }
+            sm.scal[SC_T] = found ? sel : 0xffffffffu;
+            reinterpret_cast<unsigned long long*>(sm.sums)[31] = cum;
+        }
+        __syncthreads();
+        const uint32_t sel = sm.scal[SC_T];
+        const unsigned long long cum = reinterpret_cast<unsigned long long*>(sm.sums)[31];
+        __syncthreads();
+        if (sel == 0xffffffffu) {  // fewer than k non-zero objects at this level
+            if (level == 0 || W != 16) {
+                T = 0;
+                above = 0;
+                break;
+            }
+            // level 1 with hi_sel chosen: cannot happen (level 0 found >= k)
+            T = hi_sel << 8;
+            break;
+        }
+        if (W == 16 && level == 0) {
+            hi_sel = sel;
+            cum_above = cum;
+            continue;
+        }
+        T = (W == 16) ? ((hi_sel << 8) | sel) : sel;
+        above = static_cast<uint32_t>(cum);
+    }
+    // emit: every count > T, then ties at T (T > 0) in ascending id
+    const uint32_t need = T ? it.kq - above : 0;
+    unsigned long long seen = 0;
+    for (uint32_t w0 = 0; w0 < it.words; w0 += blockDim.x) {
+        const uint32_t wi = w0 + threadIdx.x;
+        const uint32_t x = wi < it.words ? sm.cnt[wi] : 0u;
+        uint32_t tie_mask = 0;
+        if (x) {
+#pragma unroll
+            for (uint32_t j = 0; j < Pk::kPer; ++j) {
+                const uint32_t c = (x >> (j * W)) & Pk::kMask;
+                if (c > T) emit(p, it, sm, wi * Pk::kPer + j, c);
+                else if (T && c == T) tie_mask |= 1u << j;
+            }
+        }
+        unsigned long long total;
+        unsigned long long r =
+            seen + block_exclusive_scan<unsigned long long>(__popc(tie_mask), sm.sums, total);
+        while (tie_mask && r < need) {
+            const uint32_t j = __ffs(tie_mask) - 1;
+            tie_mask &= tie_mask - 1;
+            emit(p, it, sm, wi * Pk::kPer + j, T);
+            ++r;
+        }
+        seen += total;
+    }
+}
+
+template <int W>
+__device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t q, uint32_t t) {
+    using Pk = Packing<W>;
+    ItemCtx it;
+    it.q = q;
+    it.t = t;
+    it.kq = p.k[q];
+    it.bound = static_cast<uint32_t>(p.q_bound[q] < 1 ? 1 : p.q_bound[q]);
+    const uint32_t T = p.tile_bits / W;
+    it.tile_lo = t * T;
+    it.tile_n = min(T, p.n - it.tile_lo);
+    it.words = (it.tile_n + Pk::kPer - 1) / Pk::kPer;
+    it.cap = p.q_cap[q];
+    it.out_base = p.q_out_base[q] + uint64_t(t) * it.cap;
+    it.gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
+    const uint64_t want2 = 2ull * it.kq * it.bound;
+    const uint64_t want = want2 < 2 ? 2 : want2;
+    const uint64_t htc = bit_ceil64(want);
+    it.ht_cap = static_cast<uint32_t>(htc < kHtMaxSlots ? htc : kHtMaxSlots);
+
+    // setup: zero counters, empty table, ZA, AT = 1 (cpq.hpp:281-292)
+    {
+        uint4* c4 = reinterpret_cast<uint4*>(sm.cnt);
+        const uint32_t w4 = (it.words + 3) / 4;
+        for (uint32_t i = threadIdx.x; i < w4; i += blockDim.x) c4[i] = make_uint4(0, 0, 0, 0);
+        if (it.gate) {
+            for (uint32_t i = threadIdx.x; i < it.ht_cap; i += blockDim.x) sm.ht[i] = kEmptySlot;
+            for (uint32_t i = threadIdx.x; i <= it.bound; i += blockDim.x) sm.za[i] = 0;
+        }
+        if (threadIdx.x == 0) {
+            sm.scal[SC_AT] = 1;
+            sm.scal[SC_OVF] = 0;
+            sm.scal[SC_NOUT] = 0;
+        }
+    }
+    const uint32_t S = p.q_S[q];
+    const uint32_t nt = p.q_ntiles[q];
+    const uint64_t cb = p.q_cut_base[q];
+    const uint64_t sbq = p.q_span_base[q];
+    const uint32_t unit = p.unit;
+    for (uint32_t s0 = 0; s0 < S; s0 += kSpanBatch) {
+        const uint32_t nsb = min(kSpanBatch, S - s0);
+        uint32_t units = 0;
+        if (threadIdx.x < nsb) {
+            const uint32_t s = s0 + threadIdx.x;
+            const uint32_t* c = p.cuts + cb + uint64_t(s) * (nt + 1) + t;
+            const uint32_t a = c[0], e = c[1];
+            const uint64_t beg = p.span_beg[sbq + s] + a;
+            const uint32_t len = e - a;
+            sm.s_beg[threadIdx.x] = beg;
+            sm.s_len[threadIdx.x] = len;
+            units = len ? static_cast<uint32_t>((beg + len - 1) / unit - beg / unit + 1) : 0;
+        }
+        unsigned long long total;
+        const unsigned long long ex =
+            block_exclusive_scan<unsigned long long>(units, sm.sums, total);
+        if (threadIdx.x < nsb) sm.s_upref[threadIdx.x] = static_cast<uint32_t>(ex);
+        if (threadIdx.x == 0) sm.scal[SC_UCTR] = 0;
+        __syncthreads();
+        const uint32_t U = static_cast<uint32_t>(total);
+        const int lane = threadIdx.x & 31;
+        for (;;) {
+            uint32_t u = 0;
+            if (lane == 0) u = atomicAdd(&sm.scal[SC_UCTR], 1u);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            if (u >= U) break;
+            // slice holding unit u: last si with upref[si] <= u
+            uint32_t lo = 0, hi = nsb;
+            while (lo < hi) {
+                const uint32_t m = (lo + hi) >> 1;
+                if (sm.s_upref[m] <= u) lo = m + 1;
+                else hi = m;
+            }
+            const uint32_t si = lo - 1;
+            const uint64_t beg = sm.s_beg[si];
+            const uint64_t end = beg + sm.s_len[si];
+            const uint64_t j = u - sm.s_upref[si];
+            const uint64_t ua = max(beg, (beg / unit + j) * unit);
+            const uint64_t ub = min(end, (beg / unit + j + 1) * unit);
+            if (it.gate) scan_range<W, true>(p.postings, ua, ub, it, sm);
+            else scan_range<W, false>(p.postings, ua, ub, it, sm);
+        }
+        __syncthreads();
+    }
+
+    // ---- select: the tile's exact top-k
+    if (it.gate && !sm.scal[SC_OVF]) {
+        if (threadIdx.x == 0) {
+            uint32_t a = sm.scal[SC_AT];
+            while (a <= it.bound && sm.za[a] >= it.kq) ++a;
+            sm.scal[SC_AT] = a;
+        }
+        __syncthreads();
+        const uint32_t thr = sm.scal[SC_AT] - 1;  // cpq.hpp:310-311
+        // table entries above the threshold (all touched ids when thr == 0);
+        // an id may own a stale slot -- only the slot holding its final
+        // count is reported (cpq.hpp:212-222, 391-406)
+        for (uint32_t s = threadIdx.x; s < it.ht_cap; s += blockDim.x) {
+            const uint64_t w = sm.ht[s];
+            if (w == kEmptySlot) continue;
+            const uint32_t id = uint32_t(w >> 32), v = uint32_t(w >> 16) & 0xffffu;
+            const uint32_t c = Pk::get(sm.cnt, id);
+            if (v == c && c > thr) emit(p, it, sm, id, c);
+        }
+        __syncthreads();
+        const uint32_t n_above = sm.scal[SC_NOUT];
+        if (thr > 0 && n_above < it.kq) emit_ties<W>(p, it, sm, thr, it.kq - n_above);
+    } else {
+        if (it.gate && threadIdx.x == 0) atomicAdd(&p.st[ST_FALLBACK], 1ull);
+        hist_select<W>(p, it, sm);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) p.tile_len[p.q_tile_base[q] + t] = sm.scal[SC_NOUT];
+}
+
+__global__ void __launch_bounds__(kScanThreads, 1)
+    k_scan(BatchParams p, uint32_t tile_bytes) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const ScanSmem sm = carve(smem, tile_bytes);
+    if (p.st[ST_OVERFLOW]) return;
+    const uint64_t total = p.st[ST_TOTAL_WORK];
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const unsigned long long i = atomicAdd(&p.st[ST_WORK_CTR], 1ull);
+            sm.scal[SC_ITEM] = i < total ? static_cast<uint32_t>(i) : 0xffffffffu;
+        }
+        __syncthreads();
+        const uint32_t item = sm.scal[SC_ITEM];
+        __syncthreads();
+        if (item == 0xffffffffu) break;
+        const uint32_t q = p.work_q[item], t = p.work_t[item];
+        switch (p.q_W[q]) {
+            case 4: process_item<4>(p, sm, q, t); break;
+            case 8: process_item<8>(p, sm, q, t); break;
+            default: process_item<16>(p, sm, q, t); break;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ merge
+
+// Where the candidate lists of query q live.
+struct MergeSrc {
+    // mode 0: object tiles of this batch; mode 1: explicit lists (multi-GPU)
+    int mode;
+    // mode 0
+    const uint64_t* q_out_base;
+    const uint32_t* q_cap;
+    const uint32_t* q_tile_base;
+    const uint32_t* q_ntiles;
+    const uint32_t* tile_len;
+    const genie_entry* tile_out;
+    // mode 1
+    uint32_t L;
+    const genie_entry* in;
+    const uint32_t* in_len;
+    uint32_t in_stride;
+    // common
+    const uint32_t* k;
+    uint32_t Q;
+    uint32_t id_offset;
+    uint32_t* q_big;
+    unsigned long long* st;
+    uint32_t out_stride;
+    genie_entry* out;
+    uint32_t* out_len;
+    uint32_t* out_thr;
+};
+
+__device__ __forceinline__ void list_of(const MergeSrc& m, uint32_t q, uint32_t l,
+                                        const genie_entry*& base, uint32_t& len) {
+    if (m.mode == 0) {
+        base = m.tile_out + m.q_out_base[q] + uint64_t(l) * m.q_cap[q];
+        len = m.tile_len[m.q_tile_base[q] + l];
+    } else {
+        base = m.in + (uint64_t(q) * m.L + l) * m.in_stride;
+        len = m.in_len[uint64_t(q) * m.L + l];
+    }
+}
+
+__device__ __forceinline__ uint32_t nlists_of(const MergeSrc& m, uint32_t q) {
+    return m.mode == 0 ? m.q_ntiles[q] : m.L;
+}
+
+// merge_topk (engine.hpp:158-177) for unions of at most kSortCap entries:
+// concatenate, bitonic sort by (count desc, id asc), truncate to k,
+// threshold = k-th count if at least k entries else 0.
+__global__ void __launch_bounds__(kMergeThreads) k_merge(MergeSrc m) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+    __shared__ unsigned long long sums[32];
+    __shared__ uint32_t s_off[kMergeThreads + 1];
+    __shared__ uint32_t s_flag;
+    for (uint32_t q = blockIdx.x; q < m.Q; q += gridDim.x) {
+        const uint32_t L = nlists_of(m, q);
+        const uint32_t kq = m.k[q];
+        // union size
+        unsigned long long M = 0;
+        for (uint32_t l0 = 0; l0 < L; l0 += blockDim.x) {
+            const uint32_t l = l0 + threadIdx.x;
+            uint32_t len = 0;
+            if (l < L) {
+                const genie_entry* b;
+                list_of(m, q, l, b, len);
+            }
+            M += block_sum<unsigned long long>(len, sums);
+        }
+        if (M > kSortCap) {
+            if (threadIdx.x == 0) {
+                m.q_big[q] = 1;
+                atomicAdd(&m.st[ST_MERGE_BIG], 1ull);
+            }
+            __syncthreads();
+            continue;
+        }
+        if (threadIdx.x == 0) m.q_big[q] = 0;
+        // gather (chunks of blockDim lists)
+        uint32_t filled = 0;
+        for (uint32_t l0 = 0; l0 < L; l0 += blockDim.x) {
+            const uint32_t l = l0 + threadIdx.x;
+            uint32_t len = 0;
+            const genie_entry* b = nullptr;
+            if (l < L) list_of(m, q, l, b, len);
+            unsigned long long tot;
+            const unsigned long long ex = block_exclusive_scan<unsigned long long>(len, sums, tot);
+            if (threadIdx.x <= blockDim.x) s_off[threadIdx.x] = static_cast<uint32_t>(ex);
+            __syncthreads();
+            // one warp per list
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            for (uint32_t w = warp; w < blockDim.x && l0 + w < L; w += blockDim.x >> 5) {
+                const genie_entry* bb;
+                uint32_t ll;
+                list_of(m, q, l0 + w, bb, ll);
+                const uint32_t o = filled + s_off[w];
+                for (uint32_t e = lane; e < ll; e += 32) {
+                    const genie_entry x = bb[e];
+                    keys[o + e] = order_key(x.id, x.count);
+                }
+            }
+            filled += static_cast<uint32_t>(tot);
+            __syncthreads();
+        }
+        uint32_t N = 1;
+        while (N < filled) N <<= 1;
+        for (uint32_t i = filled + threadIdx.x; i < N; i += blockDim.x) keys[i] = ~0ull;
+        __syncthreads();
+        if (m.mode == 1 && filled > 1) {
+            // duplicate ids across lists are a ContractError (engine.hpp:165-172)
+            for (uint32_t i = threadIdx.x; i < filled; i += blockDim.x) {
+                const uint64_t k0 = keys[i];
+                keys[i] = (uint64_t(key_id(k0)) << 32) | key_count(k0);
+            }
+            __syncthreads();
+            bitonic_sort_smem(keys, N);
+            if (threadIdx.x == 0) s_flag = 0;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x + 1; i < filled; i += blockDim.x)
+                if ((keys[i] >> 32) == (keys[i - 1] >> 32)) s_flag = 1;
+            __syncthreads();
+            if (s_flag && threadIdx.x == 0) atomicMin(&m.st[ST_MERGE_DUP], (unsigned long long)q);
+            for (uint32_t i = threadIdx.x; i < filled; i += blockDim.x) {
+                const uint64_t k0 = keys[i];
+                keys[i] = order_key(uint32_t(k0 >> 32), uint32_t(k0));
+            }
+            __syncthreads();
+        }
+        bitonic_sort_smem(keys, N);
+        const uint32_t outn = kq < filled ? kq : filled;
+        genie_entry* row = m.out + uint64_t(q) * m.out_stride;
+        for (uint32_t e = threadIdx.x; e < outn; e += blockDim.x) {
+            genie_entry x;
+            x.id = key_id(keys[e]) + m.id_offset;
+            x.count = key_count(keys[e]);
+            row[e] = x;
+        }
+        if (threadIdx.x == 0) {
+            m.out_len[q] = outn;
+            m.out_thr[q] = filled >= kq ? key_count(keys[kq - 1]) : 0;  // engine.hpp:175
+        }
+        __syncthreads();
+    }
+}
+
+// Large unions (> kSortCap entries): exact selection by radix histograms in
+// global memory, then a shared-memory sort of the k winners (k <= kSortCap)
+// or a device segmented sort for longer rows.
+__global__ void __launch_bounds__(kMergeThreads) k_merge_big(MergeSrc m) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+    __shared__ uint32_t hist[256];
+    __shared__ unsigned long long sums[32];
+    __shared__ uint32_t s_sel;
+    __shared__ unsigned long long s_cum;
+    __shared__ uint32_t s_pos;
+    for (uint32_t q = blockIdx.x; q < m.Q; q += gridDim.x) {
+        if (!m.q_big[q]) continue;
+        const uint32_t L = nlists_of(m, q);
+        const uint32_t kq = m.k[q];
+        unsigned long long M = 0;
+        for (uint32_t l = 0; l < L; ++l) {
+            const genie_entry* b;
+            uint32_t len;
+            list_of(m, q, l, b, len);
+            M += len;
+        }
+        // --- threshold count T: 2 x 8-bit radix passes over the 16-bit counts
+        uint32_t T = 0;
+        unsigned long long n_above = 0;
+        const bool all = M <= kq;
+        if (!all) {
+            uint32_t prefix = 0;
+            unsigned long long cum_above = 0;
+            for (int pass = 0; pass < 2; ++pass) {
+                for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+                __syncthreads();
+                for (uint32_t l = 0; l < L; ++l) {
+                    const genie_entry* b;
+                    uint32_t len;
+                    list_of(m, q, l, b, len);
+                    for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
+                        const uint32_t c = b[e].count;
+                        if (pass == 0) atomicAdd(&hist[(c >> 8) & 0xffu], 1u);
+                        else if ((c >> 8) == prefix) atomicAdd(&hist[c & 0xffu], 1u);
+                    }
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    unsigned long long cum = cum_above;
+                    uint32_t sel = 0;
+                    for (int b = 255; b >= 0; --b) {
+                        if (cum + hist[b] >= kq) {
+                            sel = b;
+                            break;
+                        }
+                        cum += hist[b];
+                    }
+                    s_sel = sel;
+                    s_cum = cum;
+                }
+                __syncthreads();
+                if (pass == 0) {
+                    prefix = s_sel;
+                    cum_above = s_cum;
+                } else {
+                    T = (prefix << 8) | s_sel;
+                    n_above = s_cum;
+                }
+                __syncthreads();
+            }
+        }
+        // --- tie cutoff: the need-th smallest id among count == T (4 radix passes)
+        const unsigned long long need = all ? 0 : kq - n_above;
+        uint32_t id_cut = 0xffffffffu;
+        if (!all) {
+            uint32_t idp = 0;
+            unsigned long long below = 0;
+            for (int pass = 0; pass < 4; ++pass) {
+                const int sh = 24 - 8 * pass;
+                for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+                __syncthreads();
+                for (uint32_t l = 0; l < L; ++l) {
+                    const genie_entry* b;
+                    uint32_t len;
+                    list_of(m, q, l, b, len);
+                    for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
+                        const genie_entry x = b[e];
+                        if (x.count != T) continue;
+                        const uint32_t hi = pass ? (x.id >> (sh + 8)) : 0;
+                        if (hi == (pass ? (idp >> (sh + 8)) : 0)) atomicAdd(&hist[(x.id >> sh) & 0xffu], 1u);
+                    }
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    unsigned long long cum = below;
+                    uint32_t sel = 255;
+                    for (uint32_t b = 0; b < 256; ++b) {
+                        if (cum + hist[b] >= need) {
+                            sel = b;
+                            break;
+                        }
+                        cum += hist[b];
+                    }
+                    s_sel = sel;
+                    s_cum = cum;
+                }
+                __syncthreads();
+                idp |= s_sel << sh;
+                below = s_cum;
+                __syncthreads();
+            }
+            id_cut = idp;
+        }
+        // --- emit the winners into the output row
+        if (threadIdx.x == 0) s_pos = 0;
+        __syncthreads();
+        genie_entry* row = m.out + uint64_t(q) * m.out_stride;
+        for (uint32_t l = 0; l < L; ++l) {
+            const genie_entry* b;
+            uint32_t len;
+            list_of(m, q, l, b, len);
+            for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
+                const genie_entry x = b[e];
+                if (all || x.count > T || (x.count == T && x.id <= id_cut)) {
+                    const uint32_t pos = atomicAdd(&s_pos, 1u);
+                    row[pos] = x;
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t outn = s_pos;
+        if (outn <= kSortCap) {
+            uint32_t N = 1;
+            while (N < outn) N <<= 1;
+            for (uint32_t i = threadIdx.x; i < N; i += blockDim.x)
+                keys[i] = i < outn ? order_key(row[i].id, row[i].count) : ~0ull;
+            __syncthreads();
+            bitonic_sort_smem(keys, N);
+            for (uint32_t e = threadIdx.x; e < outn; e += blockDim.x) {
+                genie_entry x;
+                x.id = key_id(keys[e]) + m.id_offset;
+                x.count = key_count(keys[e]);
+                row[e] = x;
+            }
+        } else {
+            // leave unsorted (local ids); the segmented sort finishes the row
+            if (threadIdx.x == 0) atomicAdd(&m.st[ST_SORT_BIG], 1ull);
+        }
+        if (threadIdx.x == 0) {
+            m.out_len[q] = outn;
+            // threshold: the k-th count when at least k entries (engine.hpp:175)
+            m.out_thr[q] = (!all || M >= kq) ? (all ? 0u : T) : 0u;
+            if (all && M == kq) {
+                uint32_t mn = 0xffffffffu;
+                for (uint32_t e = 0; e < outn; ++e) mn = min(mn, row[e].count);
+                m.out_thr[q] = mn;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Rows longer than kSortCap: to order keys, segmented radix sort, back.
+__global__ void k_rows_to_keys(const genie_entry* out, const uint32_t* out_len, uint32_t stride,
+                               uint32_t Q, uint64_t* keys, uint64_t* seg_b, uint64_t* seg_e) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t total = uint64_t(Q) * stride;
+    if (i < Q) {
+        seg_b[i] = uint64_t(i) * stride;
+        seg_e[i] = uint64_t(i) * stride + (out_len[i] > kSortCap ? out_len[i] : 0);
+    }
+    if (i >= total) return;
+    const uint32_t q = static_cast<uint32_t>(i / stride), e = static_cast<uint32_t>(i % stride);
+    keys[i] = (out_len[q] > kSortCap && e < out_len[q]) ? order_key(out[i].id, out[i].count) : ~0ull;
+}
+
+__global__ void k_keys_to_rows(genie_entry* out, const uint32_t* out_len, uint32_t stride,
+                               uint32_t Q, const uint64_t* keys, uint32_t id_offset) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= uint64_t(Q) * stride) return;
+    const uint32_t q = static_cast<uint32_t>(i / stride), e = static_cast<uint32_t>(i % stride);
+    if (out_len[q] > kSortCap && e < out_len[q]) {
+        genie_entry x;
+        x.id = key_id(keys[i]) + id_offset;
+        x.count = key_count(keys[i]);
+        out[i] = x;
+    }
+}
+
+// ------------------------------------------------------------ orchestration
+
+int sm_count(int device) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    return v > 0 ? v : 148;
+}
+
+void ensure_device(int device) { GENIE_CUDA(cudaSetDevice(device)); }
+
+static void reserve_workspace(genie_index* ix, uint32_t Q, uint32_t items, uint32_t max_k,
+                              uint32_t out_stride, uint32_t tile_bits) {
+    Workspace& w = ix->ws;
+    if (!w.status.p) {
+        w.status.reserve(ST_WORDS);
+        GENIE_CUDA(cudaMallocHost(&w.h_status, ST_WORDS * sizeof(unsigned long long)));
+    }
+    const size_t q = Q + 1;
+    if (q > w.cap_q) {
+        const size_t c = std::max(q, w.cap_q * 2);
+        w.q_bound.reserve(c);
+        w.q_P.reserve(c);
+        w.q_span_base.reserve(c);
+        w.q_cut_base.reserve(c);
+        w.q_out_base.reserve(c);
+        w.q_S.reserve(c);
+        w.q_W.reserve(c);
+        w.q_ntiles.reserve(c);
+        w.q_cap.reserve(c);
+        w.q_tile_base.reserve(c);
+        w.q_rank.reserve(c);
+        w.q_big.reserve(c);
+        w.cap_q = c;
+    }
+    if (items > w.cap_items || !w.it_kb.p) {
+        const size_t c = std::max<size_t>(std::max<size_t>(items, 1024), w.cap_items * 2);
+        w.it_kb.reserve(c);
+        w.it_nk.reserve(c);
+        w.it_sbase.reserve(c);
+        w.cap_items = c;
+    }
+    // first-guess capacities; the device plan verifies them and the batch is
+    // retried with exact sizes on overflow
+    const uint64_t nt16 = ix->n ? (uint64_t(ix->n) + (tile_bits / 16) - 1) / (tile_bits / 16) : 1;
+    const uint64_t want_spans = std::max<uint64_t>(uint64_t(items) * 8, 4096);
+    const uint64_t want_work = std::max<uint64_t>(uint64_t(Q) * nt16, 1024);
+    const uint64_t want_cuts = std::max<uint64_t>(want_spans * 4, 16384);
+    const uint64_t want_tout =
+        std::max<uint64_t>(std::min<uint64_t>(uint64_t(Q) * nt16 * std::max<uint32_t>(max_k, 1),
+                                              uint64_t(Q) * (uint64_t(ix->n) + nt16)),
+                           4096);
+    if (want_spans > w.cap_spans) {
+        w.span_beg.reserve(want_spans);
+        w.cap_spans = want_spans;
+    }
+    if (want_cuts > w.cap_cuts) {
+        w.cuts.reserve(want_cuts);
+        w.cap_cuts = want_cuts;
+    }
+    if (want_work > w.cap_work) {
+        w.work_q.reserve(want_work);
+        w.work_t.reserve(want_work);
+        w.tile_len.reserve(want_work);
+        w.cap_work = want_work;
+    }
+    if (want_tout > w.cap_tout) {
+        w.tile_out.reserve(want_tout);
+        w.cap_tout = want_tout;
+    }
+    (void)out_stride;
+}
+
+static void grow_from_status(genie_index* ix) {
+    Workspace& w = ix->ws;
+    const unsigned long long* h = w.h_status;
+    if (h[ST_TOTAL_SPANS] > w.cap_spans) {
+        w.cap_spans = h[ST_TOTAL_SPANS] + (h[ST_TOTAL_SPANS] >> 2);
+        w.span_beg.reserve(w.cap_spans);
+    }
+    if (h[ST_TOTAL_CUTS] > w.cap_cuts) {
+        w.cap_cuts = h[ST_TOTAL_CUTS] + (h[ST_TOTAL_CUTS] >> 2);
+        w.cuts.reserve(w.cap_cuts);
+    }
+    if (h[ST_TOTAL_WORK] > w.cap_work) {
+        w.cap_work = h[ST_TOTAL_WORK] + (h[ST_TOTAL_WORK] >> 2);
+        w.work_q.reserve(w.cap_work);
+        w.work_t.reserve(w.cap_work);
+        w.tile_len.reserve(w.cap_work);
+    }
+    if (h[ST_TOTAL_TOUT] > w.cap_tout) {
+        w.cap_tout = h[ST_TOTAL_TOUT] + (h[ST_TOTAL_TOUT] >> 2);
+        w.tile_out.reserve(w.cap_tout);
+    }
+}
+
+static uint32_t tile_bits_of(const genie_config& cfg) {
+    uint32_t tb = cfg.tile_bytes ? cfg.tile_bytes : kDefaultTileBytes;
+    tb = std::max<uint32_t>(4096, std::min<uint32_t>(tb, 160u << 10));
+    tb &= ~15u;
+    return tb * 8;
+}
+
+static MergeSrc tile_merge_src(genie_index* ix, uint32_t Q, const uint32_t* d_k, uint32_t stride,
+                               genie_entry* out, uint32_t* out_len, uint32_t* out_thr) {
+    Workspace& w = ix->ws;
+    MergeSrc m{};
+    m.mode = 0;
+    m.q_out_base = w.q_out_base.p;
+    m.q_cap = w.q_cap.p;
+    m.q_tile_base = w.q_tile_base.p;
+    m.q_ntiles = w.q_ntiles.p;
+    m.tile_len = w.tile_len.p;
+    m.tile_out = w.tile_out.p;
+    m.k = d_k;
+    m.Q = Q;
+    m.id_offset = ix->id_offset;
+    m.q_big = w.q_big.p;
+    m.st = w.status.p;
+    m.out_stride = stride;
+    m.out = out;
+    m.out_len = out_len;
+    m.out_thr = out_thr;
+    return m;
+}
+
+static void segmented_sort_rows(genie_index* ix, uint32_t Q, uint32_t stride, genie_entry* out,
+                                uint32_t* out_len, uint32_t id_offset, cudaStream_t s) {
+    Workspace& w = ix->ws;
+    const uint64_t total = uint64_t(Q) * stride;
+    w.sort_keys.reserve(total);
+    w.sort_keys_alt.reserve(total);
+    w.sort_seg_begin.reserve(Q);
+    w.sort_seg_end.reserve(Q);
+    const uint32_t thr = 256;
+    const uint64_t blocks = (std::max<uint64_t>(total, Q) + thr - 1) / thr;
+    k_rows_to_keys<<<static_cast<unsigned>(blocks), thr, 0, s>>>(
+        out, out_len, stride, Q, w.sort_keys.p, w.sort_seg_begin.p, w.sort_seg_end.p);
+    size_t tmp = 0;
+    cub::DoubleBuffer<uint64_t> db(w.sort_keys.p, w.sort_keys_alt.p);
+    GENIE_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, db, static_cast<int>(total),
+                                                       static_cast<int>(Q), w.sort_seg_begin.p,
+                                                       w.sort_seg_end.p, 0, 64, s));
+    w.sort_tmp.reserve(tmp);
+    GENIE_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(w.sort_tmp.p, tmp, db, static_cast<int>(total),
+                                                       static_cast<int>(Q), w.sort_seg_begin.p,
+                                                       w.sort_seg_end.p, 0, 64, s));
+    k_keys_to_rows<<<static_cast<unsigned>((total + thr - 1) / thr), thr, 0, s>>>(
+        out, out_len, stride, Q, db.Current(), id_offset);
+}
+
+void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const uint32_t* d_qid,
+                  const uint32_t* d_k, const uint64_t* d_item_off, const uint16_t* d_dim,
+                  const uint32_t* d_lo, const uint32_t* d_hi, uint32_t total_items,
+                  uint32_t max_k, uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
+                  uint32_t* d_out_thr, cudaStream_t s, bool timed) {
+    (void)d_qid;
+    const uint32_t tile_bits = tile_bits_of(cfg);
+    const uint32_t tile_bytes = tile_bits / 8;
+    reserve_workspace(ix, Q, total_items, max_k, out_stride, tile_bits);
+    Workspace& w = ix->ws;
+    ix->last_Q = Q;
+    ix->last_cfg = cfg;
+    ix->last_timed = timed;
+    uint32_t launches = 0;
+
+    BatchParams p{};
+    p.keys = ix->keys.p;
+    p.key_off = ix->key_off.p;
+    p.postings = ix->postings.p;
+    p.dim_mult = ix->dim_mult.p;
+    p.K = ix->K;
+    p.n = ix->n;
+    p.id_offset = ix->id_offset;
+    p.Q = Q;
+    p.k = d_k;
+    p.item_off = d_item_off;
+    p.dim = d_dim;
+    p.lo = d_lo;
+    p.hi = d_hi;
+    p.tile_bits = tile_bits;
+    uint32_t unit = cfg.span_chunk ? cfg.span_chunk : kDefaultUnit;
+    unit = std::min<uint32_t>(std::max<uint32_t>((unit + 127) & ~127u, 128), 1u << 16);
+    p.unit = unit;
+    p.selector = cfg.selector;
+    p.q_bound = w.q_bound.p;
+    p.q_P = w.q_P.p;
+    p.q_span_base = w.q_span_base.p;
+    p.q_cut_base = w.q_cut_base.p;
+    p.q_out_base = w.q_out_base.p;
+    p.q_S = w.q_S.p;
+    p.q_W = w.q_W.p;
+    p.q_ntiles = w.q_ntiles.p;
+    p.q_cap = w.q_cap.p;
+    p.q_tile_base = w.q_tile_base.p;
+    p.q_rank = w.q_rank.p;
+    p.q_big = w.q_big.p;
+    p.it_kb = w.it_kb.p;
+    p.it_nk = w.it_nk.p;
+    p.it_sbase = w.it_sbase.p;
+    p.span_beg = w.span_beg.p;
+    p.cuts = w.cuts.p;
+    p.work_q = w.work_q.p;
+    p.work_t = w.work_t.p;
+    p.tile_len = w.tile_len.p;
+    p.tile_out = w.tile_out.p;
+    p.st = w.status.p;
+    p.cap_spans = w.cap_spans;
+    p.cap_cuts = w.cap_cuts;
+    p.cap_work = w.cap_work;
+    p.cap_tout = w.cap_tout;
+    p.out_stride = out_stride;
+    p.out = d_out;
+    p.out_len = d_out_len;
+    p.out_thr = d_out_thr;
+
+    if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[0], s));
+    k_init_status<<<1, 32, 0, s>>>(w.status.p);
+    ++launches;
+    if (Q) {
+        k_resolve<<<(Q * 32 + 255) / 256, 256, 0, s>>>(p);
+        k_plan<<<1, 1024, 0, s>>>(p);
+        k_worklist<<<(Q + 255) / 256, 256, 0, s>>>(p);
+        launches += 3;
+        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
+        const int sms = ix->sms;
+        k_cut<<<sms * 8, 256, 0, s>>>(p);
+        ++launches;
+        const size_t smem = scan_smem_bytes(tile_bytes);
+        static thread_local size_t configured = 0;
+        if (configured < smem) {
+            GENIE_CUDA(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem)));
+            configured = smem;
+        }
+        uint32_t per_sm = cfg.ctas_per_sm ? cfg.ctas_per_sm : 0;
+        if (!per_sm) {
+            int occ = 0;
+            GENIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan, kScanThreads, smem));
+            per_sm = std::max(1, occ);
+        }
+        k_scan<<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+        ++launches;
+        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
+        const MergeSrc m = tile_merge_src(ix, Q, d_k, out_stride, d_out, d_out_len, d_out_thr);
+        const size_t msmem = kSortCap * sizeof(uint64_t);
+        static thread_local bool mconf = false;
+        if (!mconf) {
+            GENIE_CUDA(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(msmem)));
+            GENIE_CUDA(cudaFuncSetAttribute(k_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(msmem)));
+            mconf = true;
+        }
+        const uint32_t mgrid = std::min<uint32_t>(Q, sms * 4);
+        k_merge<<<mgrid, kMergeThreads, msmem, s>>>(m);
+        k_merge_big<<<mgrid, kMergeThreads, msmem, s>>>(m);
+        launches += 2;
+        if (max_k > kSortCap) {
+            segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, ix->id_offset, s);
+            launches += 3;
+        }
+    } else if (timed) {
+        GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
+        GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
+    }
+    if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
+    GENIE_CUDA(cudaMemcpyAsync(w.h_status, w.status.p, ST_WORDS * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
+    GENIE_CUDA(cudaGetLastError());
+    ix->last_launches = launches;
+}
+
+int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
+                 const uint32_t* h_qid) {
+    GENIE_CUDA(cudaStreamSynchronize(ix->stream));
+    GENIE_CUDA(cudaGetLastError());
+    const unsigned long long* h = ix->ws.h_status;
+    if (stats) {
+        stats->postings = h[ST_TOTAL_POSTINGS];
+        stats->work_items = h[ST_TOTAL_WORK];
+        stats->fallback_tiles = h[ST_FALLBACK];
+    }
+    if (h[ST_OVERFLOW]) {
+        grow_from_status(ix);
+        msg = "workspace grown; re-issue the batch";
+        return GENIE_RETRY;
+    }
+    auto qname = [&](unsigned long long q) {
+        return std::to_string(h_qid ? h_qid[q] : static_cast<uint32_t>(q));
+    };
+    if (h[ST_BAD_INPUT] != ~0ull) {
+        const unsigned long long q = h[ST_BAD_INPUT] >> 8;
+        const unsigned kind = h[ST_BAD_INPUT] & 0xff;
+        msg = "Query " + qname(q) +
+              (kind == 1 ? ": no items" : kind == 2 ? ": k must be >= 1" : ": QueryItem lo > hi");
+        return GENIE_ERR_CONTRACT;
+    }
+    if (h[ST_BAD_BOUND] != ~0ull) {
+        const unsigned long long q = h[ST_BAD_BOUND];
+        uint64_t bound = 0;
+        GENIE_CUDA(cudaMemcpy(&bound, ix->ws.q_bound.p + q, sizeof(bound), cudaMemcpyDeviceToHost));
+        msg = "query " + qname(q) + " (setup): match-count bound " + std::to_string(bound) +
+              " exceeds the counter range";
+        return GENIE_ERR_CONTRACT;
+    }
+    if (h[ST_MERGE_DUP] != ~0ull) {
+        msg = "merge_topk: an object was reported by more than one partition (query " +
+              qname(h[ST_MERGE_DUP]) + ")";
+        return GENIE_ERR_CONTRACT;
+    }
+    return GENIE_OK;
+}
+
+// ------------------------------------------------------------ merge (multi-GPU)
+
+void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
+                       const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
+                       uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
+                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s) {
+    Workspace& w = ix->ws;
+    if (!w.status.p) {
+        w.status.reserve(ST_WORDS);
+        GENIE_CUDA(cudaMallocHost(&w.h_status, ST_WORDS * sizeof(unsigned long long)));
+    }
+    if (Q + 1 > w.cap_q) {
+        w.q_big.reserve(Q + 1);
+    }
+    w.q_big.reserve(std::max<size_t>(Q + 1, w.q_big.n));
+    MergeSrc m{};
+    m.mode = 1;
+    m.L = L;
+    m.in = d_in;
+    m.in_len = d_in_len;
+    m.in_stride = in_stride;
+    m.k = d_k;
+    m.Q = Q;
+    m.id_offset = 0;
+    m.q_big = w.q_big.p;
+    m.st = w.status.p;
+    m.out_stride = out_stride;
+    m.out = d_out;
+    m.out_len = d_out_len;
+    m.out_thr = d_out_thr;
+    k_init_status<<<1, 32, 0, s>>>(w.status.p);
+    const size_t msmem = kSortCap * sizeof(uint64_t);
+    GENIE_CUDA(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(msmem)));
+    GENIE_CUDA(cudaFuncSetAttribute(k_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(msmem)));
+    const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(Q, ix->sms * 4));
+    if (Q) {
+        k_merge<<<grid, kMergeThreads, msmem, s>>>(m);
+        k_merge_big<<<grid, kMergeThreads, msmem, s>>>(m);
+        if (max_k > kSortCap) segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, 0, s);
+    }
+    GENIE_CUDA(cudaMemcpyAsync(w.h_status, w.status.p, ST_WORDS * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s));
+    GENIE_CUDA(cudaGetLastError());
+    ix->last_launches = 3;
+}
+
+}  // namespace genie

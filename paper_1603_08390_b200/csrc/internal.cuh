@@ -1,0 +1,109 @@
+// Internal structures shared by the libgenie_b200 translation units.
+#pragma once
+
+#include "common.cuh"
+
+namespace genie {
+
+// Tunables (result-invariant).
+constexpr uint32_t kScanThreads = 512;        // 16 warps per scan CTA
+constexpr uint32_t kSpanBatch = 512;          // spans staged in shared memory per pass
+constexpr uint32_t kHtMaxSlots = 4096;        // shared-memory Robin Hood table (32 KB)
+constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shared memory (W <= 8)
+constexpr uint32_t kDefaultTileBytes = 128u << 10;
+constexpr uint32_t kMergeThreads = 512;
+constexpr uint32_t kSortCap = 8192;           // merge entries sorted in shared memory
+constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit
+constexpr uint64_t kEmptySlot = ~0ull;
+
+// Status block words (u64) written by the device pipeline.
+enum StatusWord : int {
+    ST_BAD_INPUT = 0,   // min (q << 8 | kind): 1 empty query, 2 k == 0, 3 lo > hi
+    ST_BAD_BOUND = 1,   // min q whose max_count_bound > 0xffff
+    ST_TOTAL_SPANS = 2,
+    ST_TOTAL_CUTS = 3,
+    ST_TOTAL_WORK = 4,
+    ST_TOTAL_TOUT = 5,
+    ST_TOTAL_POSTINGS = 6,
+    ST_OVERFLOW = 7,    // workspace too small
+    ST_WORK_CTR = 8,    // persistent scan queue cursor
+    ST_FALLBACK = 9,    // tiles that fell back to histogram select
+    ST_MERGE_BIG = 10,  // queries merged by the large-union path
+    ST_MERGE_DUP = 11,  // min q with a duplicate id across merge lists
+    ST_CLASS0 = 12,     // queries per counter-width class (W = 4, 8, 16)
+    ST_CLASS1 = 13,
+    ST_CLASS2 = 14,
+    ST_CUT_CTR = 15,
+    ST_SORT_BIG = 16,   // rows longer than kSortCap left for the segmented sort
+    ST_WORDS = 32
+};
+
+// Per-batch device scratch, grown on demand (never shrinks).
+struct Workspace {
+    // per query
+    DevBuf<uint64_t> q_bound, q_P, q_span_base, q_cut_base, q_out_base;
+    DevBuf<uint32_t> q_S, q_W, q_ntiles, q_cap, q_tile_base, q_rank, q_big;
+    // per item
+    DevBuf<uint32_t> it_kb, it_nk, it_sbase;
+    // spans / cuts / work / tiles
+    DevBuf<uint64_t> span_beg;
+    DevBuf<uint32_t> cuts;
+    DevBuf<uint32_t> work_q, work_t;
+    DevBuf<uint32_t> tile_len;
+    DevBuf<genie_entry> tile_out;
+    // status
+    DevBuf<unsigned long long> status;
+    unsigned long long* h_status = nullptr;  // pinned mirror
+    // host-API staging (device copies of caller buffers)
+    DevBuf<uint32_t> d_qid, d_k, d_lo, d_hi;
+    DevBuf<uint64_t> d_item_off;
+    DevBuf<uint16_t> d_dim;
+    DevBuf<genie_entry> d_out;
+    DevBuf<uint32_t> d_out_len, d_out_thr;
+    // segmented-sort scratch for rows longer than kSortCap
+    DevBuf<uint64_t> sort_keys, sort_keys_alt;
+    DevBuf<uint64_t> sort_seg_begin, sort_seg_end;
+    DevBuf<unsigned char> sort_tmp;
+
+    size_t cap_q = 0, cap_items = 0, cap_spans = 0, cap_cuts = 0, cap_work = 0, cap_tout = 0;
+};
+
+}  // namespace genie
+
+struct genie_index {
+    int device = 0;
+    uint32_t n = 0;
+    uint64_t K = 0, P = 0;
+    uint32_t id_offset = 0;
+    int sms = 148;
+    genie::DevBuf<uint64_t> keys, key_off;
+    genie::DevBuf<uint32_t> postings;  // padded for aligned 16-byte tail loads
+    genie::DevBuf<uint32_t> dim_mult;  // 65536
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};
+    genie::Workspace ws;
+    // last device batch
+    uint32_t last_Q = 0;
+    uint32_t last_launches = 0;
+    bool last_timed = false;
+    genie_config last_cfg{};
+};
+
+namespace genie {
+
+// Launches the whole device pipeline for a batch already resident on the
+// device.  Does not synchronise.  Implemented in genie_query.cu.
+void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const uint32_t* d_qid,
+                  const uint32_t* d_k, const uint64_t* d_item_off, const uint16_t* d_dim,
+                  const uint32_t* d_lo, const uint32_t* d_hi, uint32_t total_items,
+                  uint32_t max_k, uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
+                  uint32_t* d_out_thr, cudaStream_t stream, bool timed);
+
+// Reads the status block (synchronises) and converts it to a status code +
+// message.  Grows the workspace and returns GENIE_RETRY on overflow.
+int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
+                 const uint32_t* h_qid /* optional, for messages */);
+
+void ensure_device(int device);
+
+}  // namespace genie
