@@ -66,8 +66,12 @@ typedef struct {
     uint32_t max_spans_per_task; /* accepted for API parity; must be > 0 */
     uint32_t tile_bytes;         /* shared-memory counter bytes per object tile (0: default) */
     uint32_t ctas_per_sm;        /* persistent scan CTAs per SM (0: default) */
-    uint32_t flags;              /* reserved, 0 */
+    uint32_t flags;              /* GENIE_FLAG_* */
 } genie_config;
+
+/* genie_config.flags: record CUDA events around the device stages on the
+ * launching stream (read back with genie_last_stage_ns after synchronising). */
+#define GENIE_FLAG_STAGE_EVENTS 1u
 
 /* mcx::StageTimings (engine.hpp:44-50), measured with CUDA events on the
  * handle's stream (device stages) and the host clock (total). */
@@ -168,6 +172,12 @@ int genie_query_status(genie_index* ix, genie_batch_stats* stats, char* err, siz
 
 /* Kernels launched by the last batch (for launch accounting). */
 uint32_t genie_last_launch_count(const genie_index* ix);
+
+/* Device stage times of the last batch launched with GENIE_FLAG_STAGE_EVENTS
+ * (or through genie_query_batch with timings): lookup = resolve + plan + cut,
+ * match = the fused scan / c-PQ / tile-select kernel, merge = the per-query
+ * merge kernels.  total_ns = sum of the device stages.  Synchronises. */
+int genie_last_stage_ns(genie_index* ix, genie_stage_ns* out, char* err, size_t errlen);
 
 /* mcx::merge_topk (engine.hpp:158-177) over device-resident candidate lists,
  * batched over queries: list l of query q is d_in[(q*L + l)*in_stride ...]

@@ -28,6 +28,7 @@ GENIE_ERR_INVARIANT = 3
 GENIE_ERR_CUDA = 4
 GENIE_ERR_NCCL = 5
 GENIE_RETRY = 6
+GENIE_FLAG_STAGE_EVENTS = 1
 
 
 class Entry(C.Structure):
@@ -89,6 +90,7 @@ ENGINE_SYMBOLS = {
                                            C.c_size_t]),
     "genie_query_status": (C.c_int, [vp, C.POINTER(BatchStats), C.c_char_p, C.c_size_t]),
     "genie_last_launch_count": (C.c_uint32, [vp]),
+    "genie_last_stage_ns": (C.c_int, [vp, C.POINTER(StageNs), C.c_char_p, C.c_size_t]),
     "genie_merge_topk_device": (C.c_int, [vp, C.c_uint32, C.c_uint32, vp, vp, C.c_uint32, vp, C.c_uint32,
                                           vp, vp, vp, vp, C.c_char_p, C.c_size_t]),
     "genie_merge_topk": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.POINTER(Entry), u32p, C.c_uint32, u32p,

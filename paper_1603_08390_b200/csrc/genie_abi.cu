@@ -167,10 +167,10 @@ int genie_query_batch_device(genie_index* ix, const genie_config* cfg_in, uint32
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix->stream;
         launch_batch(ix, cfg, Q, d_qid, d_k, d_item_off, d_item_dim, d_item_lo, d_item_hi, total_items,
                      max_k, std::max<uint32_t>(out_stride, 1), d_out, d_out_len, d_out_threshold, s,
-                     false);
+                     (cfg.flags & GENIE_FLAG_STAGE_EVENTS) != 0);
         if (s != ix->stream) {
             // make genie_query_status's synchronisation cover the caller's stream
-            cudaEvent_t e = ix->ev[4];
+            cudaEvent_t e = ix->ev[5];
             GENIE_CUDA(cudaEventRecord(e, s));
             GENIE_CUDA(cudaStreamWaitEvent(ix->stream, e, 0));
         }
@@ -190,6 +190,25 @@ int genie_query_status(genie_index* ix, genie_batch_stats* stats, char* err, siz
 
 uint32_t genie_last_launch_count(const genie_index* ix) { return ix ? ix->last_launches : 0; }
 
+int genie_last_stage_ns(genie_index* ix, genie_stage_ns* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&]() -> int {
+        if (!ix || !out) throw Error(GENIE_ERR_CONTRACT, "null argument");
+        if (!ix->last_timed) throw Error(GENIE_ERR_CONTRACT, "last batch was not launched with stage events");
+        ensure_device(ix->device);
+        GENIE_CUDA(cudaEventSynchronize(ix->ev[3]));
+        float a = 0, b = 0, c = 0;
+        GENIE_CUDA(cudaEventElapsedTime(&a, ix->ev[0], ix->ev[1]));
+        GENIE_CUDA(cudaEventElapsedTime(&b, ix->ev[1], ix->ev[2]));
+        GENIE_CUDA(cudaEventElapsedTime(&c, ix->ev[2], ix->ev[3]));
+        out->lookup_ns = static_cast<uint64_t>(double(a) * 1e6);
+        out->match_ns = static_cast<uint64_t>(double(b) * 1e6);
+        out->select_ns = 0;
+        out->merge_ns = static_cast<uint64_t>(double(c) * 1e6);
+        out->total_ns = out->lookup_ns + out->match_ns + out->merge_ns;
+        return GENIE_OK;
+    });
+}
+
 int genie_merge_topk_device(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
                             const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
                             uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
@@ -203,8 +222,8 @@ int genie_merge_topk_device(genie_index* ix, uint32_t Q, uint32_t L, const genie
         launch_list_merge(ix, Q, L, d_in, d_in_len, in_stride, d_k, out_stride, d_out, d_out_len,
                           d_out_threshold, max_rows, s);
         if (s != ix->stream) {
-            GENIE_CUDA(cudaEventRecord(ix->ev[4], s));
-            GENIE_CUDA(cudaStreamWaitEvent(ix->stream, ix->ev[4], 0));
+            GENIE_CUDA(cudaEventRecord(ix->ev[5], s));
+            GENIE_CUDA(cudaStreamWaitEvent(ix->stream, ix->ev[5], 0));
         }
         return GENIE_OK;
     });

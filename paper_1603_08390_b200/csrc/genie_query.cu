@@ -61,7 +61,8 @@ struct BatchParams {
     uint32_t selector;
     // workspace
     uint64_t *q_bound, *q_P, *q_span_base, *q_cut_base, *q_out_base;
-    uint32_t *q_S, *q_W, *q_ntiles, *q_cap, *q_tile_base, *q_rank, *q_big;
+    uint32_t *q_S, *q_W, *q_ntiles, *q_cap, *q_tile_base, *q_rank, *q_big, *q_floor;
+    uint32_t ht_slots;
     uint32_t *it_kb, *it_nk, *it_sbase;
     uint64_t* span_beg;
     uint32_t* cuts;
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
     p.q_bound[q] = bound;
     p.q_S[q] = carry;
     p.q_P[q] = P;
+    p.q_floor[q] = 0;
     p.q_W[q] = W;
     p.q_ntiles[q] = nt;
     if (nt) atomicAdd(&p.st[ST_TOTAL_POSTINGS], static_cast<unsigned long long>(P));
@@ -307,15 +309,16 @@ enum ScalarSlot {
     SC_T = 7,
     SC_ABOVE = 8,
     SC_DONE = 9,
+    SC_FLOOR = 10,
     SC_WORDS = 16
 };
 
-__device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t tile_bytes) {
+__device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t tile_bytes, uint32_t ht_slots) {
     ScanSmem s;
     s.cnt = reinterpret_cast<uint32_t*>(base);
     base += tile_bytes;
     s.ht = reinterpret_cast<uint64_t*>(base);
-    base += kHtMaxSlots * sizeof(uint64_t);
+    base += ht_slots * sizeof(uint64_t);
     s.s_beg = reinterpret_cast<uint64_t*>(base);
     base += kSpanBatch * sizeof(uint64_t);
     s.sums = reinterpret_cast<unsigned long long*>(base);
@@ -330,8 +333,8 @@ __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t tile_bytes) {
     return s;
 }
 
-inline size_t scan_smem_bytes(uint32_t tile_bytes) {
-    return tile_bytes + kHtMaxSlots * 8 + kSpanBatch * 8 + 32 * 8 + kZaMax * 4 + kSpanBatch * 4 * 2 +
+inline size_t scan_smem_bytes(uint32_t tile_bytes, uint32_t ht_slots) {
+    return tile_bytes + size_t(ht_slots) * 8 + kSpanBatch * 8 + 32 * 8 + kZaMax * 4 + kSpanBatch * 4 * 2 +
            SC_WORDS * 4;
 }
 
@@ -348,7 +351,7 @@ __device__ __forceinline__ uint64_t pack_slot(uint32_t id, uint32_t v, uint32_t 
 // raise value keeping age, dead resident (value + 1 < AT) -> overwrite,
 // younger resident -> displace and keep probing with it.  Returns false when
 // the table is full (the caller falls back to an exact histogram select).
-__device__ bool ht_insert(uint64_t* ht, uint32_t cap, uint32_t id, uint32_t value,
+__device__ __forceinline__ bool ht_insert(uint64_t* ht, uint32_t cap, uint32_t id, uint32_t value,
                           uint32_t cur_at) {
     const uint32_t mask = cap - 1;
     uint64_t carried = pack_slot(id, value, 0);
@@ -429,55 +432,82 @@ struct ItemCtx {
     bool gate;
 };
 
+// The c-PQ admission path (cpq.hpp:294-301): the new value passed the
+// register copy of the gate, so re-check against the live AuditThreshold,
+// insert into the table, bump ZA[val] and advance AT while ZA[AT] >= k
+// (cpq.hpp:374-389).  Rare once AT has climbed; kept out of line so the scan
+// loop stays small.  Returns the refreshed gate comparand.
+template <int W>
+__device__ __noinline__ uint32_t cpq_admit(uint64_t* ht, uint32_t* za, uint32_t* scal, uint32_t ht_cap,
+                                           uint32_t bound, uint32_t kq, uint32_t local, uint32_t old,
+                                           uint32_t sh) {
+    constexpr uint32_t kMask = (W == 32) ? 0xffffffffu : ((1u << W) - 1u);
+    const uint32_t val = ((old >> sh) & kMask) + 1;
+    volatile uint32_t* s_at = scal + SC_AT;
+    uint32_t a = *s_at;
+    if (val >= a) {
+        if (!ht_insert(ht, ht_cap, local, val, a)) scal[SC_OVF] = 1;
+        atomicAdd(&za[val], 1u);
+        a = *s_at;
+        while (a <= bound && reinterpret_cast<volatile uint32_t*>(za)[a] >= kq) {
+            atomicCAS(scal + SC_AT, a, a + 1);
+            a = *s_at;
+        }
+    }
+    return (a - 1) << (32 - W);
+}
+
 // Count every posting of [ua, ub) (absolute positions) into the tile's
 // shared counters; with the gate on, feed the c-PQ with each new value.
+//
+// Per posting: one shared atomicAdd of 1 << shift on the packed word (exact:
+// the query's max_count_bound keeps every counter below 2^W, so no carry
+// crosses lanes), then the gate test "old value >= AT - 1" done on the word
+// shifted so the counter sits in the top W bits (one shift + one compare).
 template <int W, bool GATE>
 __device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings, uint64_t ua,
                                            uint64_t ub, const ItemCtx& it, const ScanSmem& sm) {
-    using Pk = Packing<W>;
+    constexpr uint32_t kPer = 32 / W, kTop = 32 - W;
     constexpr int UNR = 4;
-    const int lane = threadIdx.x & 31;
-    const uint64_t base = ua & ~3ull;
-    uint32_t at = GATE ? *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]) : 0;
-    for (uint64_t p0 = base + uint64_t(lane) * 4; p0 < ub; p0 += 128 * UNR) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t* base = postings + (ua & ~3ull);
+    const uint32_t lo = static_cast<uint32_t>(ua & 3ull);
+    const uint32_t len = static_cast<uint32_t>(ub - (ua & ~3ull));
+    uint32_t* cnt = sm.cnt;
+    const uint32_t tlo = it.tile_lo;
+    volatile uint32_t* s_at = sm.scal + SC_AT;
+    uint32_t gate = 0;
+    if constexpr (GATE) gate = (*s_at - 1) << kTop;
+    for (uint32_t off = lane * 4; off < len; off += 128 * UNR) {
         uint4 v[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-            const uint64_t pp = p0 + uint64_t(u) * 128;
-            v[u] = pp < ub ? ldg_stream_v4(postings + pp) : make_uint4(0, 0, 0, 0);
+            const uint32_t o = off + u * 128;
+            v[u] = o < len ? ldg_stream_v4(base + o) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-            const uint64_t pp = p0 + uint64_t(u) * 128;
-            const uint32_t e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            const uint32_t o = off + u * 128;
+            // valid elements of [o, o + 4): positions in [lo, len)
+            const uint32_t hi_n = len > o ? min(len - o, 4u) : 0u;
+            const uint32_t lo_n = lo > o ? lo - o : 0u;
+            const uint32_t m = ((1u << hi_n) - 1u) & ~((1u << lo_n) - 1u);
+            const uint32_t x[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const uint64_t pos = pp + e;
-                if (pos >= ua && pos < ub) {
-                    const uint32_t local = e4[e] - it.tile_lo;
-                    const uint32_t sh = (local % Pk::kPer) * W;
-                    const uint32_t old = atomicAdd(&sm.cnt[local / Pk::kPer], 1u << sh);
+                if (m & (1u << e)) {
+                    const uint32_t local = x[e] - tlo;
+                    const uint32_t sh = (local % kPer) * W;
+                    const uint32_t old = atomicAdd(&cnt[local / kPer], 1u << sh);
                     if constexpr (GATE) {
-                        const uint32_t val = ((old >> sh) & Pk::kMask) + 1;
-                        if (val >= at) {
-                            // cpq.hpp:294-301: insert, bump ZA[val], advance AT
-                            const uint32_t cur =
-                                *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]);
-                            if (!ht_insert(sm.ht, it.ht_cap, local, val, cur)) sm.scal[SC_OVF] = 1;
-                            atomicAdd(&sm.za[val], 1u);
-                            uint32_t a = *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]);
-                            while (a <= it.bound &&
-                                   *reinterpret_cast<volatile uint32_t*>(&sm.za[a]) >= it.kq) {
-                                atomicCAS(&sm.scal[SC_AT], a, a + 1);
-                                a = *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]);
-                            }
-                            at = a;
-                        }
+                        if ((old << (kTop - sh)) >= gate)
+                            gate = cpq_admit<W>(sm.ht, sm.za, sm.scal, it.ht_cap, it.bound, it.kq, local,
+                                                old, sh);
                     }
                 }
             }
+            if constexpr (GATE) gate = (*s_at - 1) << kTop;
         }
-        if constexpr (GATE) at = *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_AT]);
     }
 }
 
@@ -522,7 +552,7 @@ __device__ void emit_ties(const BatchParams& p, const ItemCtx& it, const ScanSme
 // tile, zeros included (0 if fewer than k non-zero), then every count > T
 // and the first ties at T in ascending id.
 template <int W>
-__device__ void hist_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm) {
+__device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm) {
     using Pk = Packing<W>;
     const int warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
@@ -623,6 +653,7 @@ __device__ void hist_select(const BatchParams& p, const ItemCtx& it, const ScanS
         }
         seen += total;
     }
+    return T;
 }
 
 template <int W>
@@ -643,7 +674,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     const uint64_t want2 = 2ull * it.kq * it.bound;
     const uint64_t want = want2 < 2 ? 2 : want2;
     const uint64_t htc = bit_ceil64(want);
-    it.ht_cap = static_cast<uint32_t>(htc < kHtMaxSlots ? htc : kHtMaxSlots);
+    it.ht_cap = static_cast<uint32_t>(htc < p.ht_slots ? htc : p.ht_slots);
 
     // setup: zero counters, empty table, ZA, AT = 1 (cpq.hpp:281-292)
     {
@@ -655,11 +686,16 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
             for (uint32_t i = threadIdx.x; i <= it.bound; i += blockDim.x) sm.za[i] = 0;
         }
         if (threadIdx.x == 0) {
-            sm.scal[SC_AT] = 1;
+            // AT starts at the query's floor: a lower bound on the global k-th
+            // count published by this query's finished tiles (see extract)
+            const uint32_t floor = it.gate ? *reinterpret_cast<volatile uint32_t*>(&p.q_floor[q]) : 0u;
+            sm.scal[SC_AT] = floor > 1 ? floor : 1;
+            sm.scal[SC_FLOOR] = floor;
             sm.scal[SC_OVF] = 0;
             sm.scal[SC_NOUT] = 0;
         }
     }
+    __syncthreads();
     const uint32_t S = p.q_S[q];
     const uint32_t nt = p.q_ntiles[q];
     const uint64_t cb = p.q_cut_base[q];
@@ -731,19 +767,28 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         }
         __syncthreads();
         const uint32_t n_above = sm.scal[SC_NOUT];
-        if (thr > 0 && n_above < it.kq) emit_ties<W>(p, it, sm, thr, it.kq - n_above);
+        const uint32_t floor = sm.scal[SC_FLOOR];
+        // thr >= floor: thr is the tile's true k-th count -> tie fill and
+        // publish it as the query's new floor.  thr < floor (AT never left
+        // the floor): fewer than k objects reach the floor here; they are all
+        // in the table and nothing below the floor can make the global top-k.
+        if (thr > 0 && thr >= floor) {
+            if (n_above < it.kq) emit_ties<W>(p, it, sm, thr, it.kq - n_above);
+            if (threadIdx.x == 0) atomicMax(&p.q_floor[q], thr);
+        }
     } else {
         if (it.gate && threadIdx.x == 0) atomicAdd(&p.st[ST_FALLBACK], 1ull);
-        hist_select<W>(p, it, sm);
+        const uint32_t T_t = hist_select<W>(p, it, sm);
+        if (it.gate && T_t > 0 && threadIdx.x == 0) atomicMax(&p.q_floor[q], T_t);
     }
     __syncthreads();
     if (threadIdx.x == 0) p.tile_len[p.q_tile_base[q] + t] = sm.scal[SC_NOUT];
 }
 
-__global__ void __launch_bounds__(kScanThreads, 1)
+__global__ void __launch_bounds__(kScanThreads, 2)
     k_scan(BatchParams p, uint32_t tile_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const ScanSmem sm = carve(smem, tile_bytes);
+    const ScanSmem sm = carve(smem, tile_bytes, p.ht_slots);
     if (p.st[ST_OVERFLOW]) return;
     const uint64_t total = p.st[ST_TOTAL_WORK];
     for (;;) {
@@ -1126,6 +1171,7 @@ static void reserve_workspace(genie_index* ix, uint32_t Q, uint32_t items, uint3
         w.q_tile_base.reserve(c);
         w.q_rank.reserve(c);
         w.q_big.reserve(c);
+        w.q_floor.reserve(c);
         w.cap_q = c;
     }
     if (items > w.cap_items || !w.it_kb.p) {
@@ -1290,6 +1336,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.q_tile_base = w.q_tile_base.p;
     p.q_rank = w.q_rank.p;
     p.q_big = w.q_big.p;
+    p.q_floor = w.q_floor.p;
     p.it_kb = w.it_kb.p;
     p.it_nk = w.it_nk.p;
     p.it_sbase = w.it_sbase.p;
@@ -1317,11 +1364,12 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         k_plan<<<1, 1024, 0, s>>>(p);
         k_worklist<<<(Q + 255) / 256, 256, 0, s>>>(p);
         launches += 3;
-        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
         const int sms = ix->sms;
         k_cut<<<sms * 8, 256, 0, s>>>(p);
         ++launches;
-        const size_t smem = scan_smem_bytes(tile_bytes);
+        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
+        p.ht_slots = tile_bytes > (64u << 10) ? kHtMaxSlots : kHtMaxSlots / 2;
+        const size_t smem = scan_smem_bytes(tile_bytes, p.ht_slots);
         static thread_local size_t configured = 0;
         if (configured < smem) {
             GENIE_CUDA(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1355,11 +1403,12 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
             segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, ix->id_offset, s);
             launches += 3;
         }
+        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
     } else if (timed) {
         GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
         GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
+        GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
     }
-    if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
     GENIE_CUDA(cudaMemcpyAsync(w.h_status, w.status.p, ST_WORDS * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s));
     GENIE_CUDA(cudaGetLastError());

@@ -10,7 +10,7 @@ constexpr uint32_t kScanThreads = 512;        // 16 warps per scan CTA
 constexpr uint32_t kSpanBatch = 512;          // spans staged in shared memory per pass
 constexpr uint32_t kHtMaxSlots = 4096;        // shared-memory Robin Hood table (32 KB)
 constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shared memory (W <= 8)
-constexpr uint32_t kDefaultTileBytes = 128u << 10;
+constexpr uint32_t kDefaultTileBytes = 64u << 10;
 constexpr uint32_t kMergeThreads = 512;
 constexpr uint32_t kSortCap = 8192;           // merge entries sorted in shared memory
 constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit
@@ -42,7 +42,7 @@ enum StatusWord : int {
 struct Workspace {
     // per query
     DevBuf<uint64_t> q_bound, q_P, q_span_base, q_cut_base, q_out_base;
-    DevBuf<uint32_t> q_S, q_W, q_ntiles, q_cap, q_tile_base, q_rank, q_big;
+    DevBuf<uint32_t> q_S, q_W, q_ntiles, q_cap, q_tile_base, q_rank, q_big, q_floor;
     // per item
     DevBuf<uint32_t> it_kb, it_nk, it_sbase;
     // spans / cuts / work / tiles

@@ -153,8 +153,9 @@ class Results:
 
 
 def config(selector: int = 0, span_chunk: Optional[int] = None, max_spans_per_task: int = 2,
-           tile_bytes: int = 0, ctas_per_sm: int = 0) -> N.Config:
+           tile_bytes: int = 0, ctas_per_sm: int = 0, stage_events: bool = False) -> N.Config:
     c = N.engine().genie_config_default()
+    c.flags = N.GENIE_FLAG_STAGE_EVENTS if stage_events else 0
     c.selector = selector
     if span_chunk is not None:
         c.span_chunk = span_chunk
@@ -266,13 +267,19 @@ class DeviceIndex:
 
     # queries -----------------------------------------------------------------
     def query(self, batch: QueryBatch, cfg: Optional[N.Config] = None, stride: Optional[int] = None,
-              timings: bool = False, want_bound: bool = False) -> Results:
-        """execute_batch (engine.hpp:184-304) with host buffers."""
+              timings: bool = False, want_bound: bool = False, out=None, copy: bool = True) -> Results:
+        """execute_batch (engine.hpp:184-304) with host buffers.  `out` may hold
+        preallocated (pinned) result buffers (entries [Q, stride, 2] u32, length
+        [Q] u32, threshold [Q] u32)."""
         Q = len(batch)
         stride = int(stride if stride is not None else max(batch.max_k, 1))
-        ent = np.zeros((Q, stride, 2), dtype=np.uint32)
-        ln = np.zeros(Q, np.uint32)
-        thr = np.zeros(Q, np.uint32)
+        if out is not None:
+            ent, ln, thr = out
+            assert ent.shape == (Q, stride, 2) and ent.dtype == np.uint32 and ent.flags.c_contiguous
+        else:
+            ent = np.zeros((Q, stride, 2), dtype=np.uint32)
+            ln = np.zeros(Q, np.uint32)
+            thr = np.zeros(Q, np.uint32)
         bound = np.zeros(Q, np.uint64) if want_bound else None
         st = N.StageNs()
         stats = N.BatchStats()
@@ -287,7 +294,15 @@ class DeviceIndex:
         check(rc, err)
         tdict = {f: getattr(st, f) for f, _ in N.StageNs._fields_} if timings else None
         sdict = {f: getattr(stats, f) for f, _ in N.BatchStats._fields_}
+        if not copy:
+            return Results(batch.qid, ent[:, :, 0], ent[:, :, 1], ln, thr, bound, tdict, sdict)
         return Results(batch.qid.copy(), ent[:, :, 0].copy(), ent[:, :, 1].copy(), ln, thr, bound, tdict, sdict)
+
+    def stage_ns(self) -> dict:
+        """Device stage times of the last batch launched with stage events."""
+        st, err = N.StageNs(), _errbuf()
+        check(self._lib.genie_last_stage_ns(self._h, C.byref(st), err, len(err)), err)
+        return {f: getattr(st, f) for f, _ in N.StageNs._fields_}
 
     def query_device(self, d: dict, cfg: Optional[N.Config] = None, stream: Optional[int] = None) -> int:
         """Enqueue a batch whose arrays are torch CUDA tensors in `d` (keys qid,
