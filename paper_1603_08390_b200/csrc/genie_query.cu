@@ -464,17 +464,40 @@ __device__ __noinline__ uint32_t cpq_admit(uint64_t* ht, uint32_t* za, uint32_t*
 // the query's max_count_bound keeps every counter below 2^W, so no carry
 // crosses lanes), then the gate test "old value >= AT - 1" done on the word
 // shifted so the counter sits in the top W bits (one shift + one compare).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Shared-memory atomic add on a 32-bit shared-window address (no memory
+// clobber: the counters are only read after a __syncthreads()).
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t addr, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v));
+    return old;
+}
+
+// Count every posting of [ua, ub) (absolute positions) into the tile's
+// shared counters; with the gate on, feed the c-PQ with each new value.
+//
+// Per posting: one shared atomicAdd of 1 << shift on the packed word (exact:
+// the query's max_count_bound keeps every counter below 2^W, so no carry
+// crosses lanes).  Addresses are 32-bit shared-window offsets with the tile
+// origin folded into the base (tile_lo is a multiple of 32/W, so the lane
+// inside the word depends on the id alone).  The gate test "old value >=
+// AT - 1" is done on the word shifted so the counter sits in the top W bits,
+// as one max over the four postings of a 16-byte group and one compare.
 template <int W, bool GATE>
 __device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings, uint64_t ua,
                                            uint64_t ub, const ItemCtx& it, const ScanSmem& sm) {
     constexpr uint32_t kPer = 32 / W, kTop = 32 - W;
+    constexpr uint32_t kLog = W == 4 ? 3 : (W == 8 ? 2 : 1);  // log2(kPer)
     constexpr int UNR = 4;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t* base = postings + (ua & ~3ull);
     const uint32_t lo = static_cast<uint32_t>(ua & 3ull);
     const uint32_t len = static_cast<uint32_t>(ub - (ua & ~3ull));
-    uint32_t* cnt = sm.cnt;
-    const uint32_t tlo = it.tile_lo;
+    // byte address of the word holding id x: cbase + (x >> kLog) * 4 (mod 2^32)
+    const uint32_t cbase = smem_u32(sm.cnt) - ((it.tile_lo >> kLog) << 2);
     volatile uint32_t* s_at = sm.scal + SC_AT;
     uint32_t gate = 0;
     if constexpr (GATE) gate = (*s_at - 1) << kTop;
@@ -488,25 +511,46 @@ __device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
             const uint32_t o = off + u * 128;
-            // valid elements of [o, o + 4): positions in [lo, len)
-            const uint32_t hi_n = len > o ? min(len - o, 4u) : 0u;
-            const uint32_t lo_n = lo > o ? lo - o : 0u;
-            const uint32_t m = ((1u << hi_n) - 1u) & ~((1u << lo_n) - 1u);
             const uint32_t x[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            if (o >= len) continue;  // past the end for this lane
+            uint32_t old[4];
+            uint32_t m = 0xfu;
+            uint32_t top = 0;
+            if (o >= lo && o + 4 <= len) {  // full group: unconditional atomics
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if (m & (1u << e)) {
-                    const uint32_t local = x[e] - tlo;
-                    const uint32_t sh = (local % kPer) * W;
-                    const uint32_t old = atomicAdd(&cnt[local / kPer], 1u << sh);
-                    if constexpr (GATE) {
-                        if ((old << (kTop - sh)) >= gate)
-                            gate = cpq_admit<W>(sm.ht, sm.za, sm.scal, it.ht_cap, it.bound, it.kq, local,
-                                                old, sh);
-                    }
+                for (int e = 0; e < 4; ++e) {
+                    // r = kTop - shift: the counter's distance from the top of the word
+                    const uint32_t r = ((~x[e]) & (kPer - 1)) * W;
+                    old[e] = atom_add_shared(cbase + ((x[e] >> kLog) << 2), (1u << kTop) >> r);
+                    if constexpr (GATE) top = max(top, old[e] << r);
+                }
+            } else {  // edge of the range: positions in [lo, len); others add 0 to a
+                      // private word (one per lane: no bank conflicts)
+                const uint32_t hi_n = min(len - o, 4u);
+                const uint32_t lo_n = lo > o ? lo - o : 0u;
+                m = ((1u << hi_n) - 1u) & ~((1u << lo_n) - 1u);
+                const uint32_t word0 = smem_u32(sm.cnt) + lane * 4;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t r = ((~x[e]) & (kPer - 1)) * W;
+                    const bool ok = (m >> e) & 1u;
+                    old[e] = atom_add_shared(ok ? cbase + ((x[e] >> kLog) << 2) : word0,
+                                             ok ? (1u << kTop) >> r : 0u);
+                    if constexpr (GATE) top = max(top, ok ? old[e] << r : 0u);
                 }
             }
-            if constexpr (GATE) gate = (*s_at - 1) << kTop;
+            if constexpr (GATE) {
+                if (top >= gate) {  // some new value may pass: check each
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t r = ((~x[e]) & (kPer - 1)) * W;
+                        if ((m & (1u << e)) && (old[e] << r) >= gate)
+                            gate = cpq_admit<W>(sm.ht, sm.za, sm.scal, it.ht_cap, it.bound, it.kq,
+                                                x[e] - it.tile_lo, old[e], kTop - r);
+                    }
+                }
+                gate = (*s_at - 1) << kTop;
+            }
         }
     }
 }
@@ -701,47 +745,64 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     const uint64_t cb = p.q_cut_base[q];
     const uint64_t sbq = p.q_span_base[q];
     const uint32_t unit = p.unit;
+    // Work inside the tile: the staged slices cut into 128-posting groups
+    // aligned to absolute 512-byte boundaries (only a slice's first and last
+    // group are partial); warps claim runs of groups with guided
+    // self-scheduling, so chunks shrink as the tile drains and the warps reach
+    // the end-of-tile barrier together.
     for (uint32_t s0 = 0; s0 < S; s0 += kSpanBatch) {
         const uint32_t nsb = min(kSpanBatch, S - s0);
-        uint32_t units = 0;
+        uint32_t groups = 0;
         if (threadIdx.x < nsb) {
             const uint32_t s = s0 + threadIdx.x;
             const uint32_t* c = p.cuts + cb + uint64_t(s) * (nt + 1) + t;
             const uint32_t a = c[0], e = c[1];
             const uint64_t beg = p.span_beg[sbq + s] + a;
-            const uint32_t len = e - a;
             sm.s_beg[threadIdx.x] = beg;
-            sm.s_len[threadIdx.x] = len;
-            units = len ? static_cast<uint32_t>((beg + len - 1) / unit - beg / unit + 1) : 0;
+            sm.s_len[threadIdx.x] = e - a;
+            groups = e > a ? static_cast<uint32_t>(((beg + (e - a) - 1) >> 7) - (beg >> 7) + 1) : 0u;
         }
         unsigned long long total;
-        const unsigned long long ex =
-            block_exclusive_scan<unsigned long long>(units, sm.sums, total);
+        const unsigned long long ex = block_exclusive_scan<unsigned long long>(groups, sm.sums, total);
         if (threadIdx.x < nsb) sm.s_upref[threadIdx.x] = static_cast<uint32_t>(ex);
         if (threadIdx.x == 0) sm.scal[SC_UCTR] = 0;
         __syncthreads();
-        const uint32_t U = static_cast<uint32_t>(total);
+        const uint32_t G = static_cast<uint32_t>(total);
         const int lane = threadIdx.x & 31;
+        const uint32_t nwarps = blockDim.x >> 5;
+        const uint32_t max_chunk = max(1u, unit >> 7);
         for (;;) {
-            uint32_t u = 0;
-            if (lane == 0) u = atomicAdd(&sm.scal[SC_UCTR], 1u);
-            u = __shfl_sync(0xffffffffu, u, 0);
-            if (u >= U) break;
-            // slice holding unit u: last si with upref[si] <= u
-            uint32_t lo = 0, hi = nsb;
-            while (lo < hi) {
-                const uint32_t m = (lo + hi) >> 1;
-                if (sm.s_upref[m] <= u) lo = m + 1;
-                else hi = m;
+            uint32_t g0 = 0, chunk = 0;
+            if (lane == 0) {
+                const uint32_t cur = *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_UCTR]);
+                const uint32_t rem = cur < G ? G - cur : 0u;
+                chunk = min(max_chunk, max(1u, rem / (2 * nwarps)));
+                g0 = rem ? atomicAdd(&sm.scal[SC_UCTR], chunk) : G;
             }
-            const uint32_t si = lo - 1;
-            const uint64_t beg = sm.s_beg[si];
-            const uint64_t end = beg + sm.s_len[si];
-            const uint64_t j = u - sm.s_upref[si];
-            const uint64_t ua = max(beg, (beg / unit + j) * unit);
-            const uint64_t ub = min(end, (beg / unit + j + 1) * unit);
-            if (it.gate) scan_range<W, true>(p.postings, ua, ub, it, sm);
-            else scan_range<W, false>(p.postings, ua, ub, it, sm);
+            g0 = __shfl_sync(0xffffffffu, g0, 0);
+            chunk = __shfl_sync(0xffffffffu, chunk, 0);
+            if (g0 >= G) break;
+            const uint32_t g1 = min(G, g0 + chunk);
+            while (g0 < g1) {
+                // slice holding group g0: last si with upref[si] <= g0
+                uint32_t lo = 0, hi = nsb;
+                while (lo < hi) {
+                    const uint32_t m = (lo + hi) >> 1;
+                    if (sm.s_upref[m] <= g0) lo = m + 1;
+                    else hi = m;
+                }
+                const uint32_t si = lo - 1;
+                const uint64_t beg = sm.s_beg[si];
+                const uint64_t end = beg + sm.s_len[si];
+                const uint32_t gs = (si + 1 < nsb ? sm.s_upref[si + 1] : G);  // slice's group end
+                const uint32_t take = min(g1, gs) - g0;
+                const uint64_t gb = (beg >> 7) + (g0 - sm.s_upref[si]);
+                const uint64_t ua = max(beg, gb << 7);
+                const uint64_t ub = min(end, (gb + take) << 7);
+                if (it.gate) scan_range<W, true>(p.postings, ua, ub, it, sm);
+                else scan_range<W, false>(p.postings, ua, ub, it, sm);
+                g0 += take;
+            }
         }
         __syncthreads();
     }
