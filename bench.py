@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--selector", type=int, default=0, help="0 cpq, 1 bucket/histogram ablation")
     ap.add_argument("--tile-bytes", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--span-chunk", type=int, default=None, help="postings per warp work unit (result-invariant)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=0, help="queries per reference step (0: auto)")
     return ap.parse_args()
@@ -218,7 +219,7 @@ def main_genie(args):
     K = int(qb.max_k)
     stride = K
     cfg = config(selector=args.selector, tile_bytes=args.tile_bytes, ctas_per_sm=args.ctas_per_sm,
-                 stage_events=True)
+                 span_chunk=args.span_chunk, stage_events=True)
     # device-resident query batch
     d = {
         "qid": torch.from_numpy(qb.qid.astype(np.int32)).to(dev),
@@ -312,7 +313,8 @@ def main_genie(args):
     from paper_1603_08390_b200.engine import QueryBatch
     hb = QueryBatch(pin(qb.qid), pin(qb.k), pin(qb.item_off), pin(qb.dim), pin(qb.lo), pin(qb.hi))
     hout = (pin(np.zeros((Q, stride, 2), np.uint32)), pin(np.zeros(Q, np.uint32)), pin(np.zeros(Q, np.uint32)))
-    e2e_cfg = config(selector=args.selector, tile_bytes=args.tile_bytes, ctas_per_sm=args.ctas_per_sm)
+    e2e_cfg = config(selector=args.selector, tile_bytes=args.tile_bytes, ctas_per_sm=args.ctas_per_sm,
+                     span_chunk=args.span_chunk)
     for _ in range(2):
         res = ix.query(hb, e2e_cfg, stride=stride, out=hout, copy=False)
     e2e_times = []

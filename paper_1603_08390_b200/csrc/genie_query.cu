@@ -715,10 +715,13 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     it.cap = p.q_cap[q];
     it.out_base = p.q_out_base[q] + uint64_t(t) * it.cap;
     it.gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
-    const uint64_t want2 = 2ull * it.kq * it.bound;
-    const uint64_t want = want2 < 2 ? 2 : want2;
-    const uint64_t htc = bit_ceil64(want);
-    it.ht_cap = static_cast<uint32_t>(htc < p.ht_slots ? htc : p.ht_slots);
+    // bit_ceil(max(2 k bound, 2)) (cpq.hpp:137-138, 283), capped by the shared table
+    {
+        const uint64_t want = max(2ull * it.kq * it.bound, 2ull);
+        const uint32_t lz = __clzll(want - 1);
+        const uint64_t htc = lz == 0 ? (1ull << 63) : (1ull << (64 - lz));
+        it.ht_cap = static_cast<uint32_t>(htc < p.ht_slots ? htc : p.ht_slots);
+    }
 
     // setup: zero counters, empty table, ZA, AT = 1 (cpq.hpp:281-292)
     {
