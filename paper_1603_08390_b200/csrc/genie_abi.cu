@@ -79,8 +79,9 @@ int genie_query_batch(genie_index* ix, const genie_config* cfg_in, uint32_t Q, c
         validate_queries(Q, qid, k, item_off, item_dim, item_lo, item_hi);
         uint32_t max_k = 0;
         for (uint32_t q = 0; q < Q; ++q) max_k = std::max(max_k, k[q]);
-        if (Q && out_stride < max_k)
-            throw Error(GENIE_ERR_CONTRACT, "out_stride must be >= the largest k");
+        // a row never holds more than min(k, n) entries
+        if (Q && out_stride < std::min<uint64_t>(max_k, std::max<uint32_t>(ix ? ix->n : 0, 1)))
+            throw Error(GENIE_ERR_CONTRACT, "out_stride must be >= min(largest k, num_objects)");
         ensure_device(ix->device);
         Workspace& w = ix->ws;
         cudaStream_t s = ix->stream;
@@ -162,7 +163,8 @@ int genie_query_batch_device(genie_index* ix, const genie_config* cfg_in, uint32
         validate_config(cfg);
         if (!ix) throw Error(GENIE_ERR_CONTRACT, "null index");
         if (Q >= (1u << 21)) throw Error(GENIE_ERR_CONTRACT, "batch exceeds 2^21 queries");
-        if (Q && out_stride < max_k) throw Error(GENIE_ERR_CONTRACT, "out_stride must be >= max_k");
+        if (Q && out_stride < std::min<uint64_t>(max_k, std::max<uint32_t>(ix->n, 1)))
+            throw Error(GENIE_ERR_CONTRACT, "out_stride must be >= min(max_k, num_objects)");
         ensure_device(ix->device);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix->stream;
         launch_batch(ix, cfg, Q, d_qid, d_k, d_item_off, d_item_dim, d_item_lo, d_item_hi, total_items,

@@ -272,7 +272,7 @@ class DeviceIndex:
         preallocated (pinned) result buffers (entries [Q, stride, 2] u32, length
         [Q] u32, threshold [Q] u32)."""
         Q = len(batch)
-        stride = int(stride if stride is not None else max(batch.max_k, 1))
+        stride = int(stride if stride is not None else max(min(batch.max_k, self.num_objects), 1))
         if out is not None:
             ent, ln, thr = out
             assert ent.shape == (Q, stride, 2) and ent.dtype == np.uint32 and ent.flags.c_contiguous

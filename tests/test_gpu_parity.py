@@ -1,11 +1,17 @@
-"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
-same seeded inputs.  Bit-exact: entries, thresholds and hash_results."""
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+results (golden fixtures) and the CPU oracle on the same seeded inputs.
+Bit-exact: entries, thresholds and hash_results (engine.hpp:141-153)."""
+import json
+from pathlib import Path
+
 import numpy as np
 import pytest
 
-from paper_1603_08390_b200 import DeviceIndex, config, synth
+from paper_1603_08390_b200 import CSR, ContractError, DeviceIndex, QueryBatch, config, merge_lists, synth
+from tests.golden_util import config_dataset
 
 pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
 
 
 def assert_same(got, want, label=""):
@@ -15,31 +21,223 @@ def assert_same(got, want, label=""):
         assert got.row(q) == want.row(q), f"{label}: query {q} differs"
 
 
-@pytest.mark.parametrize("seed", range(12))
+def test_golden_instances_equal_reference(gpu):
+    g = np.load(GOLD / "random_instances.npz")
+    for i in range(int(g["count"][0])):
+        p = f"i{i}_"
+        csr = CSR(int(g[p + "csr_n"][0]), g[p + "keys"], g[p + "key_off"], g[p + "postings"])
+        qb = QueryBatch(*(g[p + "q_" + f] for f in ("qid", "k", "item_off", "dim", "lo", "hi")))
+        ix = DeviceIndex.from_csr(csr, device=gpu)
+        for sel in (0, 1, 2):
+            r = ix.query(qb, config(selector=sel), stride=g[p + "ids"].shape[1])
+            assert np.array_equal(r.length, g[p + "len"]) and np.array_equal(r.threshold, g[p + "thr"]), (i, sel)
+            for q in range(len(qb)):
+                n = int(r.length[q])
+                assert np.array_equal(r.ids[q, :n], g[p + "ids"][q, :n]), (i, q, sel)
+                assert np.array_equal(r.counts[q, :n], g[p + "counts"][q, :n]), (i, q, sel)
+            assert r.hash() == int(g[p + "hash"][0])
+
+
+@pytest.mark.parametrize("name", ["adult", "tweets_200k", "tweets_1m"])
+def test_config_hash_equals_reference(gpu, name):
+    want = json.loads((GOLD / "configs.json").read_text())[name]
+    ds = config_dataset(name)
+    got = DeviceIndex.from_csr(ds.csr, device=gpu).query(ds.queries)
+    assert f"{got.hash():#018x}" == want["hash"]
+
+
+@pytest.mark.parametrize("seed", range(10))
 def test_random_instances_match_oracle(gpu, oracle, seed):
-    ds = synth.random_instance(n=50 + 97 * seed, queries=16, seed=seed + 1)
+    ds = synth.random_instance(n=50 + 997 * seed, dims=4, tokens=8 + seed, max_kw=6, queries=24, max_items=5,
+                               max_span=3, max_k=120, seed=seed + 1)
     want = oracle.index(ds.csr).execute(ds.queries)
     ix = DeviceIndex.from_csr(ds.csr, device=gpu)
     for sel in (0, 1):
-        got = ix.query(ds.queries, config(selector=sel))
-        assert_same(got, want, f"seed {seed} selector {sel}")
+        assert_same(ix.query(ds.queries, config(selector=sel)), want, f"seed {seed} selector {sel}")
 
 
 def test_adult_full_config(gpu, oracle):
     ds = synth.adult()
     want = oracle.index(ds.csr).execute(ds.queries)
-    ix = DeviceIndex.from_csr(ds.csr, device=gpu)
-    got = ix.query(ds.queries, timings=True)
+    got = DeviceIndex.from_csr(ds.csr, device=gpu).query(ds.queries, timings=True, want_bound=True)
     assert_same(got, want, "adult")
-    assert got.hash() == oracle.hash_results(want.qid, want.threshold, want.length, want.ids, want.counts)
+    assert np.array_equal(got.bound, want.bound)
     assert got.stats["postings"] == int(want.postings.sum())
+    t = got.timings
+    assert t["lookup_ns"] + t["match_ns"] + t["select_ns"] + t["merge_ns"] <= t["total_ns"]
 
 
-@pytest.mark.parametrize("tile_bytes", [0, 8192, 65536])
-def test_tweets_small_multi_tile(gpu, oracle, tile_bytes):
+@pytest.mark.parametrize("tile_bytes", [0, 4096, 8192, 65536, 131072])
+def test_tweets_multi_tile(gpu, oracle, tile_bytes):
     ds = synth.tweets(n=300_000, vocab=100_000, words=10, queries=96, k=100)
     want = oracle.index(ds.csr).execute(ds.queries)
     ix = DeviceIndex.from_csr(ds.csr, device=gpu)
     for sel in (0, 1):
-        got = ix.query(ds.queries, config(selector=sel, tile_bytes=tile_bytes))
-        assert_same(got, want, f"tweets tile {tile_bytes} sel {sel}")
+        assert_same(ix.query(ds.queries, config(selector=sel, tile_bytes=tile_bytes)), want,
+                    f"tweets tile {tile_bytes} sel {sel}")
+
+
+def test_scheduler_knobs_are_result_invariant(gpu):
+    # test_engine.cpp:134-157: results independent of the decomposition knobs
+    ds = synth.tweets(n=120_000, vocab=20_000, words=10, queries=40, k=64)
+    ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+    base = ix.query(ds.queries).hash()
+    for chunk in (128, 1000, 4096, 65536):
+        for tb in (16384, 65536):
+            for cps in (0, 1):
+                for sel in (0, 1, 2):
+                    h = ix.query(ds.queries, config(selector=sel, span_chunk=chunk, tile_bytes=tb,
+                                                    ctas_per_sm=cps)).hash()
+                    assert h == base, (chunk, tb, cps, sel)
+    with pytest.raises(ContractError, match="span_chunk and max_spans_per_task must be positive"):
+        ix.query(ds.queries, config(span_chunk=0))
+
+
+def test_wide_counters_w8_w16(gpu, oracle):
+    # many items push max_count_bound past 15 (W=8) and 255 (W=16)
+    ds = synth.random_instance(n=3000, dims=2, tokens=4, max_kw=8, queries=30, max_items=400, max_span=3,
+                               max_k=50, seed=77)
+    want = oracle.index(ds.csr).execute(ds.queries)
+    assert want.bound.max() > 255 and (want.bound < 255).any()
+    ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+    for sel in (0, 1):
+        for tb in (0, 4096):
+            assert_same(ix.query(ds.queries, config(selector=sel, tile_bytes=tb)), want, f"wide {sel} {tb}")
+
+
+@pytest.mark.parametrize("k,tile_bytes", [(1000, 4096), (20000, 0), (20000, 4096), (10**6, 0)])
+def test_large_k_and_large_unions(gpu, oracle, k, tile_bytes):
+    ds = synth.random_instance(n=50_000, dims=3, tokens=6, max_kw=5, queries=6, max_items=4, max_span=2, max_k=1,
+                               seed=9)
+    qb = ds.queries
+    qb.k[:] = k
+    want = oracle.index(ds.csr).execute(qb, stride=min(k, 60_000))
+    got = DeviceIndex.from_csr(ds.csr, device=gpu).query(qb, config(tile_bytes=tile_bytes), stride=min(k, 60_000))
+    assert_same(got, want, f"k={k}")
+
+
+def test_edge_cases(gpu, oracle):
+    # absent dims/tokens, duplicated and overlapping items, full-domain item, k > n, k = 1
+    objs = [[(0, 1), (1, 2), (2, 1)], [(0, 2), (1, 1), (2, 2)], [(0, 1), (1, 2), (2, 2)], []]
+    off = np.cumsum([0] + [len(o) for o in objs]).astype(np.uint64)
+    csr = synth.csr_from_objects(4, off, np.array([d for o in objs for d, _ in o], np.uint16),
+                                 np.array([t for o in objs for _, t in o], np.uint32))
+    queries = [(0, 1, [(0, 1, 2), (1, 1, 1), (2, 2, 3)]),      # running example -> (1,3) thr 3
+               (1, 10, [(9, 0, 100)]),                          # absent dim
+               (2, 2, [(0, 1, 1), (0, 1, 1), (0, 0, 5)]),       # duplicate + overlapping items
+               (3, 5, [(2, 0, 0xFFFFFFFF)]),                    # full domain, k > n
+               (4, 4, [(1, 7, 9)]),                             # absent tokens, k == n
+               (7, 3, [(0, 2, 2), (1, 1, 2), (2, 0, 1)])]
+    off = np.cumsum([0] + [len(q[2]) for q in queries]).astype(np.uint64)
+    its = [it for q in queries for it in q[2]]
+    qb = QueryBatch([q[0] for q in queries], [q[1] for q in queries], off, [i[0] for i in its], [i[1] for i in its],
+                    [i[2] for i in its])
+    want = oracle.index(csr).execute(qb)
+    got = DeviceIndex.from_csr(csr, device=gpu).query(qb)
+    assert_same(got, want, "edges")
+    assert got.row(0) == [(1, 3)] and got.threshold[0] == 3
+    assert got.row(1) == [] and got.threshold[1] == 0
+    assert got.row(2)[0] == (0, 3)
+    assert got.threshold[3] == 0 and got.length[3] == 3
+    assert list(got.qid) == [0, 1, 2, 3, 4, 7]
+
+
+def test_empty_batch_and_empty_index(gpu):
+    ds = synth.random_instance(n=100, seed=3)
+    ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+    empty = QueryBatch([], [], [0], [], [], [])
+    r = ix.query(empty)
+    assert r.length.shape == (0,)
+    e = DeviceIndex.from_csr(CSR(0, np.zeros(0, np.uint64), np.zeros(1, np.uint64), np.zeros(0, np.uint32)),
+                             device=gpu)
+    r = e.query(ds.queries)
+    assert np.all(r.length == 0) and np.all(r.threshold == 0)
+
+
+def test_contract_errors(gpu):
+    ds = synth.random_instance(n=100, seed=3)
+    ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+    bad = QueryBatch([5], [0], [0, 1], [0], [0], [0])
+    with pytest.raises(ContractError, match="Query 5: k must be >= 1"):
+        ix.query(bad)
+    with pytest.raises(ContractError, match="Query 6: no items"):
+        ix.query(QueryBatch([6], [1], [0, 0], [], [], []))
+    with pytest.raises(ContractError, match="lo 3 > hi 2"):
+        ix.query(QueryBatch([6], [1], [0, 1], [0], [3], [2]))
+    # a bound above 0xffff is a ContractError at setup (engine.hpp:230-233)
+    d, t = int(ds.csr.keys[0]) >> 32, int(ds.csr.keys[0]) & 0xFFFFFFFF
+    n_items = 70_000
+    big = QueryBatch([0, 41], [1, 1], [0, 1, 1 + n_items], [d] * (1 + n_items), [t] * (1 + n_items),
+                     [t] * (1 + n_items))
+    with pytest.raises(ContractError, match=r"query 41 \(setup\): match-count bound 70000 exceeds the counter range"):
+        ix.query(big)
+
+
+def test_shards_merge_equals_whole(gpu, oracle):
+    # execute_partitioned semantics (engine.hpp:308-347) with device shards + device merge
+    ds = synth.tweets(n=200_000, vocab=30_000, words=10, queries=50, k=100)
+    want = oracle.index(ds.csr).execute(ds.queries)
+    world = 3
+    Q, K = len(ds.queries), 100
+    ids = np.zeros((Q, world, K), np.uint32)
+    cnt = np.zeros((Q, world, K), np.uint32)
+    lens = np.zeros((Q, world), np.uint32)
+    from paper_1603_08390_b200.dist import shard_range
+    for r in range(world):
+        lo, hi = shard_range(ds.csr.n, r, world)
+        sh = DeviceIndex.shard(ds.csr, lo, hi, device=gpu)
+        assert sh.id_offset == lo and sh.num_objects == hi - lo
+        res = sh.query(ds.queries)
+        ids[:, r], cnt[:, r], lens[:, r] = res.ids, res.counts, res.length
+    oi, oc, ol, ot = merge_lists(ids, cnt, lens, ds.queries.k, device=gpu)
+    assert np.array_equal(ol, want.length) and np.array_equal(ot, want.threshold)
+    for q in range(Q):
+        n = int(ol[q])
+        assert np.array_equal(oi[q, :n], want.ids[q, :n]) and np.array_equal(oc[q, :n], want.counts[q, :n])
+    # duplicate ids across lists -> ContractError
+    ids[0, 1, 0] = ids[0, 0, 0]
+    cnt[0, 1, 0] = 1
+    lens[0, 1] = max(lens[0, 1], 1)
+    with pytest.raises(ContractError):
+        merge_lists(ids, cnt, lens, ds.queries.k, device=gpu)
+
+
+def test_device_api_equals_host_api(gpu):
+    import torch
+
+    ds = synth.tweets(n=150_000, vocab=20_000, words=10, queries=64, k=100)
+    ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+    host = ix.query(ds.queries)
+    qb, dev = ds.queries, torch.device("cuda", gpu)
+    s = torch.cuda.Stream(dev)
+    with torch.cuda.stream(s):
+        d = {"qid": torch.from_numpy(qb.qid.astype(np.int32)).to(dev), "k": torch.from_numpy(qb.k.astype(np.int32)).to(dev),
+             "item_off": torch.from_numpy(qb.item_off.astype(np.int64)).to(dev),
+             "dim": torch.from_numpy(qb.dim.astype(np.int16)).to(dev), "lo": torch.from_numpy(qb.lo.astype(np.int32)).to(dev),
+             "hi": torch.from_numpy(qb.hi.astype(np.int32)).to(dev),
+             "out": torch.zeros((len(qb), 100, 2), dtype=torch.int32, device=dev),
+             "out_len": torch.zeros(len(qb), dtype=torch.int32, device=dev),
+             "out_thr": torch.zeros(len(qb), dtype=torch.int32, device=dev),
+             "max_k": 100, "total_items": qb.num_items, "stride": 100}
+        for _ in range(4):
+            ix.query_device(d, stream=s.cuda_stream)
+            if not ix.status().get("retry"):
+                break
+    s.synchronize()
+    out = d["out"].cpu().numpy().view(np.uint32)
+    assert np.array_equal(d["out_len"].cpu().numpy(), host.length.astype(np.int32))
+    assert np.array_equal(d["out_thr"].cpu().numpy(), host.threshold.astype(np.int32))
+    for q in range(len(qb)):
+        n = int(host.length[q])
+        assert np.array_equal(out[q, :n, 0], host.ids[q, :n]) and np.array_equal(out[q, :n, 1], host.counts[q, :n])
+
+
+def test_device_dim_stats_match_oracle(gpu, oracle):
+    ds = synth.random_instance(n=5000, dims=6, tokens=9, max_kw=8, queries=1, seed=12)
+    ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+    dm = ix.dim_stats()
+    oi = oracle.index(ds.csr)
+    for d in range(8):
+        assert dm[d] == oi.max_multiplicity(d)
+    back = ix.export()
+    assert np.array_equal(back.keys, ds.csr.keys) and np.array_equal(back.postings, ds.csr.postings)
