@@ -170,6 +170,10 @@ int genie_query_batch_device(genie_index* ix, const genie_config* cfg, uint32_t 
  * handle's stream).  Fills stats if non-NULL. */
 int genie_query_status(genie_index* ix, genie_batch_stats* stats, char* err, size_t errlen);
 
+/* Raw device status words of the last batch (diagnostics; words 20-22 hold
+ * per-phase k_scan cycle sums in GENIE_PHASE_TIMERS builds).  Synchronises. */
+int genie_debug_status(genie_index* ix, uint64_t* words, uint32_t n_words, char* err, size_t errlen);
+
 /* Kernels launched by the last batch (for launch accounting). */
 uint32_t genie_last_launch_count(const genie_index* ix);
 

@@ -10,7 +10,8 @@ import os
 from pathlib import Path
 
 LIB_DIR = Path(__file__).resolve().parent / "lib"
-ENGINE_LIB = LIB_DIR / "libgenie_b200.so"
+# GENIE_ENGINE_LIB selects an instrumented build (tools/phase_timers.py); default: the product library
+ENGINE_LIB = Path(os.environ.get("GENIE_ENGINE_LIB", LIB_DIR / "libgenie_b200.so"))
 SYNTH_LIB = LIB_DIR / "libgenie_synth.so"
 
 u8p = C.POINTER(C.c_uint8)
@@ -91,6 +92,7 @@ ENGINE_SYMBOLS = {
     "genie_query_status": (C.c_int, [vp, C.POINTER(BatchStats), C.c_char_p, C.c_size_t]),
     "genie_last_launch_count": (C.c_uint32, [vp]),
     "genie_last_stage_ns": (C.c_int, [vp, C.POINTER(StageNs), C.c_char_p, C.c_size_t]),
+    "genie_debug_status": (C.c_int, [vp, u64p, C.c_uint32, C.c_char_p, C.c_size_t]),
     "genie_merge_topk_device": (C.c_int, [vp, C.c_uint32, C.c_uint32, vp, vp, C.c_uint32, vp, C.c_uint32,
                                           vp, vp, vp, vp, C.c_char_p, C.c_size_t]),
     "genie_merge_topk": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.POINTER(Entry), u32p, C.c_uint32, u32p,

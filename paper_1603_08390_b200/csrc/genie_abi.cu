@@ -192,6 +192,16 @@ int genie_query_status(genie_index* ix, genie_batch_stats* stats, char* err, siz
 
 uint32_t genie_last_launch_count(const genie_index* ix) { return ix ? ix->last_launches : 0; }
 
+int genie_debug_status(genie_index* ix, uint64_t* words, uint32_t n_words, char* err, size_t errlen) {
+    return guarded(err, errlen, [&]() -> int {
+        if (!ix || !ix->ws.h_status) throw Error(GENIE_ERR_CONTRACT, "no batch has run on this index");
+        ensure_device(ix->device);
+        GENIE_CUDA(cudaStreamSynchronize(ix->stream));
+        for (uint32_t i = 0; i < n_words && i < ST_WORDS; ++i) words[i] = ix->ws.h_status[i];
+        return GENIE_OK;
+    });
+}
+
 int genie_last_stage_ns(genie_index* ix, genie_stage_ns* out, char* err, size_t errlen) {
     return guarded(err, errlen, [&]() -> int {
         if (!ix || !out) throw Error(GENIE_ERR_CONTRACT, "null argument");

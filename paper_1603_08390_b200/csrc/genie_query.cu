@@ -703,6 +703,9 @@ __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const S
 template <int W>
 __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t q, uint32_t t) {
     using Pk = Packing<W>;
+#ifdef GENIE_PHASE_TIMERS
+    const long long t_begin = clock64();
+#endif
     ItemCtx it;
     it.q = q;
     it.t = t;
@@ -743,6 +746,9 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         }
     }
     __syncthreads();
+#ifdef GENIE_PHASE_TIMERS
+    const long long t_setup = clock64();
+#endif
     const uint32_t S = p.q_S[q];
     const uint32_t nt = p.q_ntiles[q];
     const uint64_t cb = p.q_cut_base[q];
@@ -810,6 +816,9 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         __syncthreads();
     }
 
+#ifdef GENIE_PHASE_TIMERS
+    const long long t_scanned = clock64();
+#endif
     // ---- select: the tile's exact top-k
     if (it.gate && !sm.scal[SC_OVF]) {
         if (threadIdx.x == 0) {
@@ -847,6 +856,14 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     }
     __syncthreads();
     if (threadIdx.x == 0) p.tile_len[p.q_tile_base[q] + t] = sm.scal[SC_NOUT];
+#ifdef GENIE_PHASE_TIMERS
+    if (threadIdx.x == 0) {
+        const long long t_end = clock64();
+        atomicAdd(&p.st[ST_T_SETUP], static_cast<unsigned long long>(t_setup - t_begin));
+        atomicAdd(&p.st[ST_T_SCAN], static_cast<unsigned long long>(t_scanned - t_setup));
+        atomicAdd(&p.st[ST_T_EXTRACT], static_cast<unsigned long long>(t_end - t_scanned));
+    }
+#endif
 }
 
 __global__ void __launch_bounds__(kScanThreads, 2)
@@ -887,6 +904,7 @@ struct MergeSrc {
     const uint32_t* q_ntiles;
     const uint32_t* tile_len;
     const genie_entry* tile_out;
+    const uint32_t* q_floor;  // per-query floor (tile mode) or null
     // mode 1
     uint32_t L;
     const genie_entry* in;
@@ -926,23 +944,39 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(MergeSrc m) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
     __shared__ unsigned long long sums[32];
-    __shared__ uint32_t s_off[kMergeThreads + 1];
-    __shared__ uint32_t s_flag;
+    __shared__ uint32_t s_flag, s_pos;
     for (uint32_t q = blockIdx.x; q < m.Q; q += gridDim.x) {
         const uint32_t L = nlists_of(m, q);
         const uint32_t kq = m.k[q];
-        // union size
-        unsigned long long M = 0;
-        for (uint32_t l0 = 0; l0 < L; l0 += blockDim.x) {
-            const uint32_t l = l0 + threadIdx.x;
-            uint32_t len = 0;
-            if (l < L) {
-                const genie_entry* b;
-                list_of(m, q, l, b, len);
+        // Gather the union, dropping entries below the query's floor: the
+        // floor is the k-th count of some tile, so at least k entries sit at
+        // or above it and nothing below can make the merged top-k.
+        const uint32_t floor = m.q_floor ? m.q_floor[q] : 0u;
+        if (threadIdx.x == 0) s_pos = 0;
+        __syncthreads();
+        {
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+            for (uint32_t l = warp; l < L; l += blockDim.x >> 5) {
+                const genie_entry* bb;
+                uint32_t ll;
+                list_of(m, q, l, bb, ll);
+                for (uint32_t e0 = 0; e0 < ll; e0 += 32) {
+                    const uint32_t e = e0 + lane;
+                    genie_entry x{0, 0};
+                    if (e < ll) x = bb[e];
+                    const bool keep = e < ll && x.count >= floor;
+                    const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+                    uint32_t base = 0;
+                    if (lane == 0 && mask) base = atomicAdd(&s_pos, static_cast<uint32_t>(__popc(mask)));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    const uint32_t pos = base + __popc(mask & ((1u << lane) - 1u));
+                    if (keep && pos < kSortCap) keys[pos] = order_key(x.id, x.count);
+                }
             }
-            M += block_sum<unsigned long long>(len, sums);
         }
-        if (M > kSortCap) {
+        __syncthreads();
+        const uint32_t filled = s_pos;
+        if (filled > kSortCap) {  // large union: radix selection path
             if (threadIdx.x == 0) {
                 m.q_big[q] = 1;
                 atomicAdd(&m.st[ST_MERGE_BIG], 1ull);
@@ -951,32 +985,6 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(MergeSrc m) {
             continue;
         }
         if (threadIdx.x == 0) m.q_big[q] = 0;
-        // gather (chunks of blockDim lists)
-        uint32_t filled = 0;
-        for (uint32_t l0 = 0; l0 < L; l0 += blockDim.x) {
-            const uint32_t l = l0 + threadIdx.x;
-            uint32_t len = 0;
-            const genie_entry* b = nullptr;
-            if (l < L) list_of(m, q, l, b, len);
-            unsigned long long tot;
-            const unsigned long long ex = block_exclusive_scan<unsigned long long>(len, sums, tot);
-            if (threadIdx.x <= blockDim.x) s_off[threadIdx.x] = static_cast<uint32_t>(ex);
-            __syncthreads();
-            // one warp per list
-            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-            for (uint32_t w = warp; w < blockDim.x && l0 + w < L; w += blockDim.x >> 5) {
-                const genie_entry* bb;
-                uint32_t ll;
-                list_of(m, q, l0 + w, bb, ll);
-                const uint32_t o = filled + s_off[w];
-                for (uint32_t e = lane; e < ll; e += 32) {
-                    const genie_entry x = bb[e];
-                    keys[o + e] = order_key(x.id, x.count);
-                }
-            }
-            filled += static_cast<uint32_t>(tot);
-            __syncthreads();
-        }
         uint32_t N = 1;
         while (N < filled) N <<= 1;
         for (uint32_t i = filled + threadIdx.x; i < N; i += blockDim.x) keys[i] = ~0ull;
@@ -1317,6 +1325,7 @@ static MergeSrc tile_merge_src(genie_index* ix, uint32_t Q, const uint32_t* d_k,
     m.q_ntiles = w.q_ntiles.p;
     m.tile_len = w.tile_len.p;
     m.tile_out = w.tile_out.p;
+    m.q_floor = w.q_floor.p;
     m.k = d_k;
     m.Q = Q;
     m.id_offset = ix->id_offset;

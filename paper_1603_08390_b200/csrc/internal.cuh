@@ -35,6 +35,9 @@ enum StatusWord : int {
     ST_CLASS2 = 14,
     ST_CUT_CTR = 15,
     ST_SORT_BIG = 16,   // rows longer than kSortCap left for the segmented sort
+    ST_T_SETUP = 20,    // GENIE_PHASE_TIMERS builds: k_scan cycles per phase (thread 0 of each CTA)
+    ST_T_SCAN = 21,
+    ST_T_EXTRACT = 22,
     ST_WORDS = 32
 };
 
