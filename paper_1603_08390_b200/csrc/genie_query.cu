@@ -940,11 +940,12 @@ __device__ __forceinline__ uint32_t nlists_of(const MergeSrc& m, uint32_t q) {
 // merge_topk (engine.hpp:158-177) for unions of at most kSortCap entries:
 // concatenate, bitonic sort by (count desc, id asc), truncate to k,
 // threshold = k-th count if at least k entries else 0.
-__global__ void __launch_bounds__(kMergeThreads) k_merge(MergeSrc m) {
+__global__ void __launch_bounds__(kMergeThreads, 1) k_merge(MergeSrc m) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
     __shared__ unsigned long long sums[32];
     __shared__ uint32_t s_flag, s_pos;
+    __shared__ uint32_t s_scratch[256 + 8];
     for (uint32_t q = blockIdx.x; q < m.Q; q += gridDim.x) {
         const uint32_t L = nlists_of(m, q);
         const uint32_t kq = m.k[q];
@@ -1009,7 +1010,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge(MergeSrc m) {
             }
             __syncthreads();
         }
-        bitonic_sort_smem(keys, N);
+        select_k_smallest(keys, filled, kq, s_scratch);
         const uint32_t outn = kq < filled ? kq : filled;
         genie_entry* row = m.out + uint64_t(q) * m.out_stride;
         for (uint32_t e = threadIdx.x; e < outn; e += blockDim.x) {
