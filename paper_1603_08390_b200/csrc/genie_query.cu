@@ -571,20 +571,31 @@ template <int W>
 __device__ void emit_ties(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t T,
                           uint32_t need) {
     using Pk = Packing<W>;
+    constexpr uint32_t WPT = 4;  // counter words per thread per step (one 16-byte load)
+    const uint4* c4 = reinterpret_cast<const uint4*>(sm.cnt);
+    const uint32_t w4 = (it.words + 3) / 4;  // counters past the tile are zero and never match T > 0
     unsigned long long seen = 0;
-    for (uint32_t w0 = 0; w0 < it.words; w0 += blockDim.x) {
-        const uint32_t wi = w0 + threadIdx.x;
-        const uint32_t x = wi < it.words ? sm.cnt[wi] : 0u;
-        uint32_t m = wi < it.words ? Pk::eq_mask(x, T) : 0u;
+    for (uint32_t g0 = 0; g0 < w4; g0 += blockDim.x) {
+        const uint32_t gi = g0 + threadIdx.x;
+        uint32_t m[WPT] = {0, 0, 0, 0};
+        if (gi < w4) {
+            const uint4 x = c4[gi];
+            m[0] = Pk::eq_mask(x.x, T);
+            m[1] = Pk::eq_mask(x.y, T);
+            m[2] = Pk::eq_mask(x.z, T);
+            m[3] = Pk::eq_mask(x.w, T);
+        }
+        const uint32_t c = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
         unsigned long long total;
-        const unsigned long long before =
-            seen + block_exclusive_scan<unsigned long long>(__popc(m), sm.sums, total);
-        unsigned long long r = before;
-        while (m && r < need) {
-            const uint32_t b = __ffs(m) - 1;
-            m &= m - 1;
-            emit(p, it, sm, wi * Pk::kPer + b / W, T);
-            ++r;
+        unsigned long long r = seen + block_exclusive_scan<unsigned long long>(c, sm.sums, total);
+#pragma unroll
+        for (uint32_t j = 0; j < WPT; ++j) {
+            while (m[j] && r < need) {
+                const uint32_t bit = __ffs(m[j]) - 1;
+                m[j] &= m[j] - 1;
+                emit(p, it, sm, (gi * WPT + j) * Pk::kPer + bit / W, T);
+                ++r;
+            }
         }
         seen += total;
         if (seen >= need) break;  // uniform: total is block-wide
