@@ -1,30 +1,35 @@
 #!/usr/bin/env python
 """Benchmark of the GENIE match-count hot path on B200 (BASELINE.json metric).
 
-Workload (N=1 line): C2 Tweets-shaped bag-of-words match count -- 7M docs,
+Default line (N=1): C2 Tweets-shaped bag-of-words match count -- 7M docs,
 vocab 1M, 10 distinct Zipf(1) words per doc, 1024 fresh-document queries,
 top-k = 100 (BASELINE.json configs[1], the config the north star targets).
-A "step" is one full batch of 1024 queries through the hot path: lookup ->
-scan + c-PQ + tile select -> merge (+ all-gather and merge for N > 1).
+--workload {adult,sift,minhash,ocr} measures the other configs the same way.
+
+A "step" is one full query batch through the hot path: (LSH / minHash encode
+of the query batch for C3-C5) -> lookup -> scan + c-PQ + tile select -> merge
+(+ NCCL all-gather and device merge for N > 1).
 
 value : queries/s with the index and the query batch resident in HBM
-        (device API, CUDA events around each step, L2 flushed between steps)
-e2e   : queries/s through the public C-ABI call (genie_query_batch) with host
-        (pinned) query buffers and host result buffers; H2D of the queries
-        and D2H of the results are inside the timed region.
+        (device API, CUDA events around each step on the launching stream,
+        256 MiB L2 flush between steps, untimed)
+e2e   : queries/s through the public API with host (pinned) buffers: the
+        C-ABI call genie_query_batch (plus genie_lsh_encode for C3-C5); H2D of
+        the queries and D2H of the results are inside the timed region.
 
---impl reference times the reference CPU implementation (mcx built from the
-unmodified headers, oracle/_ref) on the box's host cores on the same workload.
+--impl reference times the reference's CPU implementation of the path on
+the box's host cores: the unmodified mcx engine (oracle/_ref) for C1/C2, the
+plain-C port of it (oracle/) for C3-C5, whose reference index build
+(~10^9 (keyword, id) pairs) does not fit a bench run.
 
 Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under
-torch.distributed.run (one process per GPU; object-id shards + NCCL
+torch.distributed.run (one process per GPU; object-id shards + one NCCL
 all-gather of per-shard top-k, merged on the device).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -43,7 +48,11 @@ WORKLOADS = {
     "tweets": "C2 tweets-shaped bag-of-words: 7M docs, vocab 1M, 10 distinct Zipf(1) words/doc, "
               "1024 fresh-doc queries, k=100",
     "adult": "C1 adult-shaped relational range match: 48842 x 14 attrs (+-50 windows), 1024 queries, k=100",
+    "sift": "C3 SIFT-shaped 128-d E2LSH: 4M points, p-stable m=237 (w=4, 67 buckets), 1024 queries, k=100",
+    "minhash": "C4 document minHash Jaccard: 2M sets (32-256 u64), 128 functions, D=8192, 4096 queries, k=100",
+    "ocr": "C5 OCR-shaped kernel-space LSH: 1M x 784-d, random binning m=237, D=8192, 2048 queries, k=1 (1-NN)",
 }
+QUERIES = {"tweets": 1024, "adult": 1024, "sift": 1024, "minhash": 4096, "ocr": 2048}
 
 
 def parse():
@@ -53,8 +62,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="genie", choices=["genie", "reference"])
     ap.add_argument("--workload", default="tweets", choices=list(WORKLOADS))
-    ap.add_argument("--n", type=int, default=None, help="override object count (debug)")
-    ap.add_argument("--queries", type=int, default=1024)
+    ap.add_argument("--n", type=int, default=None, help="override object count (debug only)")
+    ap.add_argument("--queries", type=int, default=None)
     ap.add_argument("--selector", type=int, default=0, help="0 cpq, 1 bucket/histogram ablation")
     ap.add_argument("--tile-bytes", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
@@ -67,15 +76,6 @@ def parse():
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
-
-
-def make_dataset(args):
-    from paper_1603_08390_b200 import synth
-
-    if args.workload == "tweets":
-        n = args.n or 7_000_000
-        return synth.tweets(n=n, vocab=1_000_000, words=10, queries=args.queries, k=100)
-    return synth.adult(n=args.n or 48842, queries=args.queries, k=100)
 
 
 # ------------------------------------------------------------------ clocks
@@ -136,40 +136,205 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# --------------------------------------------------------------- workloads
+
+class Workload:
+    """One BASELINE config: the host data, this rank's device index and the
+    device-resident query batch.  `encode()` re-encodes the device query
+    points into the batch's items (C3-C5) and is part of every step."""
+
+    lsh = None  # engine.Encoder for C3-C5
+
+    def __init__(self, args, rank, world, dev, local):
+        import torch
+
+        from paper_1603_08390_b200 import DeviceIndex, engine as E, synth
+
+        self.name = args.workload
+        self.torch = torch
+        self.dev = dev
+        Q = args.queries or QUERIES[self.name]
+        t0 = time.perf_counter()
+        self.qpoints = self.qsets = None
+        if self.name in ("tweets", "adult"):
+            ds = (synth.tweets(n=args.n or 7_000_000, vocab=1_000_000, words=10, queries=Q, k=100)
+                  if self.name == "tweets" else synth.adult(n=args.n or 48842, queries=Q, k=100))
+            self.gen_s = time.perf_counter() - t0
+            self.csr, self.batch = ds.csr, ds.queries
+            self.n = self.csr.n
+            t0 = time.perf_counter()
+            if world > 1:
+                lo, hi = self.n * rank // world, self.n * (rank + 1) // world
+                self.ix = DeviceIndex.shard(self.csr, lo, hi, device=local)
+            else:
+                self.ix = DeviceIndex.from_csr(self.csr, device=local)
+            self.build_s = time.perf_counter() - t0
+            self.k = 100
+            self.m = None
+        else:
+            if self.name == "sift":
+                ds = synth.sift(n=args.n or 4_000_000, dims=128, queries=Q)
+                cfg = E.lsh_config(E.PSTABLE, 237, 128, 3, w=4.0)
+                domain, self.k = 67, 100
+            elif self.name == "ocr":
+                ds = synth.ocr(n=args.n or 1_000_000, dims=784, queries=Q)
+                sigma = E.kernel_width_heuristic(ds.points[:10_000])
+                cfg = E.lsh_config(E.RBH, 237, 784, 7, sigma=sigma, rehash_domain=8192)
+                domain, self.k = 8192, 1
+                self.sigma = sigma
+            else:
+                ds = synth.sets(n=args.n or 2_000_000, queries=Q)
+                cfg = E.lsh_config(E.MINHASH, 128, 0, 5, rehash_domain=8192)
+                domain, self.k = 8192, 100
+            self.gen_s = time.perf_counter() - t0
+            self.ds = ds
+            self.m = cfg.m
+            self.lsh = E.Encoder(cfg, local)
+            t0 = time.perf_counter()
+            n_all = ds.points.shape[0] if ds.points is not None else ds.set_off.shape[0] - 1
+            lo, hi = n_all * rank // world, n_all * (rank + 1) // world
+            self.n = n_all
+            tok = torch.zeros((hi - lo, self.m), dtype=torch.int32, device=dev)
+            if self.name == "minhash":
+                off = ds.set_off[lo:hi + 1]
+                d_off = torch.from_numpy((off - off[0]).astype(np.int64)).to(dev)
+                d_el = torch.from_numpy(ds.elems[off[0]:off[-1]].view(np.int64)).to(dev)
+                self.lsh.encode_sets_device(d_off, d_el, tok)
+                del d_off, d_el
+            else:
+                d_pts = torch.from_numpy(ds.points[lo:hi]).to(dev)
+                self.lsh.encode_device(d_pts, tok)
+                del d_pts
+            torch.cuda.synchronize(dev)
+            self.ix = DeviceIndex.from_tokens_device(tok.data_ptr(), hi - lo, self.m, domain, device=local,
+                                                     id_offset=lo)
+            del tok
+            self.build_s = time.perf_counter() - t0
+            # query batch skeleton: items (i, token_i) for every function i
+            qtok = self.lsh.encode_sets(ds.query_set_off, ds.query_elems) if self.name == "minhash" else \
+                self.lsh.encode(ds.query_points)
+            self.batch = E.point_queries(qtok, self.k)
+            if self.name == "minhash":
+                self.qsets = (torch.from_numpy(ds.query_set_off.astype(np.int64)).to(dev),
+                              torch.from_numpy(ds.query_elems.view(np.int64)).to(dev))
+            else:
+                self.qpoints = torch.from_numpy(ds.query_points).to(dev)
+        qb = self.batch
+        self.Q = len(qb)
+        self.stride = max(1, min(int(qb.max_k), self.ix.num_objects or 1))
+        self.d = {
+            "qid": torch.from_numpy(qb.qid.astype(np.int32)).to(dev),
+            "k": torch.from_numpy(qb.k.astype(np.int32)).to(dev),
+            "item_off": torch.from_numpy(qb.item_off.astype(np.int64)).to(dev),
+            "dim": torch.from_numpy(qb.dim.astype(np.int16)).to(dev),
+            "lo": torch.from_numpy(qb.lo.astype(np.int32)).to(dev),
+            "hi": torch.from_numpy(qb.hi.astype(np.int32)).to(dev),
+            "out": torch.zeros((self.Q, self.stride, 2), dtype=torch.int32, device=dev),
+            "out_len": torch.zeros(self.Q, dtype=torch.int32, device=dev),
+            "out_thr": torch.zeros(self.Q, dtype=torch.int32, device=dev),
+            "max_k": int(qb.max_k), "total_items": qb.num_items, "stride": self.stride,
+        }
+        if self.m:
+            self.qtok = torch.zeros((self.Q, self.m), dtype=torch.int32, device=dev)
+
+    def encode(self, stream_ptr):
+        """Query-side transform on the device (part of each C3-C5 step)."""
+        if not self.m:
+            return 0
+        if self.qsets is not None:
+            self.lsh.encode_sets_device(self.qsets[0], self.qsets[1], self.qtok, stream=stream_ptr)
+        else:
+            self.lsh.encode_device(self.qpoints, self.qtok, stream=stream_ptr)
+        flat = self.qtok.view(-1)
+        self.d["lo"].copy_(flat)
+        self.d["hi"].copy_(flat)
+        return 1
+
+    def host_encode(self):
+        """e2e: host query points/sets -> tokens through the public API."""
+        from paper_1603_08390_b200 import engine as E
+
+        if self.name == "minhash":
+            t = self.lsh.encode_sets(self.ds.query_set_off, self.ds.query_elems)
+            h2d = self.ds.query_set_off.nbytes + self.ds.query_elems.nbytes
+        else:
+            t = self.lsh.encode(self.ds.query_points)
+            h2d = self.ds.query_points.nbytes
+        return E.point_queries(t, self.k), h2d, t.nbytes
+
+    def cpu_csr(self):
+        if self.m is None:
+            return self.csr
+        return self.ix.export()  # the device CSR (equal to the host build, tests/test_gpu_lsh.py)
+
+
 # --------------------------------------------------------------- reference
 
-def reference_qps(csr, queries, sample: int, steps: int, warmup: int):
-    """The reference CPU engine (mcx::execute_batch, Selector::cpq, all host
-    threads) on a bounded sample of the workload.  Returns (qps list, cores,
-    build seconds)."""
-    from oracle.pyoracle import RefLib
+def reference_qps(w: Workload, sample: int, steps: int, warmup: int):
+    """The reference CPU engine on the box's cores over a bounded query sample
+    of the same index: mcx::execute_batch (Selector::cpq, parallel, all
+    threads; oracle/_ref) for C1/C2, the C port (oracle/, all threads) for
+    C3-C5.  Returns (qps per step, cores, kind, build seconds)."""
+    from oracle.pyoracle import Oracle, RefLib, threads
 
-    ref = RefLib()
+    csr = w.cpu_csr()
     t0 = time.perf_counter()
-    rix = ref.index(csr)
+    if w.m is None:
+        ref = RefLib()
+        rix = ref.index(csr)
+        cores, kind = ref.hardware_threads(), "reference"
+
+        def run(b):
+            rc, r = rix.execute(b, selector=0, sequential=False, workers=0)
+            if rc:
+                raise RuntimeError(r)
+    else:
+        o = Oracle()
+        oix = o.index(csr)
+        cores, kind = threads(), "port"
+
+        def run(b):
+            oix.execute(b, nthreads=cores)
     build_s = time.perf_counter() - t0
-    cores = ref.hardware_threads()
     per_step = []
+    Q = len(w.batch)
     for s in range(warmup + steps):
-        a = (s * sample) % max(1, len(queries) - sample + 1)
-        b = queries.slice(a, a + sample)
+        a = (s * sample) % max(1, Q - sample + 1)
+        b = w.batch.slice(a, a + sample)
         t = time.perf_counter()
-        rc, r = rix.execute(b, selector=0, sequential=False, workers=0)
+        run(b)
         dt = time.perf_counter() - t
-        if rc:
-            raise RuntimeError(r)
         if s >= warmup:
             per_step.append(sample / dt)
-    return per_step, cores, build_s
+    return per_step, cores, kind, build_s
+
+
+def default_sample(name: str) -> int:
+    return {"tweets": 96, "adult": 512, "sift": 16, "minhash": 512, "ocr": 16}[name]
 
 
 def run_reference_arm(args):
-    rank, _, world = dist_env()
+    import torch
+
+    rank, local, world = dist_env()
     if rank != 0:
         return 0
-    ds = make_dataset(args)
-    sample = args.ref_sample or (64 if args.workload == "tweets" else 256)
-    qps, cores, build_s = reference_qps(ds.csr, ds.queries, sample, args.steps, args.warmup)
+    dev = torch.device("cuda", local) if torch.cuda.is_available() else None
+    if args.workload in ("tweets", "adult"):
+        # no GPU involvement at all: generate the inputs on the host
+        class _W:  # minimal stand-in with the fields reference_qps uses
+            pass
+        from paper_1603_08390_b200 import synth
+        Q = args.queries or QUERIES[args.workload]
+        ds = (synth.tweets(n=args.n or 7_000_000, vocab=1_000_000, words=10, queries=Q, k=100)
+              if args.workload == "tweets" else synth.adult(n=args.n or 48842, queries=Q, k=100))
+        w = _W()
+        w.m, w.csr, w.batch = None, ds.csr, ds.queries
+        w.cpu_csr = lambda: ds.csr
+    else:
+        w = Workload(args, 0, 1, dev, local)  # tokens via the GPU encoder (inputs only)
+    sample = args.ref_sample or default_sample(args.workload)
+    qps, cores, kind, build_s = reference_qps(w, sample, args.steps, args.warmup)
     value = float(np.mean(qps))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
@@ -177,10 +342,11 @@ def run_reference_arm(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded generator, SURVEY.md 8d)",
         "config": {"workload": WORKLOADS[args.workload], "queries_per_step": sample,
-                   "engine": "mcx::execute_batch Selector::cpq ExecMode::parallel (unmodified reference headers)"},
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{sample} queries per step of the {len(ds.queries)}-query batch; "
-                                   f"index build {build_s:.1f}s untimed"},
+                   "engine": ("mcx::execute_batch Selector::cpq ExecMode::parallel (unmodified reference headers)"
+                              if kind == "reference" else "plain-C port of mcx::execute_batch (oracle/)")},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{sample} queries per step of the {len(w.batch)}-query batch; "
+                                   f"CPU index build {build_s:.1f}s untimed"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -193,8 +359,8 @@ def main_genie(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1603_08390_b200 import DeviceIndex, config
-    from paper_1603_08390_b200 import _native as N
+    from paper_1603_08390_b200 import config
+    from paper_1603_08390_b200.engine import QueryBatch
 
     rank, local, world = dist_env()
     assert world == args.gpus or world == 1, "launch N>1 under torch.distributed.run"
@@ -202,37 +368,16 @@ def main_genie(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    # a dedicated stream: torch's default stream has handle 0, which the C ABI
+    # reads as "the index's own stream"
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    sptr = stream.cuda_stream
 
-    t0 = time.perf_counter()
-    ds = make_dataset(args)
-    gen_s = time.perf_counter() - t0
-    csr, qb = ds.csr, ds.queries
-    n, Q = csr.n, len(qb)
-    t0 = time.perf_counter()
-    if world > 1:
-        lo, hi = n * rank // world, n * (rank + 1) // world
-        ix = DeviceIndex.shard(csr, lo, hi, device=local)
-    else:
-        ix = DeviceIndex.from_csr(csr, device=local)
-    build_s = time.perf_counter() - t0
-
-    K = int(qb.max_k)
-    stride = K
+    w = Workload(args, rank, world, dev, local)
+    ix, d, Q, stride = w.ix, w.d, w.Q, w.stride
     cfg = config(selector=args.selector, tile_bytes=args.tile_bytes, ctas_per_sm=args.ctas_per_sm,
                  span_chunk=args.span_chunk, stage_events=True)
-    # device-resident query batch
-    d = {
-        "qid": torch.from_numpy(qb.qid.astype(np.int32)).to(dev),
-        "k": torch.from_numpy(qb.k.astype(np.int32)).to(dev),
-        "item_off": torch.from_numpy(qb.item_off.astype(np.int64)).to(dev),
-        "dim": torch.from_numpy(qb.dim.astype(np.int16)).to(dev),
-        "lo": torch.from_numpy(qb.lo.astype(np.int32)).to(dev),
-        "hi": torch.from_numpy(qb.hi.astype(np.int32)).to(dev),
-        "out": torch.zeros((Q, stride, 2), dtype=torch.int32, device=dev),
-        "out_len": torch.zeros(Q, dtype=torch.int32, device=dev),
-        "out_thr": torch.zeros(Q, dtype=torch.int32, device=dev),
-        "max_k": K, "total_items": qb.num_items, "stride": stride,
-    }
     if world > 1:
         gath = torch.zeros((world, Q, stride, 2), dtype=torch.int32, device=dev)
         gath_len = torch.zeros((world, Q), dtype=torch.int32, device=dev)
@@ -241,19 +386,14 @@ def main_genie(args):
         fin = torch.zeros((Q, stride, 2), dtype=torch.int32, device=dev)
         fin_len = torch.zeros(Q, dtype=torch.int32, device=dev)
         fin_thr = torch.zeros(Q, dtype=torch.int32, device=dev)
-
-    # a dedicated stream: torch's default stream has handle 0, which the C ABI
-    # reads as "the index's own stream"
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
-    sptr = stream.cuda_stream
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     launches_per_step = 0
 
     def step():
         nonlocal launches_per_step
-        launches_per_step = ix.query_device(d, cfg, stream=sptr)
+        launches_per_step = w.encode(sptr)
+        launches_per_step += ix.query_device(d, cfg, stream=sptr)
         if world > 1:
             # all-gather the per-shard top-k (global ids), merge on the device
             dist.all_gather_into_tensor(gath, d["out"])
@@ -273,12 +413,11 @@ def main_genie(args):
         raise RuntimeError("workspace did not converge")
 
     for _ in range(max(args.warmup, 3)):
-        st = run_checked()
-    stats = st
+        stats = run_checked()
 
     # ---- timed region (device): per-step CUDA events, L2 flushed between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    scan_ms, step_ms, look_ms, merge_ms = [], [], [], []
+    scan_ms, look_ms, merge_ms = [], [], []
     with ClockSampler(local) as clocks:
         if world > 1:
             dist.barrier()
@@ -306,26 +445,21 @@ def main_genie(args):
     ms_per_step = total_ms / args.steps
     value = Q * args.steps / (total_ms / 1000.0)
 
-    # correctness spot-check of the timed output against the host API path
-    # (cheap; the oracle parity lives in tests/)
-    # ---- e2e through the public C-ABI call with host buffers
-    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
-    from paper_1603_08390_b200.engine import QueryBatch
-    hb = QueryBatch(pin(qb.qid), pin(qb.k), pin(qb.item_off), pin(qb.dim), pin(qb.lo), pin(qb.hi))
+    # ---- e2e through the public C-ABI calls with host (pinned) buffers
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
     hout = (pin(np.zeros((Q, stride, 2), np.uint32)), pin(np.zeros(Q, np.uint32)), pin(np.zeros(Q, np.uint32)))
     e2e_cfg = config(selector=args.selector, tile_bytes=args.tile_bytes, ctas_per_sm=args.ctas_per_sm,
                      span_chunk=args.span_chunk)
-    for _ in range(2):
-        res = ix.query(hb, e2e_cfg, stride=stride, out=hout, copy=False)
-    e2e_times = []
-    e2e_steps = max(3, min(args.steps, 10))
-    for _ in range(e2e_steps):
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        t = time.perf_counter()
-        res = ix.query(hb, e2e_cfg, stride=stride, out=hout, copy=False)
+    qb = w.batch
+    hb = QueryBatch(pin(qb.qid), pin(qb.k), pin(qb.item_off), pin(qb.dim), pin(qb.lo), pin(qb.hi))
+
+    def e2e_step():
+        h2d, d2h = hb.nbytes(), 0
+        b = hb
+        if w.m:
+            b, h2d_p, d2h_t = w.host_encode()
+            h2d, d2h = h2d_p + b.nbytes(), d2h_t
+        ix.query(b, e2e_cfg, stride=stride, out=hout, copy=False)
         if world > 1:
             lists = torch.from_numpy(hout[0]).to(dev)
             lens = torch.from_numpy(hout[1].astype(np.int32)).to(dev)
@@ -335,6 +469,18 @@ def main_genie(args):
             m_len.copy_(gath_len.t())
             ix.merge_device(Q, world, m_in, m_len, stride, d["k"], stride, fin, fin_len, fin_thr, stream=sptr)
             fin.cpu(), fin_len.cpu(), fin_thr.cpu()
+        return h2d, d2h + hout[0].nbytes + hout[1].nbytes + hout[2].nbytes
+
+    for _ in range(2):
+        e2e_step()
+    e2e_times = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        h2d_bytes, d2h_bytes = e2e_step()
         e2e_times.append(time.perf_counter() - t)
     e2e_s = float(np.mean(e2e_times))
     if world > 1:
@@ -342,8 +488,6 @@ def main_genie(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = Q / e2e_s
-    h2d_bytes = hb.nbytes()
-    d2h_bytes = hout[0].nbytes + hout[1].nbytes + hout[2].nbytes
 
     # ---- roofline of the dominant kernel (k_scan: fused scan + c-PQ + tile select)
     peaks_path = ROOT / "MEASURED_PEAKS.json"
@@ -361,8 +505,9 @@ def main_genie(args):
     if tpath.exists():
         try:
             tj = json.loads(tpath.read_text())
-            if tj.get("workload") == args.workload and tj.get("n_gpus", 1) == world:
-                traffic = tj.get("dram_bytes_per_launch")
+            entry = tj.get(args.workload) if args.workload in tj else (tj if tj.get("workload") == args.workload else None)
+            if entry and entry.get("n_gpus", 1) == world:
+                traffic = entry.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -370,11 +515,11 @@ def main_genie(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            sample = args.ref_sample or (96 if args.workload == "tweets" else 512)
-            qps, cores, build_ref_s = reference_qps(csr, qb, sample, steps=1, warmup=0)
-            cpu = {"value": round(float(np.mean(qps)), 3), "unit": UNIT, "cores": cores, "kind": "reference",
-                   "sample": f"first {sample} of the {Q} queries, same index (mcx::execute_batch, "
-                             f"Selector::cpq, parallel, {cores} threads); ref index build {build_ref_s:.1f}s untimed"}
+            sample = args.ref_sample or default_sample(args.workload)
+            qps, cores, kind, build_ref_s = reference_qps(w, sample, steps=1, warmup=0)
+            cpu = {"value": round(float(np.mean(qps)), 3), "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": f"first {sample} of the {Q} queries on the same index ({cores} threads); "
+                             f"CPU index build {build_ref_s:.1f}s untimed"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -384,30 +529,33 @@ def main_genie(args):
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator, SURVEY.md 8d)",
-            "config": {"workload": WORKLOADS[args.workload], "n_objects": n, "postings": csr.num_postings,
-                       "queries": Q, "k": K, "selector": ["cpq", "bucket"][min(args.selector, 1)],
+            "config": {"workload": WORKLOADS[args.workload], "n_objects": w.n, "queries": Q, "k": int(qb.max_k),
+                       "selector": ["cpq", "bucket"][min(args.selector, 1)],
                        "parallelism": f"object-id shards x{world} + NCCL all-gather merge" if world > 1 else "single GPU",
                        "l2": "flushed between timed steps (256 MiB write)",
                        "postings_per_query_mean": round(postings / Q, 1),
-                       "generate_s": round(gen_s, 2), "index_upload_s": round(build_s, 2)},
+                       "generate_s": round(w.gen_s, 2), "index_build_s": round(w.build_s, 2)},
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes),
                     "d2h_bytes_per_step": int(d2h_bytes),
-                    "path": "genie_query_batch (C ABI) with pinned host buffers" + (
-                        " + all-gather + genie_merge_topk_device" if world > 1 else "")},
+                    "path": ("genie_lsh_encode + " if w.m else "") + "genie_query_batch (C ABI), pinned host buffers"
+                            + (" + all-gather + genie_merge_topk_device" if world > 1 else "")},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": "k_scan (fused posting scan + c-PQ gate/table + tile top-k)",
                          "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": round(scan_avg_ms, 4),
                          "peak_source": peak_src,
-                         "note": "hot lists are shared by many queries and stay L2-resident across the "
-                                 "tile-major sweep, so algorithmic bytes exceed DRAM bytes"},
+                         "note": "algorithmic bytes = 4 B x sum_q P_q; hot lists shared by many queries stay "
+                                 "L2-resident across the tile-major sweep, so DRAM traffic is far below them"},
             "cpu_baseline": cpu,
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clocks.summary(),
             "stage_ms": {"step_mean": round(float(np.mean(step_ms)), 4), "scan_mean": round(scan_avg_ms, 4),
-                         "lookup_mean": round(float(np.mean(look_ms)), 4), "merge_mean": round(float(np.mean(merge_ms)), 4)},
+                         "lookup_mean": round(float(np.mean(look_ms)), 4),
+                         "merge_mean": round(float(np.mean(merge_ms)), 4)},
             "fallback_tiles": int(st.get("fallback_tiles", 0)), "work_items": int(st.get("work_items", 0)),
         }
+        if getattr(w, "sigma", None):
+            line["config"]["sigma"] = round(w.sigma, 6)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

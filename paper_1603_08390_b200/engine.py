@@ -475,3 +475,33 @@ def csr_from_tokens(tokens: np.ndarray) -> CSR:
     uniq, starts = np.unique(sk, return_index=True)
     off = np.concatenate([starts.astype(np.uint64), np.array([sk.shape[0]], np.uint64)])
     return CSR(n, uniq, off, ids)
+
+
+def kernel_width_heuristic(points: np.ndarray, max_pairs: int = 1_000_000) -> float:
+    """Mean pairwise l1 distance (lsh.hpp:333-363), vectorised: all pairs when
+    n(n-1)/2 <= max_pairs, else max_pairs pairs drawn with the reference's
+    SplitMix64(0x6d63782d7730) sequence.  Summation order differs from the
+    reference's sequential loop, so the last bits of sigma may differ; sigma is
+    an explicit input of the encoder on every path that is compared."""
+    pts = np.asarray(points, np.float64)
+    n = pts.shape[0]
+    if n < 2:
+        raise ContractError("kernel width needs at least 2 points")
+    total = n * (n - 1) // 2
+    if total <= max_pairs:
+        ii, jj = np.triu_indices(n, 1)
+    else:
+        gamma = np.uint64(0x9E3779B97F4A7C15)
+        t = np.arange(1, 2 * max_pairs + 1, dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            z = np.uint64(0x6D63782D7730) + t * gamma
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            z = z ^ (z >> np.uint64(31))
+        ii = (z[0::2] % np.uint64(n)).astype(np.int64)
+        jj = (z[1::2] % np.uint64(n - 1)).astype(np.int64)
+        jj += (jj >= ii)
+    acc = 0.0
+    for a in range(0, ii.shape[0], 65536):
+        acc += float(np.abs(pts[ii[a:a + 65536]] - pts[jj[a:a + 65536]]).sum())
+    return acc / ii.shape[0]
