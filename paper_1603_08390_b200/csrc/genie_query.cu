@@ -179,8 +179,10 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
                 const uint32_t T = p.tile_bits / W;
                 const uint32_t kq = p.k[q];
                 cap = min(kq, T);
-                v_span = p.q_S[q];
-                v_cut = static_cast<unsigned long long>(p.q_S[q]) * (nt + 1);
+                // single-tile queries read each item's contiguous keyword
+                // range directly (no per-keyword spans / cuts)
+                v_span = nt > 1 ? p.q_S[q] : 0u;
+                v_cut = nt > 1 ? static_cast<unsigned long long>(p.q_S[q]) * (nt + 1) : 0ull;
                 v_tile = nt;
                 v_out = static_cast<unsigned long long>(nt) * cap;
                 v_cls = 1ull << (21 * wclass(W));
@@ -729,13 +731,12 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     it.cap = p.q_cap[q];
     it.out_base = p.q_out_base[q] + uint64_t(t) * it.cap;
     it.gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
-    // bit_ceil(max(2 k bound, 2)) (cpq.hpp:137-138, 283), capped by the shared table
-    {
-        const uint64_t want = max(2ull * it.kq * it.bound, 2ull);
-        const uint32_t lz = __clzll(want - 1);
-        const uint64_t htc = lz == 0 ? (1ull << 63) : (1ull << (64 - lz));
-        it.ht_cap = static_cast<uint32_t>(htc < p.ht_slots ? htc : p.ht_slots);
-    }
+    // The table always uses the whole reserved shared region (the reference
+    // sizes it bit_ceil(2 k bound), cpq.hpp:137-138, 283; that figure is kept
+    // for MemoryStats): concurrent admissions arrive in bursts of up to one per
+    // thread before AT can move, and a larger table absorbs them without the
+    // exact-histogram fallback.  Results do not depend on the capacity.
+    it.ht_cap = p.ht_slots;
 
     // setup: zero counters, empty table, ZA, AT = 1 (cpq.hpp:281-292)
     {
@@ -760,8 +761,13 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
 #ifdef GENIE_PHASE_TIMERS
     const long long t_setup = clock64();
 #endif
-    const uint32_t S = p.q_S[q];
     const uint32_t nt = p.q_ntiles[q];
+    // one tile: the slices are the items' keyword ranges, contiguous in the
+    // postings array (keys of one dim are adjacent); several tiles: one slice
+    // per keyword list, cut at the tile boundaries by k_cut
+    const bool item_mode = nt == 1;
+    const uint64_t i0 = p.item_off[q];
+    const uint32_t S = item_mode ? static_cast<uint32_t>(p.item_off[q + 1] - i0) : p.q_S[q];
     const uint64_t cb = p.q_cut_base[q];
     const uint64_t sbq = p.q_span_base[q];
     const uint32_t unit = p.unit;
@@ -775,12 +781,20 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         uint32_t groups = 0;
         if (threadIdx.x < nsb) {
             const uint32_t s = s0 + threadIdx.x;
-            const uint32_t* c = p.cuts + cb + uint64_t(s) * (nt + 1) + t;
-            const uint32_t a = c[0], e = c[1];
-            const uint64_t beg = p.span_beg[sbq + s] + a;
+            uint64_t beg;
+            uint32_t len;
+            if (item_mode) {
+                const uint64_t it_i = i0 + s, kb = p.it_kb[it_i];
+                beg = p.key_off[kb];
+                len = static_cast<uint32_t>(p.key_off[kb + p.it_nk[it_i]] - beg);
+            } else {
+                const uint32_t* c = p.cuts + cb + uint64_t(s) * (nt + 1) + t;
+                beg = p.span_beg[sbq + s] + c[0];
+                len = c[1] - c[0];
+            }
             sm.s_beg[threadIdx.x] = beg;
-            sm.s_len[threadIdx.x] = e - a;
-            groups = e > a ? static_cast<uint32_t>(((beg + (e - a) - 1) >> 7) - (beg >> 7) + 1) : 0u;
+            sm.s_len[threadIdx.x] = len;
+            groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
         }
         unsigned long long total;
         const unsigned long long ex = block_exclusive_scan<unsigned long long>(groups, sm.sums, total);
