@@ -2,12 +2,15 @@
 // statistics, export.  Replaces the product of mcx::build_index
 // (index.hpp:190-250) and the InvertedIndex accessors (index.hpp:41-182).
 #include <algorithm>
+#include <cstdlib>
 #include <thread>
 #include <vector>
 
 #include "internal.cuh"
 
 namespace genie {
+
+void build_dense_containers(genie_index* ix, const uint64_t* h_off);
 
 // ---- max_multiplicity per dim (index.hpp:110-113, 153-174) on the device:
 // pass 1 counts the dim's keywords per object, pass 2 takes the max while
@@ -49,6 +52,51 @@ static void compute_dim_stats(genie_index* ix, const uint64_t* h_keys, const uin
                                                                             scratch.p, ix->dim_mult.p + d);
         }
         j = e;
+    }
+    GENIE_CUDA(cudaStreamSynchronize(ix->stream));
+    GENIE_CUDA(cudaGetLastError());
+}
+
+// ---- dense containers: bit i of a dense key's bitmap is set iff object i
+// carries the key.  Built from the CSR (ascending ids per list).
+__global__ void k_build_bitmap(const uint32_t* post, uint64_t b, uint64_t e, uint32_t* bm) {
+    for (uint64_t i = b + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < e;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t id = post[i];
+        atomicOr(&bm[id >> 5], 1u << (id & 31));
+    }
+}
+
+static double dense_density() {
+    const char* v = std::getenv("GENIE_DENSE_MIN_DENSITY");
+    if (!v || !*v) return 0.125;  // break-even with the posting scan is ~1/6 - 1/10
+    return std::atof(v);
+}
+
+void build_dense_containers(genie_index* ix, const uint64_t* h_off) {
+    const double dens = dense_density();
+    std::vector<int32_t> slot(ix->K, -1);
+    std::vector<uint64_t> dense_keys;
+    if (dens > 0.0 && ix->n >= 1024) {
+        for (uint64_t j = 0; j < ix->K; ++j)
+            if (double(h_off[j + 1] - h_off[j]) >= dens * double(ix->n)) {
+                slot[j] = static_cast<int32_t>(dense_keys.size());
+                dense_keys.push_back(j);
+            }
+    }
+    ix->n_dense = static_cast<uint32_t>(dense_keys.size());
+    ix->bitmap_words = ((ix->n + 31) / 32 + 3) & ~3u;  // 16-byte rows
+    ix->key_dense.reserve(ix->K + 1);
+    if (ix->K)
+        GENIE_CUDA(cudaMemcpy(ix->key_dense.p, slot.data(), ix->K * sizeof(int32_t), cudaMemcpyHostToDevice));
+    ix->bitmaps.reserve(std::max<size_t>(size_t(ix->n_dense) * ix->bitmap_words, 4));
+    if (!ix->n_dense) return;
+    GENIE_CUDA(cudaMemsetAsync(ix->bitmaps.p, 0, size_t(ix->n_dense) * ix->bitmap_words * 4, ix->stream));
+    for (uint32_t d = 0; d < ix->n_dense; ++d) {
+        const uint64_t j = dense_keys[d], b = h_off[j], e = h_off[j + 1];
+        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((e - b + 255) / 256, uint64_t(ix->sms) * 8));
+        k_build_bitmap<<<blocks, 256, 0, ix->stream>>>(ix->postings.p, b, e,
+                                                        ix->bitmaps.p + size_t(d) * ix->bitmap_words);
     }
     GENIE_CUDA(cudaStreamSynchronize(ix->stream));
     GENIE_CUDA(cudaGetLastError());
@@ -117,6 +165,7 @@ static genie_index* upload(uint32_t n, uint64_t K, const uint64_t* keys, const u
         } else {
             compute_dim_stats(ix, keys, off);
         }
+        build_dense_containers(ix, off);
         GENIE_CUDA(cudaDeviceSynchronize());
     } catch (...) {
         genie_index_destroy(ix);

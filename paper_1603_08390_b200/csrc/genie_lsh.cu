@@ -33,6 +33,8 @@ struct genie_encoder {
 
 namespace genie {
 
+void build_dense_containers(genie_index* ix, const uint64_t* h_off);
+
 // ------------------------------------------------------------ host sampling
 
 namespace {
@@ -558,6 +560,7 @@ int genie_index_from_tokens_device(const uint32_t* d_tokens, uint32_t n, uint32_
                     for (uint32_t f = 0; f < m; ++f) dm[f] = 1;
                 ix->dim_mult.reserve(65536);
                 GENIE_CUDA(cudaMemcpy(ix->dim_mult.p, dm.data(), 65536 * 4, cudaMemcpyHostToDevice));
+                build_dense_containers(ix, hoff.data());
             }
             GENIE_CUDA(cudaDeviceSynchronize());
         } catch (...) {

@@ -45,6 +45,9 @@ struct BatchParams {
     const uint64_t* key_off;
     const uint32_t* postings;
     const uint32_t* dim_mult;
+    const int32_t* key_dense;  // [K] dense-container slot or -1
+    const uint32_t* bitmaps;   // [n_dense][bitmap_words]
+    uint32_t bitmap_words, n_dense;
     uint64_t K;
     uint32_t n;
     uint32_t id_offset;
@@ -65,6 +68,7 @@ struct BatchParams {
     uint32_t ht_slots;
     uint32_t *it_kb, *it_nk, *it_sbase;
     uint64_t* span_beg;
+    uint32_t* span_key;
     uint32_t* cuts;
     uint32_t *work_q, *work_t;
     uint32_t* tile_len;
@@ -272,7 +276,10 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
         const uint64_t j = p.it_kb[it] + (s - p.it_sbase[it]);
         const uint64_t beg = p.key_off[j];
         const uint32_t len = static_cast<uint32_t>(p.key_off[j + 1] - beg);
-        if (lane == 0) p.span_beg[g] = beg;
+        if (lane == 0) {
+            p.span_beg[g] = beg;
+            p.span_key[g] = static_cast<uint32_t>(j);
+        }
         const uint32_t nt = p.q_ntiles[q];
         const uint32_t T = p.tile_bits / p.q_W[q];
         uint32_t* cut = p.cuts + p.q_cut_base[q] + uint64_t(s) * (nt + 1);
@@ -296,6 +303,7 @@ struct ScanSmem {
     uint64_t* s_beg;      // staged slices
     uint32_t* s_len;
     uint32_t* s_upref;
+    uint32_t* s_dense;         // dense-container slots of the staged spans
     unsigned long long* sums;  // block scan scratch (32)
     uint32_t* scal;            // scalars
 };
@@ -312,6 +320,7 @@ enum ScalarSlot {
     SC_ABOVE = 8,
     SC_DONE = 9,
     SC_FLOOR = 10,
+    SC_NDENSE = 11,
     SC_WORDS = 16
 };
 
@@ -331,12 +340,14 @@ __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t tile_bytes, ui
     base += kSpanBatch * sizeof(uint32_t);
     s.s_upref = reinterpret_cast<uint32_t*>(base);
     base += kSpanBatch * sizeof(uint32_t);
+    s.s_dense = reinterpret_cast<uint32_t*>(base);
+    base += kSpanBatch * sizeof(uint32_t);
     s.scal = reinterpret_cast<uint32_t*>(base);
     return s;
 }
 
 inline size_t scan_smem_bytes(uint32_t tile_bytes, uint32_t ht_slots) {
-    return tile_bytes + size_t(ht_slots) * 8 + kSpanBatch * 8 + 32 * 8 + kZaMax * 4 + kSpanBatch * 4 * 2 +
+    return tile_bytes + size_t(ht_slots) * 8 + kSpanBatch * 8 + 32 * 8 + kZaMax * 4 + kSpanBatch * 4 * 3 +
            SC_WORDS * 4;
 }
 
@@ -713,6 +724,142 @@ __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const S
     return T;
 }
 
+__device__ __forceinline__ void zero_counters(const ItemCtx& it, const ScanSmem& sm) {
+    uint4* c4 = reinterpret_cast<uint4*>(sm.cnt);
+    const uint32_t w4 = (it.words + 3) / 4;
+    for (uint32_t i = threadIdx.x; i < w4; i += blockDim.x) c4[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+}
+
+// Bit j of a bitmap word -> counter increment at the counter's lane.
+template <int W>
+__device__ __forceinline__ uint32_t expand_bits(uint32_t b);
+template <>
+__device__ __forceinline__ uint32_t expand_bits<4>(uint32_t b) {  // 8 bits -> 8 nibbles
+    uint32_t x = b & 0xffu;
+    x = (x | (x << 12)) & 0x000f000fu;
+    x = (x | (x << 6)) & 0x03030303u;
+    return (x | (x << 3)) & 0x11111111u;
+}
+template <>
+__device__ __forceinline__ uint32_t expand_bits<8>(uint32_t b) {  // 4 bits -> 4 bytes
+    return ((b & 0xfu) * 0x00204081u) & 0x01010101u;
+}
+template <>
+__device__ __forceinline__ uint32_t expand_bits<16>(uint32_t b) {  // 2 bits -> 2 halves
+    return (b & 1u) | ((b & 2u) << 15);
+}
+
+// Dense phase: the counters of the tile are initialised from the bitmaps of
+// the query's dense lists (each thread owns whole counter words: plain
+// stores, no atomics).  Then the c-PQ state is brought to what one update
+// per (dense list, member object) would have produced: ZA[v] += #objects
+// with count >= v for v >= AT, AT advanced while ZA[AT] >= k, and every
+// object at or above the new AT inserted into the table (fewer than k).
+template <int W>
+__device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t nd) {
+    using Pk = Packing<W>;
+    constexpr uint32_t kWpb = W;  // counter words per 32-bit bitmap word (32 / kPer)
+    const uint32_t bw0 = it.tile_lo >> 5;
+    const uint32_t nbw = (it.tile_n + 31) >> 5;
+    for (uint32_t bw = threadIdx.x; bw < nbw; bw += blockDim.x) {
+        uint32_t acc[kWpb];
+#pragma unroll
+        for (uint32_t j = 0; j < kWpb; ++j) acc[j] = 0;
+        for (uint32_t d = 0; d < nd; ++d) {
+            const uint32_t b = __ldg(p.bitmaps + size_t(sm.s_dense[d]) * p.bitmap_words + bw0 + bw);
+#pragma unroll
+            for (uint32_t j = 0; j < kWpb; ++j) acc[j] += expand_bits<W>(b >> (j * Pk::kPer));
+        }
+        uint4* dst = reinterpret_cast<uint4*>(sm.cnt + bw * kWpb);
+#pragma unroll
+        for (uint32_t j = 0; j < kWpb; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    }
+    // (tiles are multiples of 32 objects: the bitmap words cover every counter word)
+    __syncthreads();
+    if (!it.gate) return;
+    const uint32_t at0 = sm.scal[SC_AT];
+    const uint32_t dmax = min(nd, it.bound);
+    if (at0 <= dmax) {
+        // bulk ZA: objects reaching each level v in [at0, dmax]
+        for (uint32_t v = at0; v <= dmax; ++v) {
+            uint32_t c = 0;
+            for (uint32_t wi = threadIdx.x * 4; wi < it.words; wi += blockDim.x * 4) {
+                const uint4 x = *reinterpret_cast<const uint4*>(sm.cnt + wi);
+                const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+#pragma unroll
+                    for (uint32_t j = 0; j < Pk::kPer; ++j) c += ((xs[e] >> (j * W)) & Pk::kMask) >= v ? 1u : 0u;
+            }
+            c = warp_sum(c);
+            if ((threadIdx.x & 31) == 0 && c) atomicAdd(&sm.za[v], c);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t a = at0;
+        while (a <= it.bound && sm.za[a] >= it.kq) ++a;
+        sm.scal[SC_AT] = a;
+    }
+    __syncthreads();
+    const uint32_t at = sm.scal[SC_AT];
+    if (at <= dmax) {  // objects already at or above AT pass the gate now
+        for (uint32_t wi = threadIdx.x; wi < it.words; wi += blockDim.x) {
+            const uint32_t x = sm.cnt[wi];
+#pragma unroll
+            for (uint32_t j = 0; j < Pk::kPer; ++j) {
+                const uint32_t c = (x >> (j * W)) & Pk::kMask;
+                if (c >= at && !ht_insert(sm.ht, it.ht_cap, wi * Pk::kPer + j, c, at)) sm.scal[SC_OVF] = 1;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// The sparse (posting-list) part of the tile: guided self-scheduling of the
+// staged slices' 128-posting groups over the warps.
+template <int W>
+__device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t nsb, uint32_t G,
+                            uint32_t unit) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = blockDim.x >> 5;
+    const uint32_t max_chunk = max(1u, unit >> 7);
+    for (;;) {
+        uint32_t g0 = 0, chunk = 0;
+        if (lane == 0) {
+            const uint32_t cur = *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_UCTR]);
+            const uint32_t rem = cur < G ? G - cur : 0u;
+            chunk = min(max_chunk, max(1u, rem / (2 * nwarps)));
+            g0 = rem ? atomicAdd(&sm.scal[SC_UCTR], chunk) : G;
+        }
+        g0 = __shfl_sync(0xffffffffu, g0, 0);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if (g0 >= G) break;
+        const uint32_t g1 = min(G, g0 + chunk);
+        while (g0 < g1) {
+            // slice holding group g0: last si with upref[si] <= g0
+            uint32_t lo = 0, hi = nsb;
+            while (lo < hi) {
+                const uint32_t m = (lo + hi) >> 1;
+                if (sm.s_upref[m] <= g0) lo = m + 1;
+                else hi = m;
+            }
+            const uint32_t si = lo - 1;
+            const uint64_t beg = sm.s_beg[si];
+            const uint64_t end = beg + sm.s_len[si];
+            const uint32_t gs = (si + 1 < nsb ? sm.s_upref[si + 1] : G);  // slice's group end
+            const uint32_t take = min(g1, gs) - g0;
+            const uint64_t gb = (beg >> 7) + (g0 - sm.s_upref[si]);
+            const uint64_t ua = max(beg, gb << 7);
+            const uint64_t ub = min(end, (gb + take) << 7);
+            if (it.gate) scan_range<W, true>(p.postings, ua, ub, it, sm);
+            else scan_range<W, false>(p.postings, ua, ub, it, sm);
+            g0 += take;
+        }
+    }
+}
+
 template <int W>
 __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t q, uint32_t t) {
     using Pk = Packing<W>;
@@ -738,11 +885,8 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     // exact-histogram fallback.  Results do not depend on the capacity.
     it.ht_cap = p.ht_slots;
 
-    // setup: zero counters, empty table, ZA, AT = 1 (cpq.hpp:281-292)
+    // setup: empty table, ZA, AT (cpq.hpp:281-292); counters below
     {
-        uint4* c4 = reinterpret_cast<uint4*>(sm.cnt);
-        const uint32_t w4 = (it.words + 3) / 4;
-        for (uint32_t i = threadIdx.x; i < w4; i += blockDim.x) c4[i] = make_uint4(0, 0, 0, 0);
         if (it.gate) {
             for (uint32_t i = threadIdx.x; i < it.ht_cap; i += blockDim.x) sm.ht[i] = kEmptySlot;
             for (uint32_t i = threadIdx.x; i <= it.bound; i += blockDim.x) sm.za[i] = 0;
@@ -755,6 +899,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
             sm.scal[SC_FLOOR] = floor;
             sm.scal[SC_OVF] = 0;
             sm.scal[SC_NOUT] = 0;
+            sm.scal[SC_NDENSE] = 0;
         }
     }
     __syncthreads();
@@ -771,13 +916,16 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     const uint64_t cb = p.q_cut_base[q];
     const uint64_t sbq = p.q_span_base[q];
     const uint32_t unit = p.unit;
+    // dense containers apply when all spans of the query fit one staging batch
+    const bool dense_ok = p.n_dense && !item_mode && S <= kSpanBatch;
+    if (!dense_ok) zero_counters(it, sm);
     // Work inside the tile: the staged slices cut into 128-posting groups
     // aligned to absolute 512-byte boundaries (only a slice's first and last
     // group are partial); warps claim runs of groups with guided
     // self-scheduling, so chunks shrink as the tile drains and the warps reach
     // the end-of-tile barrier together.
-    for (uint32_t s0 = 0; s0 < S; s0 += kSpanBatch) {
-        const uint32_t nsb = min(kSpanBatch, S - s0);
+    for (uint32_t s0 = 0; s0 < S || (S == 0 && s0 == 0); s0 += kSpanBatch) {
+        const uint32_t nsb = S ? min(kSpanBatch, S - s0) : 0u;
         uint32_t groups = 0;
         if (threadIdx.x < nsb) {
             const uint32_t s = s0 + threadIdx.x;
@@ -791,6 +939,13 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
                 const uint32_t* c = p.cuts + cb + uint64_t(s) * (nt + 1) + t;
                 beg = p.span_beg[sbq + s] + c[0];
                 len = c[1] - c[0];
+                if (dense_ok) {
+                    const int32_t d = p.key_dense[p.span_key[sbq + s]];
+                    if (d >= 0) {  // the list's bitmap covers this tile: no posting scan
+                        sm.s_dense[atomicAdd(&sm.scal[SC_NDENSE], 1u)] = static_cast<uint32_t>(d);
+                        len = 0;
+                    }
+                }
             }
             sm.s_beg[threadIdx.x] = beg;
             sm.s_len[threadIdx.x] = len;
@@ -801,44 +956,15 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         if (threadIdx.x < nsb) sm.s_upref[threadIdx.x] = static_cast<uint32_t>(ex);
         if (threadIdx.x == 0) sm.scal[SC_UCTR] = 0;
         __syncthreads();
-        const uint32_t G = static_cast<uint32_t>(total);
-        const int lane = threadIdx.x & 31;
-        const uint32_t nwarps = blockDim.x >> 5;
-        const uint32_t max_chunk = max(1u, unit >> 7);
-        for (;;) {
-            uint32_t g0 = 0, chunk = 0;
-            if (lane == 0) {
-                const uint32_t cur = *reinterpret_cast<volatile uint32_t*>(&sm.scal[SC_UCTR]);
-                const uint32_t rem = cur < G ? G - cur : 0u;
-                chunk = min(max_chunk, max(1u, rem / (2 * nwarps)));
-                g0 = rem ? atomicAdd(&sm.scal[SC_UCTR], chunk) : G;
-            }
-            g0 = __shfl_sync(0xffffffffu, g0, 0);
-            chunk = __shfl_sync(0xffffffffu, chunk, 0);
-            if (g0 >= G) break;
-            const uint32_t g1 = min(G, g0 + chunk);
-            while (g0 < g1) {
-                // slice holding group g0: last si with upref[si] <= g0
-                uint32_t lo = 0, hi = nsb;
-                while (lo < hi) {
-                    const uint32_t m = (lo + hi) >> 1;
-                    if (sm.s_upref[m] <= g0) lo = m + 1;
-                    else hi = m;
-                }
-                const uint32_t si = lo - 1;
-                const uint64_t beg = sm.s_beg[si];
-                const uint64_t end = beg + sm.s_len[si];
-                const uint32_t gs = (si + 1 < nsb ? sm.s_upref[si + 1] : G);  // slice's group end
-                const uint32_t take = min(g1, gs) - g0;
-                const uint64_t gb = (beg >> 7) + (g0 - sm.s_upref[si]);
-                const uint64_t ua = max(beg, gb << 7);
-                const uint64_t ub = min(end, (gb + take) << 7);
-                if (it.gate) scan_range<W, true>(p.postings, ua, ub, it, sm);
-                else scan_range<W, false>(p.postings, ua, ub, it, sm);
-                g0 += take;
-            }
+        if (dense_ok) {
+            const uint32_t nd = sm.scal[SC_NDENSE];
+            if (nd) dense_init<W>(p, it, sm, nd);
+            else zero_counters(it, sm);
         }
+        const uint32_t G = static_cast<uint32_t>(total);
+        scan_groups<W>(p, it, sm, nsb, G, unit);
         __syncthreads();
+        if (S == 0) break;
     }
 
 #ifdef GENIE_PHASE_TIMERS
@@ -1291,6 +1417,7 @@ static void reserve_workspace(genie_index* ix, uint32_t Q, uint32_t items, uint3
                            4096);
     if (want_spans > w.cap_spans) {
         w.span_beg.reserve(want_spans);
+        w.span_key.reserve(want_spans);
         w.cap_spans = want_spans;
     }
     if (want_cuts > w.cap_cuts) {
@@ -1316,6 +1443,7 @@ static void grow_from_status(genie_index* ix) {
     if (h[ST_TOTAL_SPANS] > w.cap_spans) {
         w.cap_spans = h[ST_TOTAL_SPANS] + (h[ST_TOTAL_SPANS] >> 2);
         w.span_beg.reserve(w.cap_spans);
+        w.span_key.reserve(w.cap_spans);
     }
     if (h[ST_TOTAL_CUTS] > w.cap_cuts) {
         w.cap_cuts = h[ST_TOTAL_CUTS] + (h[ST_TOTAL_CUTS] >> 2);
@@ -1440,6 +1568,11 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.it_nk = w.it_nk.p;
     p.it_sbase = w.it_sbase.p;
     p.span_beg = w.span_beg.p;
+    p.span_key = w.span_key.p;
+    p.key_dense = ix->key_dense.p;
+    p.bitmaps = ix->bitmaps.p;
+    p.bitmap_words = ix->bitmap_words;
+    p.n_dense = ix->n_dense;
     p.cuts = w.cuts.p;
     p.work_q = w.work_q.p;
     p.work_t = w.work_t.p;

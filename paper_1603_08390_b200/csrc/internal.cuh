@@ -50,6 +50,7 @@ struct Workspace {
     DevBuf<uint32_t> it_kb, it_nk, it_sbase;
     // spans / cuts / work / tiles
     DevBuf<uint64_t> span_beg;
+    DevBuf<uint32_t> span_key;
     DevBuf<uint32_t> cuts;
     DevBuf<uint32_t> work_q, work_t;
     DevBuf<uint32_t> tile_len;
@@ -82,6 +83,11 @@ struct genie_index {
     genie::DevBuf<uint64_t> keys, key_off;
     genie::DevBuf<uint32_t> postings;  // padded for aligned 16-byte tail loads
     genie::DevBuf<uint32_t> dim_mult;  // 65536
+    // dense containers: keys whose list covers >= dense_density of the
+    // objects also carry a bitmap of n bits (Roaring-style bitmap container)
+    genie::DevBuf<int32_t> key_dense;   // [K] slot in `bitmaps` or -1
+    genie::DevBuf<uint32_t> bitmaps;    // [n_dense][bitmap_words]
+    uint32_t n_dense = 0, bitmap_words = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
     genie::Workspace ws;

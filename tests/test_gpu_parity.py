@@ -241,3 +241,19 @@ def test_device_dim_stats_match_oracle(gpu, oracle):
         assert dm[d] == oi.max_multiplicity(d)
     back = ix.export()
     assert np.array_equal(back.keys, ds.csr.keys) and np.array_equal(back.postings, ds.csr.postings)
+
+
+@pytest.mark.parametrize("density", ["0", "0.002", "0.05", "0.125", "0.5"])
+def test_dense_containers_are_result_invariant(gpu, oracle, density, monkeypatch):
+    # lists above the density threshold carry a bitmap container that replaces
+    # their posting scan; any threshold must give the oracle's results
+    monkeypatch.setenv("GENIE_DENSE_MIN_DENSITY", density)
+    for ds in (synth.tweets(n=250_000, vocab=20_000, words=10, queries=64, k=100),
+               synth.random_instance(n=40_000, dims=3, tokens=5, max_kw=8, queries=40, max_items=40, max_span=2,
+                                     max_k=60, seed=5)):
+        want = oracle.index(ds.csr).execute(ds.queries)
+        ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+        for sel in (0, 1):
+            for tb in (0, 4096, 32768):
+                assert_same(ix.query(ds.queries, config(selector=sel, tile_bytes=tb)), want,
+                            f"density {density} sel {sel} tile {tb}")
