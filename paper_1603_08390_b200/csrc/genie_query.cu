@@ -64,7 +64,7 @@ struct BatchParams {
     uint32_t selector;
     // workspace
     uint64_t *q_bound, *q_P, *q_span_base, *q_cut_base, *q_out_base;
-    uint32_t *q_S, *q_W, *q_ntiles, *q_cap, *q_tile_base, *q_rank, *q_big, *q_floor;
+    uint32_t *q_S, *q_W, *q_ntiles, *q_cap, *q_tile_base, *q_rank, *q_big, *q_floor, *q_nd;
     uint32_t ht_slots;
     uint32_t *it_kb, *it_nk, *it_sbase;
     uint64_t* span_beg;
@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
     p.q_S[q] = carry;
     p.q_P[q] = P;
     p.q_floor[q] = 0;
+    p.q_nd[q] = 0;
     p.q_W[q] = W;
     p.q_ntiles[q] = nt;
     if (nt) atomicAdd(&p.st[ST_TOTAL_POSTINGS], static_cast<unsigned long long>(P));
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
         if (lane == 0) {
             p.span_beg[g] = beg;
             p.span_key[g] = static_cast<uint32_t>(j);
+            if (p.n_dense && p.key_dense[j] >= 0) atomicAdd(&p.q_nd[q], 1u);  // dense spans per query
         }
         const uint32_t nt = p.q_ntiles[q];
         const uint32_t T = p.tile_bits / p.q_W[q];
@@ -321,7 +323,11 @@ enum ScalarSlot {
     SC_DONE = 9,
     SC_FLOOR = 10,
     SC_NDENSE = 11,
-    SC_WORDS = 16
+    SC_G = 12,       // groups of the first staged batch
+    SC_NEXT0 = 13,   // double-buffered next work item
+    SC_NEXT1 = 14,
+    SC_LVL = 16,     // 8 dense-phase level counts
+    SC_WORDS = 24
 };
 
 __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t tile_bytes, uint32_t ht_slots) {
@@ -418,24 +424,57 @@ __device__ __forceinline__ bool ht_insert(uint64_t* ht, uint32_t cap, uint32_t i
     return false;
 }
 
-template <int W>
-struct Packing {
+// ---------------------------------------------------------------- layouts
+
+// Counter layouts of a tile (x = object id relative to the tile origin, which
+// is a multiple of 32).  Both pack 32/W counters per 32-bit word and 32
+// objects per W words:
+//   linear       word x / kPer, lane x % kPer (ids ascend inside a word): the
+//                cheapest address arithmetic for the posting scan;
+//   interleaved  word (x / 32) * W + x % W, lane (x % 32) / W: bit j of a
+//                dense bitmap word lands in word j % W at lane j / W, so a
+//                dense list adds into a 32-object block with W shift-and-mask
+//                steps (no bit spreading), and the counters equal to T of a
+//                block gather into one id-ordered 32-bit mask with W shifts.
+// Items of a query with dense containers use the interleaved layout.
+template <int W, bool IL>
+struct Lay {
     static constexpr uint32_t kPer = 32 / W;
-    static constexpr uint32_t kMask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
-    __device__ static __forceinline__ uint32_t get(const uint32_t* cnt, uint32_t local) {
-        return (cnt[local / kPer] >> ((local % kPer) * W)) & kMask;
+    static constexpr uint32_t kLogW = W == 4 ? 2 : (W == 8 ? 3 : 4);
+    static constexpr uint32_t kLogPer = 5 - kLogW;
+    static constexpr uint32_t kMask = (1u << W) - 1u;
+    __device__ static __forceinline__ uint32_t word(uint32_t x) {
+        if constexpr (IL) return ((x >> 5) << kLogW) | (x & (W - 1));
+        else return x >> kLogPer;
     }
-    // Bit (pos * W + W - 1) set for every counter equal to v.
-    __device__ static __forceinline__ uint32_t eq_mask(uint32_t x, uint32_t v) {
-        if constexpr (W == 4) {
-            const uint32_t y = x ^ (v * 0x11111111u);
-            return ~(((y & 0x77777777u) + 0x77777777u) | y | 0x77777777u);
-        } else if constexpr (W == 8) {
-            const uint32_t y = x ^ (v * 0x01010101u);
-            return ~(((y & 0x7f7f7f7fu) + 0x7f7f7f7fu) | y | 0x7f7f7f7fu);
-        } else {
-            return ((x & 0xffffu) == v ? 0x8000u : 0u) | ((x >> 16) == v ? 0x80000000u : 0u);
-        }
+    __device__ static __forceinline__ uint32_t lane(uint32_t x) {
+        if constexpr (IL) return (x >> kLogW) & (kPer - 1);
+        else return x & (kPer - 1);
+    }
+    __device__ static __forceinline__ uint32_t obj(uint32_t wi, uint32_t l) {
+        if constexpr (IL) return ((wi >> kLogW) << 5) | (l << kLogW) | (wi & (W - 1));
+        else return wi * kPer + l;
+    }
+    __device__ static __forceinline__ uint32_t get(const uint32_t* cnt, uint32_t x) {
+        return (cnt[word(x)] >> (lane(x) * W)) & kMask;
+    }
+};
+
+// Lane-wise SWAR compares of packed W-bit counters: the top bit of every lane
+// whose counter equals / is at least v (1 <= v < 2^W).
+template <int W>
+struct Swar {
+    static constexpr uint32_t kOnes = W == 4 ? 0x11111111u : (W == 8 ? 0x01010101u : 0x00010001u);
+    static constexpr uint32_t kHigh = kOnes << (W - 1);
+    static constexpr uint32_t kLow = ~kHigh;
+    __device__ static __forceinline__ uint32_t eq(uint32_t x, uint32_t v) {
+        const uint32_t y = x ^ (v * kOnes);
+        return ~(((y & kLow) + kLow) | y | kLow);
+    }
+    __device__ static __forceinline__ uint32_t ge(uint32_t x, uint32_t v) {
+        const uint32_t y = v * kOnes;
+        const uint32_t d = (x | kHigh) - (y & kLow);  // lane top bit: low(x) >= low(y)
+        return ((x & ~y) | (~(x ^ y) & d)) & kHigh;
     }
 };
 
@@ -470,13 +509,6 @@ __device__ __noinline__ uint32_t cpq_admit(uint64_t* ht, uint32_t* za, uint32_t*
     return (a - 1) << (32 - W);
 }
 
-// Count every posting of [ua, ub) (absolute positions) into the tile's
-// shared counters; with the gate on, feed the c-PQ with each new value.
-//
-// Per posting: one shared atomicAdd of 1 << shift on the packed word (exact:
-// the query's max_count_bound keeps every counter below 2^W, so no carry
-// crosses lanes), then the gate test "old value >= AT - 1" done on the word
-// shifted so the counter sits in the top W bits (one shift + one compare).
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -494,23 +526,24 @@ __device__ __forceinline__ uint32_t atom_add_shared(uint32_t addr, uint32_t v) {
 //
 // Per posting: one shared atomicAdd of 1 << shift on the packed word (exact:
 // the query's max_count_bound keeps every counter below 2^W, so no carry
-// crosses lanes).  Addresses are 32-bit shared-window offsets with the tile
-// origin folded into the base (tile_lo is a multiple of 32/W, so the lane
-// inside the word depends on the id alone).  The gate test "old value >=
-// AT - 1" is done on the word shifted so the counter sits in the top W bits,
-// as one max over the four postings of a 16-byte group and one compare.
-template <int W, bool GATE>
+// crosses lanes -- the reference's CAS loop, cpq.hpp:70-88, is not needed).
+// Addresses are 32-bit shared-window offsets with the tile origin folded into
+// the base (the tile origin is a multiple of 32 objects, so both layouts map
+// absolute ids linearly across 32-object blocks).  The gate test "old value
+// >= AT - 1" is done on the word shifted so the counter sits in the top W
+// bits, as one max over the four postings of a 16-byte group and one compare.
+template <int W, bool GATE, bool IL>
 __device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings, uint64_t ua,
                                            uint64_t ub, const ItemCtx& it, const ScanSmem& sm) {
+    using L = Lay<W, IL>;
     constexpr uint32_t kPer = 32 / W, kTop = 32 - W;
-    constexpr uint32_t kLog = W == 4 ? 3 : (W == 8 ? 2 : 1);  // log2(kPer)
     constexpr int UNR = 4;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t* base = postings + (ua & ~3ull);
     const uint32_t lo = static_cast<uint32_t>(ua & 3ull);
     const uint32_t len = static_cast<uint32_t>(ub - (ua & ~3ull));
-    // byte address of the word holding id x: cbase + (x >> kLog) * 4 (mod 2^32)
-    const uint32_t cbase = smem_u32(sm.cnt) - ((it.tile_lo >> kLog) << 2);
+    // byte address of the word holding absolute id x: cbase + word(x) * 4 (mod 2^32)
+    const uint32_t cbase = smem_u32(sm.cnt) - (L::word(it.tile_lo) << 2);
     volatile uint32_t* s_at = sm.scal + SC_AT;
     uint32_t gate = 0;
     if constexpr (GATE) gate = (*s_at - 1) << kTop;
@@ -533,8 +566,8 @@ __device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     // r = kTop - shift: the counter's distance from the top of the word
-                    const uint32_t r = ((~x[e]) & (kPer - 1)) * W;
-                    old[e] = atom_add_shared(cbase + ((x[e] >> kLog) << 2), (1u << kTop) >> r);
+                    const uint32_t r = ((~L::lane(x[e])) & (kPer - 1)) * W;
+                    old[e] = atom_add_shared(cbase + (L::word(x[e]) << 2), (1u << kTop) >> r);
                     if constexpr (GATE) top = max(top, old[e] << r);
                 }
             } else {  // edge of the range: positions in [lo, len); others add 0 to a
@@ -545,9 +578,9 @@ __device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings
                 const uint32_t word0 = smem_u32(sm.cnt) + lane * 4;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const uint32_t r = ((~x[e]) & (kPer - 1)) * W;
+                    const uint32_t r = ((~L::lane(x[e])) & (kPer - 1)) * W;
                     const bool ok = (m >> e) & 1u;
-                    old[e] = atom_add_shared(ok ? cbase + ((x[e] >> kLog) << 2) : word0,
+                    old[e] = atom_add_shared(ok ? cbase + (L::word(x[e]) << 2) : word0,
                                              ok ? (1u << kTop) >> r : 0u);
                     if constexpr (GATE) top = max(top, ok ? old[e] << r : 0u);
                 }
@@ -556,7 +589,7 @@ __device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings
                 if (top >= gate) {  // some new value may pass: check each
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const uint32_t r = ((~x[e]) & (kPer - 1)) * W;
+                        const uint32_t r = ((~L::lane(x[e])) & (kPer - 1)) * W;
                         if ((m & (1u << e)) && (old[e] << r) >= gate)
                             gate = cpq_admit<W>(sm.ht, sm.za, sm.scal, it.ht_cap, it.bound, it.kq,
                                                 x[e] - it.tile_lo, old[e], kTop - r);
@@ -577,41 +610,85 @@ __device__ __forceinline__ void emit(const BatchParams& p, const ItemCtx& it, co
     p.tile_out[it.out_base + pos] = e;
 }
 
+// Id-ordered mask of the counters equal to T in the 32-object block whose
+// W words are w[0..W) (interleaved layout: object j sits in word j % W at
+// lane j / W, and Swar::eq flags bit lane * W + W - 1).
+template <int W>
+__device__ __forceinline__ uint32_t block_eq_mask_il(const uint32_t* w, uint32_t T) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) m |= Swar<W>::eq(w[j], T) >> (W - 1 - j);
+    return m;
+}
+
 // Ties at T in ascending local id, the first `need` of them
 // (cpq.hpp:330-336).  Ordered block scan over the counter words; stops as
 // soon as enough ties were seen.
-template <int W>
+template <int W, bool IL>
 __device__ void emit_ties(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t T,
                           uint32_t need) {
-    using Pk = Packing<W>;
-    constexpr uint32_t WPT = 4;  // counter words per thread per step (one 16-byte load)
-    const uint4* c4 = reinterpret_cast<const uint4*>(sm.cnt);
-    const uint32_t w4 = (it.words + 3) / 4;  // counters past the tile are zero and never match T > 0
     unsigned long long seen = 0;
-    for (uint32_t g0 = 0; g0 < w4; g0 += blockDim.x) {
-        const uint32_t gi = g0 + threadIdx.x;
-        uint32_t m[WPT] = {0, 0, 0, 0};
-        if (gi < w4) {
-            const uint4 x = c4[gi];
-            m[0] = Pk::eq_mask(x.x, T);
-            m[1] = Pk::eq_mask(x.y, T);
-            m[2] = Pk::eq_mask(x.z, T);
-            m[3] = Pk::eq_mask(x.w, T);
-        }
-        const uint32_t c = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
-        unsigned long long total;
-        unsigned long long r = seen + block_exclusive_scan<unsigned long long>(c, sm.sums, total);
+    if constexpr (IL) {
+        // one 32-object block (W words) per thread per step
+        const uint32_t nblk = it.words / W;
+        for (uint32_t g0 = 0; g0 < nblk; g0 += blockDim.x) {
+            const uint32_t gi = g0 + threadIdx.x;
+            uint32_t m = 0;
+            if (gi < nblk) {
+                uint32_t w[W];
+                const uint4* c4 = reinterpret_cast<const uint4*>(sm.cnt + gi * W);
 #pragma unroll
-        for (uint32_t j = 0; j < WPT; ++j) {
-            while (m[j] && r < need) {
-                const uint32_t bit = __ffs(m[j]) - 1;
-                m[j] &= m[j] - 1;
-                emit(p, it, sm, (gi * WPT + j) * Pk::kPer + bit / W, T);
+                for (int j = 0; j < W / 4; ++j) {
+                    const uint4 x = c4[j];
+                    w[4 * j] = x.x;
+                    w[4 * j + 1] = x.y;
+                    w[4 * j + 2] = x.z;
+                    w[4 * j + 3] = x.w;
+                }
+                m = block_eq_mask_il<W>(w, T);
+            }
+            unsigned long long total;
+            unsigned long long r = seen + block_exclusive_scan<unsigned long long>(__popc(m), sm.sums, total);
+            while (m && r < need) {
+                const uint32_t bit = __ffs(m) - 1;
+                m &= m - 1;
+                emit(p, it, sm, gi * 32 + bit, T);
                 ++r;
             }
+            seen += total;
+            if (seen >= need) break;  // uniform: total is block-wide
         }
-        seen += total;
-        if (seen >= need) break;  // uniform: total is block-wide
+    } else {
+        using Sw = Swar<W>;
+        constexpr uint32_t kPer = 32 / W;
+        constexpr uint32_t WPT = 4;  // counter words per thread per step (one 16-byte load)
+        const uint4* c4 = reinterpret_cast<const uint4*>(sm.cnt);
+        const uint32_t w4 = it.words / 4;
+        for (uint32_t g0 = 0; g0 < w4; g0 += blockDim.x) {
+            const uint32_t gi = g0 + threadIdx.x;
+            uint32_t m[WPT] = {0, 0, 0, 0};
+            if (gi < w4) {
+                const uint4 x = c4[gi];
+                m[0] = Sw::eq(x.x, T);
+                m[1] = Sw::eq(x.y, T);
+                m[2] = Sw::eq(x.z, T);
+                m[3] = Sw::eq(x.w, T);
+            }
+            const uint32_t c = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
+            unsigned long long total;
+            unsigned long long r = seen + block_exclusive_scan<unsigned long long>(c, sm.sums, total);
+#pragma unroll
+            for (uint32_t j = 0; j < WPT; ++j) {
+                while (m[j] && r < need) {
+                    const uint32_t bit = __ffs(m[j]) - 1;
+                    m[j] &= m[j] - 1;
+                    emit(p, it, sm, (gi * WPT + j) * kPer + bit / W, T);
+                    ++r;
+                }
+            }
+            seen += total;
+            if (seen >= need) break;  // uniform: total is block-wide
+        }
     }
 }
 
@@ -619,9 +696,10 @@ __device__ void emit_ties(const BatchParams& p, const ItemCtx& it, const ScanSme
 // the fallback when the table overflowed): T = k-th largest count in the
 // tile, zeros included (0 if fewer than k non-zero), then every count > T
 // and the first ties at T in ascending id.
-template <int W>
+template <int W, bool IL>
 __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm) {
-    using Pk = Packing<W>;
+    using L = Lay<W, IL>;
+    constexpr uint32_t kPer = 32 / W;
     const int warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     uint32_t* h = reinterpret_cast<uint32_t*>(sm.ht);  // 16 warps x 256 bins
@@ -637,8 +715,8 @@ __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const S
             const uint32_t x = sm.cnt[wi];
             if (!x) continue;
 #pragma unroll
-            for (uint32_t j = 0; j < Pk::kPer; ++j) {
-                const uint32_t c = (x >> (j * W)) & Pk::kMask;
+            for (uint32_t j = 0; j < kPer; ++j) {
+                const uint32_t c = (x >> (j * W)) & L::kMask;
                 if (!c) continue;
                 if (level == 0) {
                     atomicAdd(&h[warp * 256 + (c >> kShift1)], 1u);
@@ -695,18 +773,20 @@ __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const S
         T = (W == 16) ? ((hi_sel << 8) | sel) : sel;
         above = static_cast<uint32_t>(cum);
     }
-    // emit: every count > T, then ties at T (T > 0) in ascending id
+    // emit: every count > T, then ties at T (T > 0) in ascending id; one
+    // 32-object block per thread per step (both layouts keep a block in W
+    // consecutive words)
     const uint32_t need = T ? it.kq - above : 0;
+    const uint32_t nblk = it.words / W;
     unsigned long long seen = 0;
-    for (uint32_t w0 = 0; w0 < it.words; w0 += blockDim.x) {
-        const uint32_t wi = w0 + threadIdx.x;
-        const uint32_t x = wi < it.words ? sm.cnt[wi] : 0u;
+    for (uint32_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
+        const uint32_t bi = b0 + threadIdx.x;
         uint32_t tie_mask = 0;
-        if (x) {
-#pragma unroll
-            for (uint32_t j = 0; j < Pk::kPer; ++j) {
-                const uint32_t c = (x >> (j * W)) & Pk::kMask;
-                if (c > T) emit(p, it, sm, wi * Pk::kPer + j, c);
+        if (bi < nblk) {
+#pragma unroll 4
+            for (uint32_t j = 0; j < 32; ++j) {
+                const uint32_t c = L::get(sm.cnt, bi * 32 + j);
+                if (c > T) emit(p, it, sm, bi * 32 + j, c);
                 else if (T && c == T) tie_mask |= 1u << j;
             }
         }
@@ -716,7 +796,7 @@ __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const S
         while (tie_mask && r < need) {
             const uint32_t j = __ffs(tie_mask) - 1;
             tie_mask &= tie_mask - 1;
-            emit(p, it, sm, wi * Pk::kPer + j, T);
+            emit(p, it, sm, bi * 32 + j, T);
             ++r;
         }
         seen += total;
@@ -724,106 +804,186 @@ __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const S
     return T;
 }
 
-__device__ __forceinline__ void zero_counters(const ItemCtx& it, const ScanSmem& sm) {
-    uint4* c4 = reinterpret_cast<uint4*>(sm.cnt);
-    const uint32_t w4 = (it.words + 3) / 4;
-    for (uint32_t i = threadIdx.x; i < w4; i += blockDim.x) c4[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-}
-
-// Bit j of a bitmap word -> counter increment at the counter's lane.
+// Dense phase (interleaved layout): every thread owns whole 32-object blocks
+// and initialises their counters as the sum of the query's dense bitmaps
+// (plain 16-byte stores, no atomics, no zeroing pass).  With the gate on it
+// also counts, in registers, the objects reaching each level
+// v in [at0, at0 + 8) (Swar::ge + popc), for the c-PQ catch-up below.
 template <int W>
-__device__ __forceinline__ uint32_t expand_bits(uint32_t b);
-template <>
-__device__ __forceinline__ uint32_t expand_bits<4>(uint32_t b) {  // 8 bits -> 8 nibbles
-    uint32_t x = b & 0xffu;
-    x = (x | (x << 12)) & 0x000f000fu;
-    x = (x | (x << 6)) & 0x03030303u;
-    return (x | (x << 3)) & 0x11111111u;
-}
-template <>
-__device__ __forceinline__ uint32_t expand_bits<8>(uint32_t b) {  // 4 bits -> 4 bytes
-    return ((b & 0xfu) * 0x00204081u) & 0x01010101u;
-}
-template <>
-__device__ __forceinline__ uint32_t expand_bits<16>(uint32_t b) {  // 2 bits -> 2 halves
-    return (b & 1u) | ((b & 2u) << 15);
-}
-
-// Dense phase: the counters of the tile are initialised from the bitmaps of
-// the query's dense lists (each thread owns whole counter words: plain
-// stores, no atomics).  Then the c-PQ state is brought to what one update
-// per (dense list, member object) would have produced: ZA[v] += #objects
-// with count >= v for v >= AT, AT advanced while ZA[AT] >= k, and every
-// object at or above the new AT inserted into the table (fewer than k).
-template <int W>
-__device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t nd) {
-    using Pk = Packing<W>;
-    constexpr uint32_t kWpb = W;  // counter words per 32-bit bitmap word (32 / kPer)
+__device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t nd,
+                           uint32_t at0, uint32_t nlv) {
+    using Sw = Swar<W>;
+    constexpr uint32_t BPT = W == 4 ? 4 : (W == 8 ? 2 : 1);  // blocks per thread step (16 words)
+    constexpr uint32_t NW = BPT * W;
     const uint32_t bw0 = it.tile_lo >> 5;
-    const uint32_t nbw = (it.tile_n + 31) >> 5;
-    for (uint32_t bw = threadIdx.x; bw < nbw; bw += blockDim.x) {
-        uint32_t acc[kWpb];
+    const uint32_t nblk = it.words / W;
+    uint32_t lv[kLvl] = {0, 0, 0, 0};
+    for (uint32_t b0 = threadIdx.x * BPT; b0 < nblk; b0 += blockDim.x * BPT) {
+        uint32_t acc[NW];
 #pragma unroll
-        for (uint32_t j = 0; j < kWpb; ++j) acc[j] = 0;
-        for (uint32_t d = 0; d < nd; ++d) {
-            const uint32_t b = __ldg(p.bitmaps + size_t(sm.s_dense[d]) * p.bitmap_words + bw0 + bw);
+        for (uint32_t j = 0; j < NW; ++j) acc[j] = 0;
+        const uint32_t* col = p.bitmaps + bw0 + b0;
+        uint32_t d = 0;
+        for (; d + 4 <= nd; d += 4) {  // four lists' loads in flight
+            uint32_t b[4][BPT];
 #pragma unroll
-            for (uint32_t j = 0; j < kWpb; ++j) acc[j] += expand_bits<W>(b >> (j * Pk::kPer));
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t* src = col + size_t(sm.s_dense[d + u]) * p.bitmap_words;
+                if constexpr (BPT == 4) {
+                    const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
+                    b[u][0] = x.x, b[u][1] = x.y, b[u][2] = x.z, b[u][3] = x.w;
+                } else if constexpr (BPT == 2) {
+                    const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
+                    b[u][0] = x.x, b[u][1] = x.y;
+                } else {
+                    b[u][0] = __ldg(src);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (uint32_t i = 0; i < BPT; ++i)
+#pragma unroll
+                    for (uint32_t m = 0; m < W; ++m) acc[i * W + m] += (b[u][i] >> m) & Sw::kOnes;
         }
-        uint4* dst = reinterpret_cast<uint4*>(sm.cnt + bw * kWpb);
+        for (; d < nd; ++d) {
+            const uint32_t* src = col + size_t(sm.s_dense[d]) * p.bitmap_words;
+            uint32_t b[BPT];
+            if constexpr (BPT == 4) {
+                const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
+                b[0] = x.x, b[1] = x.y, b[2] = x.z, b[3] = x.w;
+            } else if constexpr (BPT == 2) {
+                const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
+                b[0] = x.x, b[1] = x.y;
+            } else {
+                b[0] = __ldg(src);
+            }
 #pragma unroll
-        for (uint32_t j = 0; j < kWpb; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            for (uint32_t i = 0; i < BPT; ++i)
+#pragma unroll
+                for (uint32_t m = 0; m < W; ++m) acc[i * W + m] += (b[i] >> m) & Sw::kOnes;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(sm.cnt + b0 * W);
+#pragma unroll
+        for (uint32_t j = 0; j < NW; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        if (nlv) {
+#pragma unroll
+            for (uint32_t l = 0; l < kLvl; ++l) {
+                if (l < nlv) {
+#pragma unroll
+                    for (uint32_t j = 0; j < NW; ++j) lv[l] += __popc(Sw::ge(acc[j], at0 + l));
+                }
+            }
+        }
     }
-    // (tiles are multiples of 32 objects: the bitmap words cover every counter word)
+    // (the blocks of a tile come in whole thread steps: tiles are multiples
+    // of 32 * BPT objects and bitmap rows are padded to 16 bytes)
+    if (nlv) {
+#pragma unroll
+        for (uint32_t l = 0; l < kLvl; ++l) {
+            if (l < nlv) {
+                const uint32_t c = warp_sum(lv[l]);
+                if ((threadIdx.x & 31) == 0 && c) atomicAdd(&sm.scal[SC_LVL + l], c);
+            }
+        }
+    }
     __syncthreads();
-    if (!it.gate) return;
-    const uint32_t at0 = sm.scal[SC_AT];
-    const uint32_t dmax = min(nd, it.bound);
-    if (at0 <= dmax) {
-        // bulk ZA: objects reaching each level v in [at0, dmax]
-        for (uint32_t v = at0; v <= dmax; ++v) {
-            uint32_t c = 0;
+}
+
+// Brings the c-PQ state to what one gated update per (dense list, member
+// object) yields (cpq.hpp:294-301, 374-389): AT advances to the smallest
+// level v >= at0 that fewer than k objects reach (ZA below AT is never read
+// again); every object at or above the new AT -- fewer than k -- enters the
+// table and adds one to ZA[v] for each level v in [AT, count].
+template <int W>
+__device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, uint32_t dmax,
+                           uint32_t nlv) {
+    using Sw = Swar<W>;
+    using L = Lay<W, true>;
+    uint32_t j = 0;
+    while (j < nlv && sm.scal[SC_LVL + j] >= it.kq) ++j;
+    uint32_t a = at0 + j;
+    if (j == nlv && a <= dmax) {
+        // beyond the register levels: binary search for the smallest v in
+        // [a, dmax + 1] with #(count >= v) < k (block-uniform)
+        uint32_t lo = a, hi = dmax + 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            unsigned long long c = 0;
             for (uint32_t wi = threadIdx.x * 4; wi < it.words; wi += blockDim.x * 4) {
                 const uint4 x = *reinterpret_cast<const uint4*>(sm.cnt + wi);
-                const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-#pragma unroll
-                    for (uint32_t j = 0; j < Pk::kPer; ++j) c += ((xs[e] >> (j * W)) & Pk::kMask) >= v ? 1u : 0u;
+                c += __popc(Sw::ge(x.x, mid)) + __popc(Sw::ge(x.y, mid)) + __popc(Sw::ge(x.z, mid)) +
+                     __popc(Sw::ge(x.w, mid));
             }
-            c = warp_sum(c);
-            if ((threadIdx.x & 31) == 0 && c) atomicAdd(&sm.za[v], c);
+            const unsigned long long tot = block_sum<unsigned long long>(c, sm.sums);
+            if (tot >= it.kq) lo = mid + 1;
+            else hi = mid;
         }
+        a = lo;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t a = at0;
-        while (a <= it.bound && sm.za[a] >= it.kq) ++a;
-        sm.scal[SC_AT] = a;
-    }
-    __syncthreads();
-    const uint32_t at = sm.scal[SC_AT];
-    if (at <= dmax) {  // objects already at or above AT pass the gate now
+    if (threadIdx.x == 0) sm.scal[SC_AT] = a;
+    if (a <= dmax) {
         for (uint32_t wi = threadIdx.x; wi < it.words; wi += blockDim.x) {
             const uint32_t x = sm.cnt[wi];
-#pragma unroll
-            for (uint32_t j = 0; j < Pk::kPer; ++j) {
-                const uint32_t c = (x >> (j * W)) & Pk::kMask;
-                if (c >= at && !ht_insert(sm.ht, it.ht_cap, wi * Pk::kPer + j, c, at)) sm.scal[SC_OVF] = 1;
+            uint32_t m = Sw::ge(x, a);
+            while (m) {
+                const uint32_t l = (__ffs(m) - 1) / W;
+                m &= m - 1;
+                const uint32_t c = (x >> (l * W)) & L::kMask;
+                if (!ht_insert(sm.ht, it.ht_cap, L::obj(wi, l), c, a)) sm.scal[SC_OVF] = 1;
+                for (uint32_t v = a; v <= c; ++v) atomicAdd(&sm.za[v], 1u);
             }
         }
     }
     __syncthreads();
 }
 
-// The sparse (posting-list) part of the tile: guided self-scheduling of the
-// staged slices' 128-posting groups over the warps.
-template <int W>
+// One warp's share [g0, g1) of the staged slices' 128-posting groups.
+template <int W, bool IL>
+__device__ __forceinline__ void scan_group_range(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
+                                                 uint32_t nsb, uint32_t G, uint32_t g0, uint32_t g1) {
+    if (g0 >= g1) return;
+    // slice holding group g0: last si with upref[si] <= g0 (empty slices share
+    // the next slice's prefix, so this is the non-empty one)
+    uint32_t lo = 0, hi = nsb;
+    while (lo < hi) {
+        const uint32_t m = (lo + hi) >> 1;
+        if (sm.s_upref[m] <= g0) lo = m + 1;
+        else hi = m;
+    }
+    uint32_t si = lo - 1;
+    for (;;) {
+        const uint64_t beg = sm.s_beg[si];
+        const uint64_t end = beg + sm.s_len[si];
+        const uint32_t gs = (si + 1 < nsb ? sm.s_upref[si + 1] : G);  // slice's group end
+        const uint32_t take = min(g1, gs) - g0;
+        const uint64_t gb = (beg >> 7) + (g0 - sm.s_upref[si]);
+        const uint64_t ua = max(beg, gb << 7);
+        const uint64_t ub = min(end, (gb + take) << 7);
+        if (it.gate) scan_range<W, true, IL>(p.postings, ua, ub, it, sm);
+        else scan_range<W, false, IL>(p.postings, ua, ub, it, sm);
+        g0 += take;
+        if (g0 >= g1) break;
+        while (si + 1 < nsb && sm.s_upref[si + 1] <= g0) ++si;
+    }
+}
+
+// The sparse (posting-list) part of the tile.  Few groups per warp: a static
+// contiguous split (no claiming); many: guided self-scheduling of runs of
+// groups (chunks shrink as the tile drains, so the warps reach the
+// end-of-tile barrier together).
+template <int W, bool IL>
 __device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t nsb, uint32_t G,
                             uint32_t unit) {
     const int lane = threadIdx.x & 31;
+    const uint32_t warp = threadIdx.x >> 5;
     const uint32_t nwarps = blockDim.x >> 5;
+    if (G <= kStaticGroups * nwarps) {
+        const uint32_t g0 = static_cast<uint32_t>(uint64_t(G) * warp / nwarps);
+        const uint32_t g1 = static_cast<uint32_t>(uint64_t(G) * (warp + 1) / nwarps);
+        scan_group_range<W, IL>(p, it, sm, nsb, G, g0, g1);
+        return;
+    }
     const uint32_t max_chunk = max(1u, unit >> 7);
     for (;;) {
         uint32_t g0 = 0, chunk = 0;
@@ -836,33 +996,179 @@ __device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanS
         g0 = __shfl_sync(0xffffffffu, g0, 0);
         chunk = __shfl_sync(0xffffffffu, chunk, 0);
         if (g0 >= G) break;
-        const uint32_t g1 = min(G, g0 + chunk);
-        while (g0 < g1) {
-            // slice holding group g0: last si with upref[si] <= g0
-            uint32_t lo = 0, hi = nsb;
-            while (lo < hi) {
-                const uint32_t m = (lo + hi) >> 1;
-                if (sm.s_upref[m] <= g0) lo = m + 1;
-                else hi = m;
-            }
-            const uint32_t si = lo - 1;
-            const uint64_t beg = sm.s_beg[si];
-            const uint64_t end = beg + sm.s_len[si];
-            const uint32_t gs = (si + 1 < nsb ? sm.s_upref[si + 1] : G);  // slice's group end
-            const uint32_t take = min(g1, gs) - g0;
-            const uint64_t gb = (beg >> 7) + (g0 - sm.s_upref[si]);
-            const uint64_t ua = max(beg, gb << 7);
-            const uint64_t ub = min(end, (gb + take) << 7);
-            if (it.gate) scan_range<W, true>(p.postings, ua, ub, it, sm);
-            else scan_range<W, false>(p.postings, ua, ub, it, sm);
-            g0 += take;
+        scan_group_range<W, IL>(p, it, sm, nsb, G, g0, min(G, g0 + chunk));
+    }
+}
+
+// Stages spans [s0, s0 + nsb) of item (q, t): the slice of each list inside
+// the tile (s_beg, s_len), its first 128-posting group's rank (s_upref) and,
+// for dense spans, the bitmap slot (s_dense, in span order; the slice is then
+// empty).  Returns the number of groups.  Warp-only variant for nsb <= 32
+// (called by warp 0 alone, no barrier); block variant otherwise (every thread,
+// ends with a barrier).
+struct StageArgs {
+    bool item_mode, dense;
+    uint64_t i0, cb, sbq;
+    uint32_t nt;
+};
+
+__device__ __forceinline__ void stage_one(const BatchParams& p, const StageArgs& a, uint32_t t, uint32_t s,
+                                          uint64_t& beg, uint32_t& len, int32_t& dslot) {
+    dslot = -1;
+    if (a.item_mode) {
+        const uint64_t it_i = a.i0 + s, kb = p.it_kb[it_i];
+        beg = p.key_off[kb];
+        len = static_cast<uint32_t>(p.key_off[kb + p.it_nk[it_i]] - beg);
+    } else {
+        const uint32_t* c = p.cuts + a.cb + uint64_t(s) * (a.nt + 1) + t;
+        beg = p.span_beg[a.sbq + s] + c[0];
+        len = c[1] - c[0];
+        if (a.dense) {
+            dslot = p.key_dense[p.span_key[a.sbq + s]];
+            if (dslot >= 0) len = 0;  // the list's bitmap covers this tile: no posting scan
         }
     }
 }
 
+__device__ __forceinline__ uint32_t stage_warp(const BatchParams& p, const StageArgs& a, const ScanSmem& sm,
+                                               uint32_t t, uint32_t s0, uint32_t nsb) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t beg = 0;
+    uint32_t len = 0, groups = 0;
+    int32_t dslot = -1;
+    if (lane < nsb) {
+        stage_one(p, a, t, s0 + lane, beg, len, dslot);
+        groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
+    }
+    const uint32_t incl = warp_inclusive_scan(groups);
+    const uint32_t dm = __ballot_sync(0xffffffffu, dslot >= 0);
+    if (lane < nsb) {
+        sm.s_beg[lane] = beg;
+        sm.s_len[lane] = len;
+        sm.s_upref[lane] = incl - groups;
+        if (dslot >= 0) sm.s_dense[__popc(dm & ((1u << lane) - 1u))] = static_cast<uint32_t>(dslot);
+    }
+    return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+__device__ __forceinline__ uint32_t stage_block(const BatchParams& p, const StageArgs& a, const ScanSmem& sm,
+                                                uint32_t t, uint32_t s0, uint32_t nsb) {
+    uint64_t beg = 0;
+    uint32_t len = 0, groups = 0;
+    int32_t dslot = -1;
+    if (threadIdx.x < nsb) {
+        stage_one(p, a, t, s0 + threadIdx.x, beg, len, dslot);
+        groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
+    }
+    // one scan of (dense flag << 40 | groups): group ranks and dense slots
+    const unsigned long long v = (static_cast<unsigned long long>(dslot >= 0) << 40) | groups;
+    unsigned long long total;
+    const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, sm.sums, total);
+    if (threadIdx.x < nsb) {
+        sm.s_beg[threadIdx.x] = beg;
+        sm.s_len[threadIdx.x] = len;
+        sm.s_upref[threadIdx.x] = static_cast<uint32_t>(ex & ((1ull << 40) - 1));
+        if (dslot >= 0) sm.s_dense[ex >> 40] = static_cast<uint32_t>(dslot);
+    }
+    if (threadIdx.x == 0) sm.scal[SC_UCTR] = 0;
+    __syncthreads();
+    return static_cast<uint32_t>(total & ((1ull << 40) - 1));
+}
+
+// The rest of an item once its counters hold the dense part (or zeros):
+// posting scan, then the tile's exact top-k.
+__device__ __forceinline__ StageArgs stage_args(const BatchParams& p, uint32_t q, uint32_t& S) {
+    StageArgs sa;
+    sa.nt = p.q_ntiles[q];
+    // one tile: the slices are the items' keyword ranges, contiguous in the
+    // postings array (keys of one dim are adjacent); several tiles: one slice
+    // per keyword list, cut at the tile boundaries by k_cut
+    sa.item_mode = sa.nt == 1;
+    sa.i0 = p.item_off[q];
+    sa.cb = p.q_cut_base[q];
+    sa.sbq = p.q_span_base[q];
+    S = sa.item_mode ? static_cast<uint32_t>(p.item_off[q + 1] - sa.i0) : p.q_S[q];
+    // dense containers apply when all spans of the query fit one staging batch
+    sa.dense = p.n_dense && !sa.item_mode && S <= kSpanBatch;
+    return sa;
+}
+
+template <int W, bool IL>
+__device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t S,
+                                uint32_t nsb, uint32_t G) {
+    using L = Lay<W, IL>;
+#ifdef GENIE_PHASE_TIMERS
+    const long long t_setup = clock64();
+#endif
+    scan_groups<W, IL>(p, it, sm, nsb, G, p.unit);
+    __syncthreads();
+    for (uint32_t s0 = kSpanBatch; s0 < S; s0 += kSpanBatch) {  // long queries: further batches
+        uint32_t S_;
+        const StageArgs sa = stage_args(p, it.q, S_);
+        const uint32_t nb = min(kSpanBatch, S - s0);
+        const uint32_t g = stage_block(p, sa, sm, it.t, s0, nb);
+        scan_groups<W, IL>(p, it, sm, nb, g, p.unit);
+        __syncthreads();
+    }
+#ifdef GENIE_PHASE_TIMERS
+    const long long t_scanned = clock64();
+#endif
+    // ---- select: the tile's exact top-k
+    if (it.gate && !sm.scal[SC_OVF]) {
+        uint32_t a = sm.scal[SC_AT];  // every thread finishes AT (cpq.hpp:383-389)
+        while (a <= it.bound && sm.za[a] >= it.kq) ++a;
+        const uint32_t thr = a - 1;  // cpq.hpp:310-311
+        // table entries above the threshold (all touched ids when thr == 0);
+        // an id may own a stale slot -- only the slot holding its final
+        // count is reported (cpq.hpp:212-222, 391-406)
+        const uint4* ht4 = reinterpret_cast<const uint4*>(sm.ht);
+        for (uint32_t s = threadIdx.x; s < it.ht_cap / 2; s += blockDim.x) {
+            const uint4 w2 = ht4[s];
+            const uint64_t ws[2] = {(uint64_t(w2.y) << 32) | w2.x, (uint64_t(w2.w) << 32) | w2.z};
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint64_t w = ws[e];
+                if (w == kEmptySlot) continue;
+                const uint32_t id = uint32_t(w >> 32), v = uint32_t(w >> 16) & 0xffffu;
+                const uint32_t c = L::get(sm.cnt, id);
+                if (v == c && c > thr) emit(p, it, sm, id, c);
+            }
+        }
+        __syncthreads();
+        const uint32_t n_above = sm.scal[SC_NOUT];
+        const uint32_t floor = sm.scal[SC_FLOOR];
+        // thr >= floor: thr is the tile's true k-th count -> tie fill and
+        // publish it as the query's new floor.  thr < floor (AT never left
+        // the floor): fewer than k objects reach the floor here; they are all
+        // in the table and nothing below the floor can make the global top-k.
+        if (thr > 0 && thr >= floor) {
+            if (n_above < it.kq) emit_ties<W, IL>(p, it, sm, thr, it.kq - n_above);
+            if (threadIdx.x == 0) atomicMax(&p.q_floor[it.q], thr);
+        }
+    } else {
+        if (it.gate && threadIdx.x == 0) atomicAdd(&p.st[ST_FALLBACK], 1ull);
+        const uint32_t T_t = hist_select<W, IL>(p, it, sm);
+        if (it.gate && T_t > 0 && threadIdx.x == 0) atomicMax(&p.q_floor[it.q], T_t);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) p.tile_len[p.q_tile_base[it.q] + it.t] = sm.scal[SC_NOUT];
+#ifdef GENIE_PHASE_TIMERS
+    if (threadIdx.x == 0) {
+        const long long t_end = clock64();
+        atomicAdd(&p.st[ST_T_SCAN], static_cast<unsigned long long>(t_scanned - t_setup));
+        atomicAdd(&p.st[ST_T_EXTRACT], static_cast<unsigned long long>(t_end - t_scanned));
+    }
+#endif
+}
+
+__device__ __forceinline__ uint32_t fetch_item(const BatchParams& p, uint64_t total) {
+    const unsigned long long i = atomicAdd(&p.st[ST_WORK_CTR], 1ull);
+    return i < total ? static_cast<uint32_t>(i) : 0xffffffffu;
+}
+
 template <int W>
-__device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t q, uint32_t t) {
-    using Pk = Packing<W>;
+__device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t q, uint32_t t,
+                             uint32_t next_slot, uint64_t total) {
 #ifdef GENIE_PHASE_TIMERS
     const long long t_begin = clock64();
 #endif
@@ -874,7 +1180,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     const uint32_t T = p.tile_bits / W;
     it.tile_lo = t * T;
     it.tile_n = min(T, p.n - it.tile_lo);
-    it.words = (it.tile_n + Pk::kPer - 1) / Pk::kPer;
+    it.words = ((it.tile_n + 31) >> 5) * W;  // whole 32-object blocks
     it.cap = p.q_cap[q];
     it.out_base = p.q_out_base[q] + uint64_t(t) * it.cap;
     it.gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
@@ -885,136 +1191,66 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     // exact-histogram fallback.  Results do not depend on the capacity.
     it.ht_cap = p.ht_slots;
 
-    // setup: empty table, ZA, AT (cpq.hpp:281-292); counters below
-    {
-        if (it.gate) {
-            for (uint32_t i = threadIdx.x; i < it.ht_cap; i += blockDim.x) sm.ht[i] = kEmptySlot;
-            for (uint32_t i = threadIdx.x; i <= it.bound; i += blockDim.x) sm.za[i] = 0;
-        }
-        if (threadIdx.x == 0) {
-            // AT starts at the query's floor: a lower bound on the global k-th
-            // count published by this query's finished tiles (see extract)
-            const uint32_t floor = it.gate ? *reinterpret_cast<volatile uint32_t*>(&p.q_floor[q]) : 0u;
-            sm.scal[SC_AT] = floor > 1 ? floor : 1;
-            sm.scal[SC_FLOOR] = floor;
-            sm.scal[SC_OVF] = 0;
-            sm.scal[SC_NOUT] = 0;
-            sm.scal[SC_NDENSE] = 0;
-        }
-    }
-    __syncthreads();
-#ifdef GENIE_PHASE_TIMERS
-    const long long t_setup = clock64();
-#endif
-    const uint32_t nt = p.q_ntiles[q];
-    // one tile: the slices are the items' keyword ranges, contiguous in the
-    // postings array (keys of one dim are adjacent); several tiles: one slice
-    // per keyword list, cut at the tile boundaries by k_cut
-    const bool item_mode = nt == 1;
-    const uint64_t i0 = p.item_off[q];
-    const uint32_t S = item_mode ? static_cast<uint32_t>(p.item_off[q + 1] - i0) : p.q_S[q];
-    const uint64_t cb = p.q_cut_base[q];
-    const uint64_t sbq = p.q_span_base[q];
-    const uint32_t unit = p.unit;
-    // dense containers apply when all spans of the query fit one staging batch
-    const bool dense_ok = p.n_dense && !item_mode && S <= kSpanBatch;
-    if (!dense_ok) zero_counters(it, sm);
-    // Work inside the tile: the staged slices cut into 128-posting groups
-    // aligned to absolute 512-byte boundaries (only a slice's first and last
-    // group are partial); warps claim runs of groups with guided
-    // self-scheduling, so chunks shrink as the tile drains and the warps reach
-    // the end-of-tile barrier together.
-    for (uint32_t s0 = 0; s0 < S || (S == 0 && s0 == 0); s0 += kSpanBatch) {
-        const uint32_t nsb = S ? min(kSpanBatch, S - s0) : 0u;
-        uint32_t groups = 0;
-        if (threadIdx.x < nsb) {
-            const uint32_t s = s0 + threadIdx.x;
-            uint64_t beg;
-            uint32_t len;
-            if (item_mode) {
-                const uint64_t it_i = i0 + s, kb = p.it_kb[it_i];
-                beg = p.key_off[kb];
-                len = static_cast<uint32_t>(p.key_off[kb + p.it_nk[it_i]] - beg);
-            } else {
-                const uint32_t* c = p.cuts + cb + uint64_t(s) * (nt + 1) + t;
-                beg = p.span_beg[sbq + s] + c[0];
-                len = c[1] - c[0];
-                if (dense_ok) {
-                    const int32_t d = p.key_dense[p.span_key[sbq + s]];
-                    if (d >= 0) {  // the list's bitmap covers this tile: no posting scan
-                        sm.s_dense[atomicAdd(&sm.scal[SC_NDENSE], 1u)] = static_cast<uint32_t>(d);
-                        len = 0;
-                    }
-                }
-            }
-            sm.s_beg[threadIdx.x] = beg;
-            sm.s_len[threadIdx.x] = len;
-            groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
-        }
-        unsigned long long total;
-        const unsigned long long ex = block_exclusive_scan<unsigned long long>(groups, sm.sums, total);
-        if (threadIdx.x < nsb) sm.s_upref[threadIdx.x] = static_cast<uint32_t>(ex);
-        if (threadIdx.x == 0) sm.scal[SC_UCTR] = 0;
-        __syncthreads();
-        if (dense_ok) {
-            const uint32_t nd = sm.scal[SC_NDENSE];
-            if (nd) dense_init<W>(p, it, sm, nd);
-            else zero_counters(it, sm);
-        }
-        const uint32_t G = static_cast<uint32_t>(total);
-        scan_groups<W>(p, it, sm, nsb, G, unit);
-        __syncthreads();
-        if (S == 0) break;
-    }
+    uint32_t S;
+    const StageArgs sa = stage_args(p, q, S);
+    const uint32_t nd = sa.dense ? p.q_nd[q] : 0u;
+    const uint32_t nsb = min(kSpanBatch, S);
 
-#ifdef GENIE_PHASE_TIMERS
-    const long long t_scanned = clock64();
-#endif
-    // ---- select: the tile's exact top-k
-    if (it.gate && !sm.scal[SC_OVF]) {
-        if (threadIdx.x == 0) {
-            uint32_t a = sm.scal[SC_AT];
-            while (a <= it.bound && sm.za[a] >= it.kq) ++a;
-            sm.scal[SC_AT] = a;
-        }
-        __syncthreads();
-        const uint32_t thr = sm.scal[SC_AT] - 1;  // cpq.hpp:310-311
-        // table entries above the threshold (all touched ids when thr == 0);
-        // an id may own a stale slot -- only the slot holding its final
-        // count is reported (cpq.hpp:212-222, 391-406)
-        for (uint32_t s = threadIdx.x; s < it.ht_cap; s += blockDim.x) {
-            const uint64_t w = sm.ht[s];
-            if (w == kEmptySlot) continue;
-            const uint32_t id = uint32_t(w >> 32), v = uint32_t(w >> 16) & 0xffffu;
-            const uint32_t c = Pk::get(sm.cnt, id);
-            if (v == c && c > thr) emit(p, it, sm, id, c);
-        }
-        __syncthreads();
-        const uint32_t n_above = sm.scal[SC_NOUT];
-        const uint32_t floor = sm.scal[SC_FLOOR];
-        // thr >= floor: thr is the tile's true k-th count -> tie fill and
-        // publish it as the query's new floor.  thr < floor (AT never left
-        // the floor): fewer than k objects reach the floor here; they are all
-        // in the table and nothing below the floor can make the global top-k.
-        if (thr > 0 && thr >= floor) {
-            if (n_above < it.kq) emit_ties<W>(p, it, sm, thr, it.kq - n_above);
-            if (threadIdx.x == 0) atomicMax(&p.q_floor[q], thr);
-        }
-    } else {
-        if (it.gate && threadIdx.x == 0) atomicAdd(&p.st[ST_FALLBACK], 1ull);
-        const uint32_t T_t = hist_select<W>(p, it, sm);
-        if (it.gate && T_t > 0 && threadIdx.x == 0) atomicMax(&p.q_floor[q], T_t);
+    // setup (cpq.hpp:281-292): empty table and ZA, AT at the query's floor (a
+    // lower bound on the global k-th count published by its finished tiles);
+    // counters zeroed unless the dense phase writes them; the first batch of
+    // spans staged by warp 0 meanwhile when it fits a warp
+    if (it.gate) {
+        uint4* ht4 = reinterpret_cast<uint4*>(sm.ht);
+        for (uint32_t i = threadIdx.x; i < it.ht_cap / 2; i += blockDim.x) ht4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+        for (uint32_t i = threadIdx.x; i <= it.bound; i += blockDim.x) sm.za[i] = 0;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) p.tile_len[p.q_tile_base[q] + t] = sm.scal[SC_NOUT];
-#ifdef GENIE_PHASE_TIMERS
+    if (!nd) {
+        uint4* c4 = reinterpret_cast<uint4*>(sm.cnt);
+        for (uint32_t i = threadIdx.x; i < it.words / 4; i += blockDim.x) c4[i] = make_uint4(0, 0, 0, 0);
+    }
     if (threadIdx.x == 0) {
-        const long long t_end = clock64();
-        atomicAdd(&p.st[ST_T_SETUP], static_cast<unsigned long long>(t_setup - t_begin));
-        atomicAdd(&p.st[ST_T_SCAN], static_cast<unsigned long long>(t_scanned - t_setup));
-        atomicAdd(&p.st[ST_T_EXTRACT], static_cast<unsigned long long>(t_end - t_scanned));
+        const uint32_t floor = it.gate ? *reinterpret_cast<volatile uint32_t*>(&p.q_floor[q]) : 0u;
+        sm.scal[SC_AT] = floor > 1 ? floor : 1;
+        sm.scal[SC_FLOOR] = floor;
+        sm.scal[SC_OVF] = 0;
+        sm.scal[SC_NOUT] = 0;
+        sm.scal[SC_UCTR] = 0;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) sm.scal[SC_LVL + l] = 0;
+        sm.scal[next_slot] = fetch_item(p, total);  // prefetch the CTA's next item
     }
+    uint32_t G;
+    if (nsb <= 32) {
+        if (threadIdx.x < 32) {
+            const uint32_t g = stage_warp(p, sa, sm, t, 0, nsb);
+            if (threadIdx.x == 0) sm.scal[SC_G] = g;
+        }
+        __syncthreads();
+        G = sm.scal[SC_G];
+    } else {
+        __syncthreads();  // scalars (SC_UCTR) before the block staging
+        G = stage_block(p, sa, sm, t, 0, nsb);
+    }
+#ifdef GENIE_PHASE_TIMERS
+    if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_SETUP], static_cast<unsigned long long>(clock64() - t_begin));
 #endif
+    if (nd) {
+        const uint32_t at0 = sm.scal[SC_AT];
+        const uint32_t dmax = min(nd, it.bound);
+        const uint32_t nlv = (it.gate && at0 <= dmax) ? min(dmax - at0 + 1, kLvl) : 0u;
+#ifdef GENIE_PHASE_TIMERS
+        const long long t_d = clock64();
+#endif
+        dense_init<W>(p, it, sm, nd, at0, nlv);
+        if (it.gate && at0 <= dmax) dense_gate<W>(it, sm, at0, dmax, nlv);
+#ifdef GENIE_PHASE_TIMERS
+        if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_DENSE], static_cast<unsigned long long>(clock64() - t_d));
+#endif
+        scan_and_select<W, true>(p, it, sm, S, nsb, G);
+    } else {
+        scan_and_select<W, false>(p, it, sm, S, nsb, G);
+    }
 }
 
 __global__ void __launch_bounds__(kScanThreads, 2)
@@ -1023,22 +1259,20 @@ __global__ void __launch_bounds__(kScanThreads, 2)
     const ScanSmem sm = carve(smem, tile_bytes, p.ht_slots);
     if (p.st[ST_OVERFLOW]) return;
     const uint64_t total = p.st[ST_TOTAL_WORK];
-    for (;;) {
-        if (threadIdx.x == 0) {
-            const unsigned long long i = atomicAdd(&p.st[ST_WORK_CTR], 1ull);
-            sm.scal[SC_ITEM] = i < total ? static_cast<uint32_t>(i) : 0xffffffffu;
-        }
-        __syncthreads();
-        const uint32_t item = sm.scal[SC_ITEM];
-        __syncthreads();
+    // double-buffered item slots: item i's setup prefetches item i+1 into the
+    // other slot, read after item i's final barrier
+    if (threadIdx.x == 0) sm.scal[SC_NEXT0] = fetch_item(p, total);
+    __syncthreads();
+    for (uint32_t iter = 0;; ++iter) {
+        const uint32_t item = sm.scal[SC_NEXT0 + (iter & 1)];
         if (item == 0xffffffffu) break;
         const uint32_t q = p.work_q[item], t = p.work_t[item];
+        const uint32_t next_slot = SC_NEXT0 + ((iter + 1) & 1);
         switch (p.q_W[q]) {
-            case 4: process_item<4>(p, sm, q, t); break;
-            case 8: process_item<8>(p, sm, q, t); break;
-            default: process_item<16>(p, sm, q, t); break;
+            case 4: process_item<4>(p, sm, q, t, next_slot, total); break;
+            case 8: process_item<8>(p, sm, q, t, next_slot, total); break;
+            default: process_item<16>(p, sm, q, t, next_slot, total); break;
         }
-        __syncthreads();
     }
 }
 
@@ -1396,6 +1630,7 @@ static void reserve_workspace(genie_index* ix, uint32_t Q, uint32_t items, uint3
         w.q_rank.reserve(c);
         w.q_big.reserve(c);
         w.q_floor.reserve(c);
+        w.q_nd.reserve(c);
         w.cap_q = c;
     }
     if (items > w.cap_items || !w.it_kb.p) {
@@ -1464,7 +1699,7 @@ static void grow_from_status(genie_index* ix) {
 static uint32_t tile_bits_of(const genie_config& cfg) {
     uint32_t tb = cfg.tile_bytes ? cfg.tile_bytes : kDefaultTileBytes;
     tb = std::max<uint32_t>(4096, std::min<uint32_t>(tb, 160u << 10));
-    tb &= ~15u;
+    tb &= ~63u;  // tiles of whole 32-object blocks in 16-byte bitmap steps for every W
     return tb * 8;
 }
 
@@ -1564,6 +1799,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.q_rank = w.q_rank.p;
     p.q_big = w.q_big.p;
     p.q_floor = w.q_floor.p;
+    p.q_nd = w.q_nd.p;
     p.it_kb = w.it_kb.p;
     p.it_nk = w.it_nk.p;
     p.it_sbase = w.it_sbase.p;

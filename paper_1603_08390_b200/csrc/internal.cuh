@@ -13,7 +13,9 @@ constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shar
 constexpr uint32_t kDefaultTileBytes = 64u << 10;
 constexpr uint32_t kMergeThreads = 512;
 constexpr uint32_t kSortCap = 8192;           // merge entries sorted in shared memory
-constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit
+constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit (guided scheduling)
+constexpr uint32_t kLvl = 4;                  // dense-phase c-PQ levels counted in registers
+constexpr uint32_t kStaticGroups = 64;        // <= this many 128-posting groups per warp: static split
 constexpr uint64_t kEmptySlot = ~0ull;
 
 // Status block words (u64) written by the device pipeline.
@@ -38,6 +40,7 @@ enum StatusWord : int {
     ST_T_SETUP = 20,    // GENIE_PHASE_TIMERS builds: k_scan cycles per phase (thread 0 of each CTA)
     ST_T_SCAN = 21,
     ST_T_EXTRACT = 22,
+    ST_T_DENSE = 23,
     ST_WORDS = 32
 };
 
@@ -45,7 +48,7 @@ enum StatusWord : int {
 struct Workspace {
     // per query
     DevBuf<uint64_t> q_bound, q_P, q_span_base, q_cut_base, q_out_base;
-    DevBuf<uint32_t> q_S, q_W, q_ntiles, q_cap, q_tile_base, q_rank, q_big, q_floor;
+    DevBuf<uint32_t> q_S, q_W, q_ntiles, q_cap, q_tile_base, q_rank, q_big, q_floor, q_nd;
     // per item
     DevBuf<uint32_t> it_kb, it_nk, it_sbase;
     // spans / cuts / work / tiles

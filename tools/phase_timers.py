@@ -23,8 +23,8 @@ for tb in (0, 32768, 131072):
     w = np.zeros(32, np.uint64)
     err = C.create_string_buffer(256)
     N.engine().genie_debug_status(ix.handle, w.ctypes.data_as(N.u64p), 32, err, 256)
-    tot = int(w[20] + w[21] + w[22])
+    tot = int(w[20] + w[21] + w[22] + w[23])
     items = int(r.stats["work_items"])
     print(f"tile_bytes={tb or 65536}: items={items} match_ms={r.timings['match_ns']/1e6:.3f} "
-          f"setup={100*w[20]/tot:.1f}% scan={100*w[21]/tot:.1f}% extract={100*w[22]/tot:.1f}% "
+          f"setup={100*w[20]/tot:.1f}% dense={100*w[23]/tot:.1f}% scan={100*w[21]/tot:.1f}% extract={100*w[22]/tot:.1f}% "
           f"cycles/item setup={w[20]/items:.0f} scan={w[21]/items:.0f} extract={w[22]/items:.0f}")
