@@ -65,6 +65,7 @@ struct BatchParams {
     // workspace
     uint64_t *q_bound, *q_P, *q_span_base, *q_cut_base, *q_out_base;
     uint32_t *q_S, *q_W, *q_ntiles, *q_cap, *q_tile_base, *q_rank, *q_big, *q_floor, *q_nd;
+    uint32_t* tile_rec;  // [work items][kRecWords]: what each finished tile emitted (see gate_start)
     uint32_t ht_slots;
     uint32_t *it_kb, *it_nk, *it_sbase;
     uint64_t* span_beg;
@@ -255,6 +256,9 @@ __global__ void k_worklist(BatchParams p) {
         }
         p.work_q[item] = q;
         p.work_t[item] = t;
+        uint4* rec = reinterpret_cast<uint4*>(p.tile_rec + uint64_t(p.q_tile_base[q] + t) * kRecWords);
+#pragma unroll
+        for (uint32_t j = 0; j < kRecWords / 4; ++j) rec[j] = make_uint4(0, 0, 0, 0);
     }
 }
 
@@ -307,6 +311,7 @@ struct ScanSmem {
     uint32_t* s_upref;
     uint32_t* s_dense;         // dense-container slots of the staged spans
     unsigned long long* sums;  // block scan scratch (32)
+    uint32_t* ehist;           // [kHistBins] counts of this item's emitted entries
     uint32_t* scal;            // scalars
 };
 
@@ -327,7 +332,10 @@ enum ScalarSlot {
     SC_NEXT0 = 13,   // double-buffered next work item
     SC_NEXT1 = 14,
     SC_LVL = 16,     // 8 dense-phase level counts
-    SC_WORDS = 24
+    SC_BASE = 23,       // base level of the tile's record
+    SC_ADM_CALLS = 24,  // instrumented builds only
+    SC_ADM_PASS = 25,
+    SC_WORDS = 26
 };
 
 __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t tile_bytes, uint32_t ht_slots) {
@@ -348,13 +356,15 @@ __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t tile_bytes, ui
     base += kSpanBatch * sizeof(uint32_t);
     s.s_dense = reinterpret_cast<uint32_t*>(base);
     base += kSpanBatch * sizeof(uint32_t);
+    s.ehist = reinterpret_cast<uint32_t*>(base);
+    base += kHistBins * sizeof(uint32_t);
     s.scal = reinterpret_cast<uint32_t*>(base);
     return s;
 }
 
 inline size_t scan_smem_bytes(uint32_t tile_bytes, uint32_t ht_slots) {
     return tile_bytes + size_t(ht_slots) * 8 + kSpanBatch * 8 + 32 * 8 + kZaMax * 4 + kSpanBatch * 4 * 3 +
-           SC_WORDS * 4;
+           kHistBins * 4 + SC_WORDS * 4;
 }
 
 __device__ __forceinline__ uint32_t ht_home(uint32_t id, uint32_t mask) {
@@ -497,6 +507,10 @@ __device__ __noinline__ uint32_t cpq_admit(uint64_t* ht, uint32_t* za, uint32_t*
     const uint32_t val = ((old >> sh) & kMask) + 1;
     volatile uint32_t* s_at = scal + SC_AT;
     uint32_t a = *s_at;
+#ifdef GENIE_PHASE_TIMERS
+    atomicAdd(&scal[SC_ADM_CALLS], 1u);
+    if (val >= a) atomicAdd(&scal[SC_ADM_PASS], 1u);
+#endif
     if (val >= a) {
         if (!ht_insert(ht, ht_cap, local, val, a)) scal[SC_OVF] = 1;
         atomicAdd(&za[val], 1u);
@@ -537,7 +551,7 @@ __device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings
                                            uint64_t ub, const ItemCtx& it, const ScanSmem& sm) {
     using L = Lay<W, IL>;
     constexpr uint32_t kPer = 32 / W, kTop = 32 - W;
-    constexpr int UNR = 4;
+    constexpr int UNR = kScanUnroll;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t* base = postings + (ua & ~3ull);
     const uint32_t lo = static_cast<uint32_t>(ua & 3ull);
@@ -604,6 +618,7 @@ __device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings
 __device__ __forceinline__ void emit(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
                                      uint32_t local, uint32_t count) {
     const uint32_t pos = atomicAdd(&sm.scal[SC_NOUT], 1u);
+    if (it.gate) atomicAdd(&sm.ehist[count], 1u);  // count <= bound < kHistBins (W <= 8)
     genie_entry e;
     e.id = local + it.tile_lo;
     e.count = count;
@@ -1143,22 +1158,104 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
         // in the table and nothing below the floor can make the global top-k.
         if (thr > 0 && thr >= floor) {
             if (n_above < it.kq) emit_ties<W, IL>(p, it, sm, thr, it.kq - n_above);
-            if (threadIdx.x == 0) atomicMax(&p.q_floor[it.q], thr);
+            if (threadIdx.x == 0) {
+                atomicMax(&p.q_floor[it.q], thr);
+                sm.scal[SC_BASE] = thr;
+            }
+        } else if (threadIdx.x == 0) {
+            sm.scal[SC_BASE] = floor;
         }
     } else {
         if (it.gate && threadIdx.x == 0) atomicAdd(&p.st[ST_FALLBACK], 1ull);
         const uint32_t T_t = hist_select<W, IL>(p, it, sm);
         if (it.gate && T_t > 0 && threadIdx.x == 0) atomicMax(&p.q_floor[it.q], T_t);
+        if (threadIdx.x == 0) sm.scal[SC_BASE] = T_t;
     }
     __syncthreads();
     if (threadIdx.x == 0) p.tile_len[p.q_tile_base[it.q] + it.t] = sm.scal[SC_NOUT];
+    if (it.gate && threadIdx.x < 32) {
+        // the tile's record for the later tiles of its query (gate_start):
+        // base level b (every emitted entry counts >= b) and n[j] = #emitted
+        // entries counting >= b + j, j < kRecLevels
+        const uint32_t lane = threadIdx.x;
+        const uint32_t b = max(sm.scal[SC_BASE], 1u);
+        uint32_t top = 0;  // entries counting >= b + kRecLevels
+        for (uint32_t c = b + kRecLevels + lane; c <= it.bound; c += 32) top += sm.ehist[c];
+        top = warp_sum(top);
+        uint32_t* rec = p.tile_rec + uint64_t(p.q_tile_base[it.q] + it.t) * kRecWords;
+        if (lane == 0) {
+            uint32_t n = top;
+            for (int j = kRecLevels - 1; j >= 0; --j) {
+                const uint32_t c = b + j;
+                n += c <= it.bound ? sm.ehist[c] : 0u;
+                rec[1 + j] = n;
+            }
+            rec[0] = b;
+        }
+        __syncwarp();
+        for (uint32_t c = b + lane; c <= it.bound; c += 32) sm.ehist[c] = 0;
+        for (uint32_t c = lane; c < b && c <= it.bound; c += 32) sm.ehist[c] = 0;
+    }
 #ifdef GENIE_PHASE_TIMERS
     if (threadIdx.x == 0) {
         const long long t_end = clock64();
         atomicAdd(&p.st[ST_T_SCAN], static_cast<unsigned long long>(t_scanned - t_setup));
         atomicAdd(&p.st[ST_T_EXTRACT], static_cast<unsigned long long>(t_end - t_scanned));
+        atomicAdd(&p.st[ST_ADMIT_CALLS], static_cast<unsigned long long>(sm.scal[SC_ADM_CALLS]));
+        atomicAdd(&p.st[ST_ADMIT_PASS], static_cast<unsigned long long>(sm.scal[SC_ADM_PASS]));
+        sm.scal[SC_ADM_CALLS] = 0;
+        sm.scal[SC_ADM_PASS] = 0;
     }
 #endif
+}
+
+// Where the c-PQ gate of tile t of query q starts (its AuditThreshold floor).
+// Two valid lower limits for the count an object of this tile needs to make
+// the merged top-k:
+//  * F = the query's published floor: the largest k-th count of a finished
+//    tile (q_floor) -- the global k-th count (Appendix A rule 2) is at least F;
+//  * c_low + 1, where k objects of LOWER tiles (smaller ids) are known to
+//    count >= c_low: an object here counting <= c_low loses to all of them
+//    (count desc, id asc -- cpq.hpp:37-40), so it cannot enter.
+// The lower tiles' knowledge comes from their records (b, n[j] = #emitted
+// entries counting >= b + j): emitted entries are distinct objects with their
+// final counts, and a record read half-written or still zero only
+// under-counts.  Called by one whole warp.  Returns max(F, c_low + 1).
+__device__ __forceinline__ uint32_t gate_start(const BatchParams& p, uint32_t q, uint32_t t, uint32_t kq,
+                                               uint32_t bound) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t F = __ldcg(p.q_floor + q);
+    uint32_t tot[kRecLevels];  // entries of lower tiles counting >= F + j
+#pragma unroll
+    for (int j = 0; j < kRecLevels; ++j) tot[j] = 0;
+    const uint32_t* base = p.tile_rec + uint64_t(p.q_tile_base[q]) * kRecWords;
+    for (uint32_t l = lane; l < t; l += 32) {
+        const uint4* r4 = reinterpret_cast<const uint4*>(base + uint64_t(l) * kRecWords);
+        uint32_t r[kRecWords];
+#pragma unroll
+        for (int j = 0; j < int(kRecWords / 4); ++j) {
+            const uint4 x = __ldcg(r4 + j);
+            r[4 * j] = x.x, r[4 * j + 1] = x.y, r[4 * j + 2] = x.z, r[4 * j + 3] = x.w;
+        }
+        const uint32_t b = r[0];
+#pragma unroll
+        for (int j = 0; j < kRecLevels; ++j) {
+            const uint32_t c = F + j;  // level whose lower-tile population is summed
+            uint32_t n = 0;
+            if (c <= b) n = r[1];
+#pragma unroll
+            for (int i = 1; i < kRecLevels; ++i)
+                if (c == b + i) n = r[1 + i];
+            tot[j] += n;
+        }
+    }
+    uint32_t start = F;
+#pragma unroll
+    for (int j = 0; j < kRecLevels; ++j) {
+        const uint32_t s = warp_sum(tot[j]);
+        if (s >= kq && F + j >= 1) start = max(start, F + j + 1);
+    }
+    return min(start, bound + 1);
 }
 
 __device__ __forceinline__ uint32_t fetch_item(const BatchParams& p, uint64_t total) {
@@ -1209,10 +1306,14 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         uint4* c4 = reinterpret_cast<uint4*>(sm.cnt);
         for (uint32_t i = threadIdx.x; i < it.words / 4; i += blockDim.x) c4[i] = make_uint4(0, 0, 0, 0);
     }
+    if (it.gate ? threadIdx.x >> 5 == 1 : threadIdx.x == 0) {
+        const uint32_t floor = it.gate ? gate_start(p, q, t, it.kq, it.bound) : 0u;
+        if ((threadIdx.x & 31) == 0) {
+            sm.scal[SC_AT] = floor > 1 ? floor : 1;
+            sm.scal[SC_FLOOR] = floor;
+        }
+    }
     if (threadIdx.x == 0) {
-        const uint32_t floor = it.gate ? *reinterpret_cast<volatile uint32_t*>(&p.q_floor[q]) : 0u;
-        sm.scal[SC_AT] = floor > 1 ? floor : 1;
-        sm.scal[SC_FLOOR] = floor;
         sm.scal[SC_OVF] = 0;
         sm.scal[SC_NOUT] = 0;
         sm.scal[SC_UCTR] = 0;
@@ -1253,7 +1354,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     }
 }
 
-__global__ void __launch_bounds__(kScanThreads, 2)
+__global__ void __launch_bounds__(kScanThreads, 1024 / kScanThreads)
     k_scan(BatchParams p, uint32_t tile_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
     const ScanSmem sm = carve(smem, tile_bytes, p.ht_slots);
@@ -1261,7 +1362,12 @@ __global__ void __launch_bounds__(kScanThreads, 2)
     const uint64_t total = p.st[ST_TOTAL_WORK];
     // double-buffered item slots: item i's setup prefetches item i+1 into the
     // other slot, read after item i's final barrier
-    if (threadIdx.x == 0) sm.scal[SC_NEXT0] = fetch_item(p, total);
+    for (uint32_t i = threadIdx.x; i < kHistBins; i += blockDim.x) sm.ehist[i] = 0;
+    if (threadIdx.x == 0) {
+        sm.scal[SC_NEXT0] = fetch_item(p, total);
+        sm.scal[SC_ADM_CALLS] = 0;
+        sm.scal[SC_ADM_PASS] = 0;
+    }
     __syncthreads();
     for (uint32_t iter = 0;; ++iter) {
         const uint32_t item = sm.scal[SC_NEXT0 + (iter & 1)];
@@ -1663,6 +1769,7 @@ static void reserve_workspace(genie_index* ix, uint32_t Q, uint32_t items, uint3
         w.work_q.reserve(want_work);
         w.work_t.reserve(want_work);
         w.tile_len.reserve(want_work);
+        w.tile_rec.reserve(want_work * kRecWords);
         w.cap_work = want_work;
     }
     if (want_tout > w.cap_tout) {
@@ -1689,6 +1796,7 @@ static void grow_from_status(genie_index* ix) {
         w.work_q.reserve(w.cap_work);
         w.work_t.reserve(w.cap_work);
         w.tile_len.reserve(w.cap_work);
+        w.tile_rec.reserve(w.cap_work * kRecWords);
     }
     if (h[ST_TOTAL_TOUT] > w.cap_tout) {
         w.cap_tout = h[ST_TOTAL_TOUT] + (h[ST_TOTAL_TOUT] >> 2);
@@ -1800,6 +1908,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.q_big = w.q_big.p;
     p.q_floor = w.q_floor.p;
     p.q_nd = w.q_nd.p;
+    p.tile_rec = w.tile_rec.p;
     p.it_kb = w.it_kb.p;
     p.it_nk = w.it_nk.p;
     p.it_sbase = w.it_sbase.p;

@@ -5,16 +5,27 @@
 
 namespace genie {
 
-// Tunables (result-invariant).
-constexpr uint32_t kScanThreads = 512;        // 16 warps per scan CTA
+// Tunables (result-invariant).  The GENIE_SCAN_* macros exist for variant
+// builds (make variant V=<name> X="-D...") used by tools/ sweeps.
+#ifndef GENIE_SCAN_THREADS
+#define GENIE_SCAN_THREADS 512
+#endif
+#ifndef GENIE_SCAN_UNROLL
+#define GENIE_SCAN_UNROLL 4
+#endif
+constexpr uint32_t kScanThreads = GENIE_SCAN_THREADS;  // threads per scan CTA
 constexpr uint32_t kSpanBatch = 512;          // spans staged in shared memory per pass
 constexpr uint32_t kHtMaxSlots = 4096;        // shared-memory Robin Hood table (32 KB)
+constexpr uint32_t kHistBins = 256;           // emitted-count histogram of a gated tile (counts <= 255)
+constexpr int kRecLevels = 8;                 // levels in a tile's record (gate_start)
+constexpr uint32_t kRecWords = 12;            // record: base level + kRecLevels counts, padded to 16 B
 constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shared memory (W <= 8)
 constexpr uint32_t kDefaultTileBytes = 64u << 10;
 constexpr uint32_t kMergeThreads = 512;
 constexpr uint32_t kSortCap = 8192;           // merge entries sorted in shared memory
 constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit (guided scheduling)
 constexpr uint32_t kLvl = 4;                  // dense-phase c-PQ levels counted in registers
+constexpr int kScanUnroll = GENIE_SCAN_UNROLL;               // 128-posting groups loaded per warp pass
 constexpr uint32_t kStaticGroups = 64;        // <= this many 128-posting groups per warp: static split
 constexpr uint64_t kEmptySlot = ~0ull;
 
@@ -41,6 +52,8 @@ enum StatusWord : int {
     ST_T_SCAN = 21,
     ST_T_EXTRACT = 22,
     ST_T_DENSE = 23,
+    ST_ADMIT_CALLS = 24,  // GENIE_PHASE_TIMERS builds: c-PQ admit path entries / passes
+    ST_ADMIT_PASS = 25,
     ST_WORDS = 32
 };
 
@@ -57,6 +70,7 @@ struct Workspace {
     DevBuf<uint32_t> cuts;
     DevBuf<uint32_t> work_q, work_t;
     DevBuf<uint32_t> tile_len;
+    DevBuf<uint32_t> tile_rec;  // [work items][kRecWords]
     DevBuf<genie_entry> tile_out;
     // status
     DevBuf<unsigned long long> status;
