@@ -302,17 +302,40 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
 
 // ------------------------------------------------------------------- scan
 
+// Staged slices of one item (double-buffered: warp 0 stages item i + 1 while
+// the other warps scan item i).
+struct StageBuf {
+    uint8_t* base;
+    // slice start (absolute posting position)
+    __device__ __forceinline__ uint64_t* beg() const { return reinterpret_cast<uint64_t*>(base); }
+    // slice length (0 for dense spans)
+    __device__ __forceinline__ uint32_t* len() const { return reinterpret_cast<uint32_t*>(base + kSpanBatch * 8); }
+    // rank of the slice's first 128-posting group
+    __device__ __forceinline__ uint32_t* upref() const { return reinterpret_cast<uint32_t*>(base + kSpanBatch * 12); }
+    // dense-container slots of the staged spans, in span order
+    __device__ __forceinline__ uint32_t* dense() const { return reinterpret_cast<uint32_t*>(base + kSpanBatch * 16); }
+};
+
+// One work item as prepared by warp 0 (prepare_item); 64 bytes.
+struct ItemDesc {
+    uint32_t valid, q, t, kq, bound, W, cap, nt, S, nd, G, a0;
+    uint64_t out_base;
+    uint32_t pad[2];
+};
+
+// Shared memory of a scan CTA.  Everything but the counters sits at a fixed
+// offset from the dynamic shared base (compile-time addresses, no pointer
+// registers); the counter tile comes last because its size is a knob.
 struct ScanSmem {
-    uint32_t* cnt;        // packed counters of the tile
-    uint64_t* ht;         // Robin Hood table / histogram scratch
-    uint32_t* za;         // ZipperArray, levels [0, bound]
-    uint64_t* s_beg;      // staged slices
-    uint32_t* s_len;
-    uint32_t* s_upref;
-    uint32_t* s_dense;         // dense-container slots of the staged spans
+    uint32_t* cnt;             // packed counters of the tile
+    uint64_t* ht;              // Robin Hood table / histogram scratch
+    uint32_t* za;              // ZipperArray, levels [0, bound]
     unsigned long long* sums;  // block scan scratch (32)
     uint32_t* ehist;           // [kHistBins] counts of this item's emitted entries
     uint32_t* scal;            // scalars
+    ItemDesc* desc;            // [2]
+    uint8_t* stage;            // 2 x StageBuf
+    __device__ __forceinline__ StageBuf sb(uint32_t b) const { return StageBuf{stage + b * (kSpanBatch * 20)}; }
 };
 
 enum ScalarSlot {
@@ -329,42 +352,43 @@ enum ScalarSlot {
     SC_FLOOR = 10,
     SC_NDENSE = 11,
     SC_G = 12,       // groups of the first staged batch
-    SC_NEXT0 = 13,   // double-buffered next work item
-    SC_NEXT1 = 14,
     SC_LVL = 16,     // 8 dense-phase level counts
     SC_BASE = 23,       // base level of the tile's record
     SC_ADM_CALLS = 24,  // instrumented builds only
     SC_ADM_PASS = 25,
     SC_WORDS = 26
 };
+static_assert(SC_WORDS <= 32, "scalar area");
 
-__device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t tile_bytes, uint32_t ht_slots) {
+namespace smem_off {
+constexpr uint32_t kScal = 0;                                  // SC_WORDS u32 (<= 32)
+constexpr uint32_t kSums = 128;                                // 32 u64
+constexpr uint32_t kDesc = kSums + 256;                        // 2 x ItemDesc
+constexpr uint32_t kZa = kDesc + 2 * sizeof(ItemDesc);         // kZaMax u32
+constexpr uint32_t kEhist = kZa + kZaMax * 4;                  // kHistBins u32
+constexpr uint32_t kStage = kEhist + kHistBins * 4;            // 2 x StageBuf
+constexpr uint32_t kStageBytes = kSpanBatch * (8 + 4 + 4 + 4);
+constexpr uint32_t kHt = kStage + 2 * kStageBytes;             // ht_slots u64, then the tile
+static_assert(kHt % 16 == 0, "16-byte aligned table");
+}  // namespace smem_off
+
+__device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t ht_slots) {
+    using namespace smem_off;
     ScanSmem s;
-    s.cnt = reinterpret_cast<uint32_t*>(base);
-    base += tile_bytes;
-    s.ht = reinterpret_cast<uint64_t*>(base);
-    base += ht_slots * sizeof(uint64_t);
-    s.s_beg = reinterpret_cast<uint64_t*>(base);
-    base += kSpanBatch * sizeof(uint64_t);
-    s.sums = reinterpret_cast<unsigned long long*>(base);
-    base += 32 * sizeof(unsigned long long);
-    s.za = reinterpret_cast<uint32_t*>(base);
-    base += kZaMax * sizeof(uint32_t);
-    s.s_len = reinterpret_cast<uint32_t*>(base);
-    base += kSpanBatch * sizeof(uint32_t);
-    s.s_upref = reinterpret_cast<uint32_t*>(base);
-    base += kSpanBatch * sizeof(uint32_t);
-    s.s_dense = reinterpret_cast<uint32_t*>(base);
-    base += kSpanBatch * sizeof(uint32_t);
-    s.ehist = reinterpret_cast<uint32_t*>(base);
-    base += kHistBins * sizeof(uint32_t);
-    s.scal = reinterpret_cast<uint32_t*>(base);
+    s.scal = reinterpret_cast<uint32_t*>(base + kScal);
+    s.sums = reinterpret_cast<unsigned long long*>(base + kSums);
+    s.desc = reinterpret_cast<ItemDesc*>(base + kDesc);
+    s.za = reinterpret_cast<uint32_t*>(base + kZa);
+    s.ehist = reinterpret_cast<uint32_t*>(base + kEhist);
+    s.stage = base + kStage;
+    static_assert(kStageBytes == kSpanBatch * 20, "stage buffer layout");
+    s.ht = reinterpret_cast<uint64_t*>(base + kHt);
+    s.cnt = reinterpret_cast<uint32_t*>(base + kHt + size_t(ht_slots) * 8);
     return s;
 }
 
 inline size_t scan_smem_bytes(uint32_t tile_bytes, uint32_t ht_slots) {
-    return tile_bytes + size_t(ht_slots) * 8 + kSpanBatch * 8 + 32 * 8 + kZaMax * 4 + kSpanBatch * 4 * 3 +
-           kHistBins * 4 + SC_WORDS * 4;
+    return smem_off::kHt + size_t(ht_slots) * 8 + tile_bytes;
 }
 
 __device__ __forceinline__ uint32_t ht_home(uint32_t id, uint32_t mask) {
@@ -825,7 +849,7 @@ __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const S
 // also counts, in registers, the objects reaching each level
 // v in [at0, at0 + 8) (Swar::ge + popc), for the c-PQ catch-up below.
 template <int W>
-__device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t nd,
+__device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb, uint32_t nd,
                            uint32_t at0, uint32_t nlv) {
     using Sw = Swar<W>;
     constexpr uint32_t BPT = W == 4 ? 4 : (W == 8 ? 2 : 1);  // blocks per thread step (16 words)
@@ -843,7 +867,7 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
             uint32_t b[4][BPT];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint32_t* src = col + size_t(sm.s_dense[d + u]) * p.bitmap_words;
+                const uint32_t* src = col + size_t(sb.dense()[d + u]) * p.bitmap_words;
                 if constexpr (BPT == 4) {
                     const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
                     b[u][0] = x.x, b[u][1] = x.y, b[u][2] = x.z, b[u][3] = x.w;
@@ -862,7 +886,7 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
                     for (uint32_t m = 0; m < W; ++m) acc[i * W + m] += (b[u][i] >> m) & Sw::kOnes;
         }
         for (; d < nd; ++d) {
-            const uint32_t* src = col + size_t(sm.s_dense[d]) * p.bitmap_words;
+            const uint32_t* src = col + size_t(sb.dense()[d]) * p.bitmap_words;
             uint32_t b[BPT];
             if constexpr (BPT == 4) {
                 const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
@@ -956,30 +980,31 @@ __device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, 
 // One warp's share [g0, g1) of the staged slices' 128-posting groups.
 template <int W, bool IL>
 __device__ __forceinline__ void scan_group_range(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
-                                                 uint32_t nsb, uint32_t G, uint32_t g0, uint32_t g1) {
+                                                 const StageBuf& sb, uint32_t nsb, uint32_t G, uint32_t g0,
+                                                 uint32_t g1) {
     if (g0 >= g1) return;
     // slice holding group g0: last si with upref[si] <= g0 (empty slices share
     // the next slice's prefix, so this is the non-empty one)
     uint32_t lo = 0, hi = nsb;
     while (lo < hi) {
         const uint32_t m = (lo + hi) >> 1;
-        if (sm.s_upref[m] <= g0) lo = m + 1;
+        if (sb.upref()[m] <= g0) lo = m + 1;
         else hi = m;
     }
     uint32_t si = lo - 1;
     for (;;) {
-        const uint64_t beg = sm.s_beg[si];
-        const uint64_t end = beg + sm.s_len[si];
-        const uint32_t gs = (si + 1 < nsb ? sm.s_upref[si + 1] : G);  // slice's group end
+        const uint64_t beg = sb.beg()[si];
+        const uint64_t end = beg + sb.len()[si];
+        const uint32_t gs = (si + 1 < nsb ? sb.upref()[si + 1] : G);  // slice's group end
         const uint32_t take = min(g1, gs) - g0;
-        const uint64_t gb = (beg >> 7) + (g0 - sm.s_upref[si]);
+        const uint64_t gb = (beg >> 7) + (g0 - sb.upref()[si]);
         const uint64_t ua = max(beg, gb << 7);
         const uint64_t ub = min(end, (gb + take) << 7);
         if (it.gate) scan_range<W, true, IL>(p.postings, ua, ub, it, sm);
         else scan_range<W, false, IL>(p.postings, ua, ub, it, sm);
         g0 += take;
         if (g0 >= g1) break;
-        while (si + 1 < nsb && sm.s_upref[si + 1] <= g0) ++si;
+        while (si + 1 < nsb && sb.upref()[si + 1] <= g0) ++si;
     }
 }
 
@@ -988,15 +1013,16 @@ __device__ __forceinline__ void scan_group_range(const BatchParams& p, const Ite
 // groups (chunks shrink as the tile drains, so the warps reach the
 // end-of-tile barrier together).
 template <int W, bool IL>
-__device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t nsb, uint32_t G,
-                            uint32_t unit) {
+__device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb,
+                            uint32_t nsb, uint32_t G, uint32_t unit, uint32_t wfirst) {
+    // warps [wfirst, nwarps) scan
     const int lane = threadIdx.x & 31;
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t nwarps = blockDim.x >> 5;
+    const uint32_t warp = (threadIdx.x >> 5) - wfirst;
+    const uint32_t nwarps = (blockDim.x >> 5) - wfirst;
     if (G <= kStaticGroups * nwarps) {
         const uint32_t g0 = static_cast<uint32_t>(uint64_t(G) * warp / nwarps);
         const uint32_t g1 = static_cast<uint32_t>(uint64_t(G) * (warp + 1) / nwarps);
-        scan_group_range<W, IL>(p, it, sm, nsb, G, g0, g1);
+        scan_group_range<W, IL>(p, it, sm, sb, nsb, G, g0, g1);
         return;
     }
     const uint32_t max_chunk = max(1u, unit >> 7);
@@ -1011,7 +1037,7 @@ __device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanS
         g0 = __shfl_sync(0xffffffffu, g0, 0);
         chunk = __shfl_sync(0xffffffffu, chunk, 0);
         if (g0 >= G) break;
-        scan_group_range<W, IL>(p, it, sm, nsb, G, g0, min(G, g0 + chunk));
+        scan_group_range<W, IL>(p, it, sm, sb, nsb, G, g0, min(G, g0 + chunk));
     }
 }
 
@@ -1045,29 +1071,38 @@ __device__ __forceinline__ void stage_one(const BatchParams& p, const StageArgs&
     }
 }
 
-__device__ __forceinline__ uint32_t stage_warp(const BatchParams& p, const StageArgs& a, const ScanSmem& sm,
+// Warp variant: spans [s0, s0 + nsb), nsb <= kSpanBatch, 32 at a time.
+__device__ __forceinline__ uint32_t stage_warp(const BatchParams& p, const StageArgs& a, const StageBuf& sb,
                                                uint32_t t, uint32_t s0, uint32_t nsb) {
     const uint32_t lane = threadIdx.x & 31;
-    uint64_t beg = 0;
-    uint32_t len = 0, groups = 0;
-    int32_t dslot = -1;
-    if (lane < nsb) {
-        stage_one(p, a, t, s0 + lane, beg, len, dslot);
-        groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
+    uint32_t carry = 0, dcarry = 0;
+    for (uint32_t c0 = 0; c0 < nsb; c0 += 32) {
+        const uint32_t i = c0 + lane;
+        uint64_t beg = 0;
+        uint32_t len = 0, groups = 0;
+        int32_t dslot = -1;
+        if (i < nsb) {
+            stage_one(p, a, t, s0 + i, beg, len, dslot);
+            groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
+        }
+        const uint32_t incl = warp_inclusive_scan(groups);
+        const uint32_t dm = __ballot_sync(0xffffffffu, dslot >= 0);
+        if (i < nsb) {
+            sb.beg()[i] = beg;
+            sb.len()[i] = len;
+            sb.upref()[i] = carry + incl - groups;
+            if (dslot >= 0) sb.dense()[dcarry + __popc(dm & ((1u << lane) - 1u))] = static_cast<uint32_t>(dslot);
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+        dcarry += __popc(dm);
     }
-    const uint32_t incl = warp_inclusive_scan(groups);
-    const uint32_t dm = __ballot_sync(0xffffffffu, dslot >= 0);
-    if (lane < nsb) {
-        sm.s_beg[lane] = beg;
-        sm.s_len[lane] = len;
-        sm.s_upref[lane] = incl - groups;
-        if (dslot >= 0) sm.s_dense[__popc(dm & ((1u << lane) - 1u))] = static_cast<uint32_t>(dslot);
-    }
-    return __shfl_sync(0xffffffffu, incl, 31);
+    return carry;
 }
 
+// Block variant (every thread; ends with a barrier): the further batches of
+// queries with more than kSpanBatch spans.
 __device__ __forceinline__ uint32_t stage_block(const BatchParams& p, const StageArgs& a, const ScanSmem& sm,
-                                                uint32_t t, uint32_t s0, uint32_t nsb) {
+                                                const StageBuf& sb, uint32_t t, uint32_t s0, uint32_t nsb) {
     uint64_t beg = 0;
     uint32_t len = 0, groups = 0;
     int32_t dslot = -1;
@@ -1080,10 +1115,10 @@ __device__ __forceinline__ uint32_t stage_block(const BatchParams& p, const Stag
     unsigned long long total;
     const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, sm.sums, total);
     if (threadIdx.x < nsb) {
-        sm.s_beg[threadIdx.x] = beg;
-        sm.s_len[threadIdx.x] = len;
-        sm.s_upref[threadIdx.x] = static_cast<uint32_t>(ex & ((1ull << 40) - 1));
-        if (dslot >= 0) sm.s_dense[ex >> 40] = static_cast<uint32_t>(dslot);
+        sb.beg()[threadIdx.x] = beg;
+        sb.len()[threadIdx.x] = len;
+        sb.upref()[threadIdx.x] = static_cast<uint32_t>(ex & ((1ull << 40) - 1));
+        if (dslot >= 0) sb.dense()[ex >> 40] = static_cast<uint32_t>(dslot);
     }
     if (threadIdx.x == 0) sm.scal[SC_UCTR] = 0;
     __syncthreads();
@@ -1108,21 +1143,25 @@ __device__ __forceinline__ StageArgs stage_args(const BatchParams& p, uint32_t q
     return sa;
 }
 
+__device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint64_t total);
+
 template <int W, bool IL>
-__device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t S,
-                                uint32_t nsb, uint32_t G) {
+__device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t b,
+                                uint32_t S, uint32_t nsb, uint32_t G, uint64_t total) {
     using L = Lay<W, IL>;
 #ifdef GENIE_PHASE_TIMERS
     const long long t_setup = clock64();
 #endif
-    scan_groups<W, IL>(p, it, sm, nsb, G, p.unit);
+    // warps 1.. scan this item's postings while warp 0 prepares the next item
+    if (threadIdx.x < 32) prepare_item(p, sm, b ^ 1u, total);
+    else scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1);
     __syncthreads();
     for (uint32_t s0 = kSpanBatch; s0 < S; s0 += kSpanBatch) {  // long queries: further batches
         uint32_t S_;
         const StageArgs sa = stage_args(p, it.q, S_);
         const uint32_t nb = min(kSpanBatch, S - s0);
-        const uint32_t g = stage_block(p, sa, sm, it.t, s0, nb);
-        scan_groups<W, IL>(p, it, sm, nb, g, p.unit);
+        const uint32_t g = stage_block(p, sa, sm, sm.sb(b), it.t, s0, nb);
+        scan_groups<W, IL>(p, it, sm, sm.sb(b), nb, g, p.unit, 0);
         __syncthreads();
     }
 #ifdef GENIE_PHASE_TIMERS
@@ -1263,23 +1302,65 @@ __device__ __forceinline__ uint32_t fetch_item(const BatchParams& p, uint64_t to
     return i < total ? static_cast<uint32_t>(i) : 0xffffffffu;
 }
 
+// Warp 0: the CTA's next work item -- claims it, loads its parameters,
+// stages its first batch of spans into stage buffer `buf` and computes where
+// its c-PQ gate starts -- into desc[buf] (valid = 0 when the queue is empty).
+// Runs while the other warps scan the current item, so an item starts with
+// everything it needs already in shared memory.
+__device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint64_t total) {
+    const uint32_t lane = threadIdx.x & 31;
+    ItemDesc* d = sm.desc + buf;
+    uint32_t item = 0;
+    if (lane == 0) item = fetch_item(p, total);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item == 0xffffffffu) {
+        if (lane == 0) d->valid = 0;
+        return;
+    }
+    const uint32_t q = p.work_q[item], t = p.work_t[item];
+    uint32_t S;
+    const StageArgs sa = stage_args(p, q, S);
+    const uint32_t W = p.q_W[q];
+    const uint32_t kq = p.k[q];
+    const uint32_t bound = static_cast<uint32_t>(p.q_bound[q] < 1 ? 1 : p.q_bound[q]);
+    const bool gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
+    const uint32_t a0 = gate ? gate_start(p, q, t, kq, bound) : 0u;
+    const uint32_t G = stage_warp(p, sa, sm.sb(buf), t, 0, min(kSpanBatch, S));
+    if (lane == 0) {
+        const uint32_t cap = p.q_cap[q];
+        d->q = q;
+        d->t = t;
+        d->kq = kq;
+        d->bound = bound;
+        d->W = W;
+        d->cap = cap;
+        d->nt = sa.nt;
+        d->S = S;
+        d->nd = sa.dense ? p.q_nd[q] : 0u;
+        d->G = G;
+        d->a0 = a0;
+        d->out_base = p.q_out_base[q] + uint64_t(t) * cap;
+        d->valid = 1;
+    }
+}
+
 template <int W>
-__device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t q, uint32_t t,
-                             uint32_t next_slot, uint64_t total) {
+__device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t b, uint64_t total) {
 #ifdef GENIE_PHASE_TIMERS
     const long long t_begin = clock64();
 #endif
+    const ItemDesc& d = sm.desc[b];
     ItemCtx it;
-    it.q = q;
-    it.t = t;
-    it.kq = p.k[q];
-    it.bound = static_cast<uint32_t>(p.q_bound[q] < 1 ? 1 : p.q_bound[q]);
+    it.q = d.q;
+    it.t = d.t;
+    it.kq = d.kq;
+    it.bound = d.bound;
     const uint32_t T = p.tile_bits / W;
-    it.tile_lo = t * T;
+    it.tile_lo = it.t * T;
     it.tile_n = min(T, p.n - it.tile_lo);
     it.words = ((it.tile_n + 31) >> 5) * W;  // whole 32-object blocks
-    it.cap = p.q_cap[q];
-    it.out_base = p.q_out_base[q] + uint64_t(t) * it.cap;
+    it.cap = d.cap;
+    it.out_base = d.out_base;
     it.gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
     // The table always uses the whole reserved shared region (the reference
     // sizes it bit_ceil(2 k bound), cpq.hpp:137-138, 283; that figure is kept
@@ -1287,16 +1368,11 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     // thread before AT can move, and a larger table absorbs them without the
     // exact-histogram fallback.  Results do not depend on the capacity.
     it.ht_cap = p.ht_slots;
-
-    uint32_t S;
-    const StageArgs sa = stage_args(p, q, S);
-    const uint32_t nd = sa.dense ? p.q_nd[q] : 0u;
+    const uint32_t S = d.S, nd = d.nd, G = d.G;
     const uint32_t nsb = min(kSpanBatch, S);
 
-    // setup (cpq.hpp:281-292): empty table and ZA, AT at the query's floor (a
-    // lower bound on the global k-th count published by its finished tiles);
-    // counters zeroed unless the dense phase writes them; the first batch of
-    // spans staged by warp 0 meanwhile when it fits a warp
+    // setup (cpq.hpp:281-292): empty table and ZA, AT at the gate start
+    // (gate_start); counters zeroed unless the dense phase writes them
     if (it.gate) {
         uint4* ht4 = reinterpret_cast<uint4*>(sm.ht);
         for (uint32_t i = threadIdx.x; i < it.ht_cap / 2; i += blockDim.x) ht4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
@@ -1306,33 +1382,17 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         uint4* c4 = reinterpret_cast<uint4*>(sm.cnt);
         for (uint32_t i = threadIdx.x; i < it.words / 4; i += blockDim.x) c4[i] = make_uint4(0, 0, 0, 0);
     }
-    if (it.gate ? threadIdx.x >> 5 == 1 : threadIdx.x == 0) {
-        const uint32_t floor = it.gate ? gate_start(p, q, t, it.kq, it.bound) : 0u;
-        if ((threadIdx.x & 31) == 0) {
-            sm.scal[SC_AT] = floor > 1 ? floor : 1;
-            sm.scal[SC_FLOOR] = floor;
-        }
-    }
     if (threadIdx.x == 0) {
+        const uint32_t floor = it.gate ? d.a0 : 0u;
+        sm.scal[SC_AT] = floor > 1 ? floor : 1;
+        sm.scal[SC_FLOOR] = floor;
         sm.scal[SC_OVF] = 0;
         sm.scal[SC_NOUT] = 0;
         sm.scal[SC_UCTR] = 0;
 #pragma unroll
         for (int l = 0; l < 8; ++l) sm.scal[SC_LVL + l] = 0;
-        sm.scal[next_slot] = fetch_item(p, total);  // prefetch the CTA's next item
     }
-    uint32_t G;
-    if (nsb <= 32) {
-        if (threadIdx.x < 32) {
-            const uint32_t g = stage_warp(p, sa, sm, t, 0, nsb);
-            if (threadIdx.x == 0) sm.scal[SC_G] = g;
-        }
-        __syncthreads();
-        G = sm.scal[SC_G];
-    } else {
-        __syncthreads();  // scalars (SC_UCTR) before the block staging
-        G = stage_block(p, sa, sm, t, 0, nsb);
-    }
+    __syncthreads();
 #ifdef GENIE_PHASE_TIMERS
     if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_SETUP], static_cast<unsigned long long>(clock64() - t_begin));
 #endif
@@ -1343,41 +1403,40 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
 #ifdef GENIE_PHASE_TIMERS
         const long long t_d = clock64();
 #endif
-        dense_init<W>(p, it, sm, nd, at0, nlv);
+        dense_init<W>(p, it, sm, sm.sb(b), nd, at0, nlv);
         if (it.gate && at0 <= dmax) dense_gate<W>(it, sm, at0, dmax, nlv);
 #ifdef GENIE_PHASE_TIMERS
         if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_DENSE], static_cast<unsigned long long>(clock64() - t_d));
 #endif
-        scan_and_select<W, true>(p, it, sm, S, nsb, G);
+        scan_and_select<W, true>(p, it, sm, b, S, nsb, G, total);
     } else {
-        scan_and_select<W, false>(p, it, sm, S, nsb, G);
+        scan_and_select<W, false>(p, it, sm, b, S, nsb, G, total);
     }
 }
 
 __global__ void __launch_bounds__(kScanThreads, 1024 / kScanThreads)
     k_scan(BatchParams p, uint32_t tile_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const ScanSmem sm = carve(smem, tile_bytes, p.ht_slots);
+    (void)tile_bytes;
+    const ScanSmem sm = carve(smem, p.ht_slots);
     if (p.st[ST_OVERFLOW]) return;
     const uint64_t total = p.st[ST_TOTAL_WORK];
-    // double-buffered item slots: item i's setup prefetches item i+1 into the
-    // other slot, read after item i's final barrier
+    // item i runs from desc[i & 1]; its scan phase prepares item i + 1 into
+    // the other descriptor / stage buffer (prepare_item)
+    if (threadIdx.x < 32) prepare_item(p, sm, 0, total);
     for (uint32_t i = threadIdx.x; i < kHistBins; i += blockDim.x) sm.ehist[i] = 0;
     if (threadIdx.x == 0) {
-        sm.scal[SC_NEXT0] = fetch_item(p, total);
         sm.scal[SC_ADM_CALLS] = 0;
         sm.scal[SC_ADM_PASS] = 0;
     }
     __syncthreads();
     for (uint32_t iter = 0;; ++iter) {
-        const uint32_t item = sm.scal[SC_NEXT0 + (iter & 1)];
-        if (item == 0xffffffffu) break;
-        const uint32_t q = p.work_q[item], t = p.work_t[item];
-        const uint32_t next_slot = SC_NEXT0 + ((iter + 1) & 1);
-        switch (p.q_W[q]) {
-            case 4: process_item<4>(p, sm, q, t, next_slot, total); break;
-            case 8: process_item<8>(p, sm, q, t, next_slot, total); break;
-            default: process_item<16>(p, sm, q, t, next_slot, total); break;
+        const uint32_t b = iter & 1u;
+        if (!sm.desc[b].valid) break;
+        switch (sm.desc[b].W) {
+            case 4: process_item<4>(p, sm, b, total); break;
+            case 8: process_item<8>(p, sm, b, total); break;
+            default: process_item<16>(p, sm, b, total); break;
         }
     }
 }

@@ -14,7 +14,7 @@ namespace genie {
 #define GENIE_SCAN_UNROLL 4
 #endif
 constexpr uint32_t kScanThreads = GENIE_SCAN_THREADS;  // threads per scan CTA
-constexpr uint32_t kSpanBatch = 512;          // spans staged in shared memory per pass
+constexpr uint32_t kSpanBatch = 256;          // spans staged in shared memory per pass (x2 buffers)
 constexpr uint32_t kHtMaxSlots = 4096;        // shared-memory Robin Hood table (32 KB)
 constexpr uint32_t kHistBins = 256;           // emitted-count histogram of a gated tile (counts <= 255)
 constexpr int kRecLevels = 8;                 // levels in a tile's record (gate_start)
