@@ -83,12 +83,21 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
+#ifndef GENIE_LDG_MODE
+#define GENIE_LDG_MODE 0
+#endif
 __device__ __forceinline__ uint4 ldg_stream_v4(const uint32_t* p) {
+#if GENIE_LDG_MODE == 1
+    return __ldg(reinterpret_cast<const uint4*>(p));
+#elif GENIE_LDG_MODE == 2
+    return __ldcg(reinterpret_cast<const uint4*>(p));
+#else
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
     return v;
+#endif
 }
 
 template <typename T>

@@ -11,7 +11,7 @@ namespace genie {
 #define GENIE_SCAN_THREADS 512
 #endif
 #ifndef GENIE_SCAN_UNROLL
-#define GENIE_SCAN_UNROLL 4
+#define GENIE_SCAN_UNROLL 2
 #endif
 constexpr uint32_t kScanThreads = GENIE_SCAN_THREADS;  // threads per scan CTA
 constexpr uint32_t kSpanBatch = 256;          // spans staged in shared memory per pass (x2 buffers)
