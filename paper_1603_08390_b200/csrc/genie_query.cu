@@ -739,9 +739,10 @@ template <int W, bool IL>
 __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm) {
     using L = Lay<W, IL>;
     constexpr uint32_t kPer = 32 / W;
-    const int warp = threadIdx.x >> 5;
-    const int nwarps = blockDim.x >> 5;
-    uint32_t* h = reinterpret_cast<uint32_t*>(sm.ht);  // 16 warps x 256 bins
+    const int nsub = static_cast<int>(it.ht_cap * 8 / 1024);  // 256-bin sub-histograms in the table's space
+    const int warp = (threadIdx.x >> 5) % nsub;
+    const int nwarps = nsub;
+    uint32_t* h = reinterpret_cast<uint32_t*>(sm.ht);
     // level 1: high byte of the count (W == 16) or the count itself (W <= 8)
     constexpr uint32_t kShift1 = W == 16 ? 8 : 0;
     uint32_t T = 0, above = 0;
@@ -1153,8 +1154,18 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
     const long long t_setup = clock64();
 #endif
     // warps 1.. scan this item's postings while warp 0 prepares the next item
+#ifdef GENIE_PHASE_TIMERS
+    if (threadIdx.x < 32) {
+        prepare_item(p, sm, b ^ 1u, total);
+        if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_PREP], static_cast<unsigned long long>(clock64() - t_setup));
+    } else {
+        scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1);
+        if (threadIdx.x == 32) atomicAdd(&p.st[ST_T_WARP1], static_cast<unsigned long long>(clock64() - t_setup));
+    }
+#else
     if (threadIdx.x < 32) prepare_item(p, sm, b ^ 1u, total);
     else scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1);
+#endif
     __syncthreads();
     for (uint32_t s0 = kSpanBatch; s0 < S; s0 += kSpanBatch) {  // long queries: further batches
         uint32_t S_;
@@ -1317,15 +1328,41 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         if (lane == 0) d->valid = 0;
         return;
     }
+#ifdef GENIE_PHASE_TIMERS
+    const long long tl0 = clock64();
+    const uint32_t q = *reinterpret_cast<const volatile uint32_t*>(p.work_q + item);
+    if (q == 0x7fffffffu) asm volatile("trap;");  // waits for q
+    const long long tl1 = clock64();
+    if (lane == 0) {
+        atomicAdd(&p.st[ST_T_LAT], static_cast<unsigned long long>(tl1 - tl0));
+        atomicAdd(&p.st[ST_T_LATN], 1ull);
+    }
+    const uint32_t t = p.work_t[item];
+#else
     const uint32_t q = p.work_q[item], t = p.work_t[item];
+#endif
     uint32_t S;
     const StageArgs sa = stage_args(p, q, S);
     const uint32_t W = p.q_W[q];
     const uint32_t kq = p.k[q];
     const uint32_t bound = static_cast<uint32_t>(p.q_bound[q] < 1 ? 1 : p.q_bound[q]);
     const bool gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
+#ifdef GENIE_PHASE_TIMERS
+    const long long tg0 = clock64();
+    const uint32_t a0 = gate ? gate_start(p, q, t, kq, bound) : 0u;
+    if (a0 == 0x7fffffffu) asm volatile("trap;");
+    const long long tg1 = clock64();
+    const uint32_t G = stage_warp(p, sa, sm.sb(buf), t, 0, min(kSpanBatch, S));
+    if (G == 0x7fffffffu) asm volatile("trap;");
+    const long long tg2 = clock64();
+    if (lane == 0) {
+        atomicAdd(&p.st[ST_T_GATE], static_cast<unsigned long long>(tg1 - tg0));
+        atomicAdd(&p.st[ST_T_STAGE], static_cast<unsigned long long>(tg2 - tg1));
+    }
+#else
     const uint32_t a0 = gate ? gate_start(p, q, t, kq, bound) : 0u;
     const uint32_t G = stage_warp(p, sa, sm.sb(buf), t, 0, min(kSpanBatch, S));
+#endif
     if (lane == 0) {
         const uint32_t cap = p.q_cap[q];
         d->q = q;
@@ -1863,8 +1900,27 @@ static void grow_from_status(genie_index* ix) {
     }
 }
 
+// Default tile: the largest counter tile with which two scan CTAs share an SM
+// (B200: 2 x 113 KB of shared memory -> ~92 KB of counters, 188K objects at
+// W = 4): fewer, larger (query, tile) items amortise the per-item work.
+static uint32_t auto_tile_bytes() {
+    static thread_local int dev_cached = -1;
+    static thread_local uint32_t tb_cached = 0;
+    int dev = 0;
+    GENIE_CUDA(cudaGetDevice(&dev));
+    if (dev != dev_cached) {
+        int smem_sm = 0, reserved = 0;
+        GENIE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+        GENIE_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+        const int per_cta = smem_sm / 2 - reserved - static_cast<int>(smem_off::kHt) - static_cast<int>(kHtSlots * 8);
+        tb_cached = per_cta > 4096 ? static_cast<uint32_t>(per_cta) : 4096u;
+        dev_cached = dev;
+    }
+    return tb_cached;
+}
+
 static uint32_t tile_bits_of(const genie_config& cfg) {
-    uint32_t tb = cfg.tile_bytes ? cfg.tile_bytes : kDefaultTileBytes;
+    uint32_t tb = cfg.tile_bytes ? cfg.tile_bytes : auto_tile_bytes();
     tb = std::max<uint32_t>(4096, std::min<uint32_t>(tb, 160u << 10));
     tb &= ~63u;  // tiles of whole 32-object blocks in 16-byte bitmap steps for every W
     return tb * 8;
@@ -2004,7 +2060,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         k_cut<<<sms * 8, 256, 0, s>>>(p);
         ++launches;
         if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
-        p.ht_slots = tile_bytes > (64u << 10) ? kHtMaxSlots : kHtMaxSlots / 2;
+        p.ht_slots = kHtSlots;
         const size_t smem = scan_smem_bytes(tile_bytes, p.ht_slots);
         static thread_local size_t configured = 0;
         if (configured < smem) {

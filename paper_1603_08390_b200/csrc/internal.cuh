@@ -15,12 +15,11 @@ namespace genie {
 #endif
 constexpr uint32_t kScanThreads = GENIE_SCAN_THREADS;  // threads per scan CTA
 constexpr uint32_t kSpanBatch = 256;          // spans staged in shared memory per pass (x2 buffers)
-constexpr uint32_t kHtMaxSlots = 4096;        // shared-memory Robin Hood table (32 KB)
+constexpr uint32_t kHtSlots = 1024;           // shared-memory Robin Hood table (8 KB; >= 4 x 256-bin histograms)
 constexpr uint32_t kHistBins = 256;           // emitted-count histogram of a gated tile (counts <= 255)
 constexpr int kRecLevels = 8;                 // levels in a tile's record (gate_start)
 constexpr uint32_t kRecWords = 12;            // record: base level + kRecLevels counts, padded to 16 B
 constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shared memory (W <= 8)
-constexpr uint32_t kDefaultTileBytes = 64u << 10;
 constexpr uint32_t kMergeThreads = 512;
 constexpr uint32_t kSortCap = 8192;           // merge entries sorted in shared memory
 constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit (guided scheduling)
@@ -54,6 +53,12 @@ enum StatusWord : int {
     ST_T_DENSE = 23,
     ST_ADMIT_CALLS = 24,  // GENIE_PHASE_TIMERS builds: c-PQ admit path entries / passes
     ST_ADMIT_PASS = 25,
+    ST_T_PREP = 26,     // warp 0's prepare_item / warp 1's scan share, cycles
+    ST_T_WARP1 = 27,
+    ST_T_LAT = 28,      // latency of one dependent global load in prepare_item (cycles, count)
+    ST_T_LATN = 29,
+    ST_T_GATE = 30,     // prepare_item: gate start / span staging cycles
+    ST_T_STAGE = 31,
     ST_WORDS = 32
 };
 

@@ -28,4 +28,5 @@ for tb in (0, 32768, 131072):
     print(f"tile_bytes={tb or 65536}: items={items} match_ms={r.timings['match_ns']/1e6:.3f} "
           f"setup={100*w[20]/tot:.1f}% dense={100*w[23]/tot:.1f}% scan={100*w[21]/tot:.1f}% extract={100*w[22]/tot:.1f}% "
           f"cycles/item setup={w[20]/items:.0f} dense={w[23]/items:.0f} scan={w[21]/items:.0f} extract={w[22]/items:.0f} "
-          f"admits/item calls={w[24]/items:.0f} pass={w[25]/items:.0f} prep={w[26]/items:.0f} warp1={w[27]/items:.0f}")
+          f"admits/item calls={w[24]/items:.0f} pass={w[25]/items:.0f} prep={w[26]/items:.0f} warp1={w[27]/items:.0f} "
+          f"load_lat={w[28]/max(1, w[29]):.0f} gate={w[30]/items:.0f} stage={w[31]/items:.0f}")
