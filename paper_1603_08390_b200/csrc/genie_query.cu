@@ -382,8 +382,9 @@ __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t ht_slots) {
     s.ehist = reinterpret_cast<uint32_t*>(base + kEhist);
     s.stage = base + kStage;
     static_assert(kStageBytes == kSpanBatch * 20, "stage buffer layout");
-    s.ht = reinterpret_cast<uint64_t*>(base + kHt);
-    s.cnt = reinterpret_cast<uint32_t*>(base + kHt + size_t(ht_slots) * 8);
+    s.cnt = reinterpret_cast<uint32_t*>(base + kHt);
+    s.ht = nullptr;  // per item: right after the item's counters (process_item)
+    (void)ht_slots;
     return s;
 }
 
@@ -1382,10 +1383,11 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
 }
 
 template <int W>
-__device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t b, uint64_t total) {
+__device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t b, uint64_t total) {
 #ifdef GENIE_PHASE_TIMERS
     const long long t_begin = clock64();
 #endif
+    ScanSmem sm = sm0;
     const ItemDesc& d = sm.desc[b];
     ItemCtx it;
     it.q = d.q;
@@ -1399,12 +1401,20 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     it.cap = d.cap;
     it.out_base = d.out_base;
     it.gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
-    // The table always uses the whole reserved shared region (the reference
-    // sizes it bit_ceil(2 k bound), cpq.hpp:137-138, 283; that figure is kept
-    // for MemoryStats): concurrent admissions arrive in bursts of up to one per
-    // thread before AT can move, and a larger table absorbs them without the
-    // exact-histogram fallback.  Results do not depend on the capacity.
-    it.ht_cap = p.ht_slots;
+    // The table takes the shared memory after the item's counters (whole
+    // 16-word steps of dense_init), at least p.ht_slots, at most kHtMaxSlots
+    // slots -- small tiles (one-tile queries over few objects) get a large
+    // table.  The reference sizes it bit_ceil(2 k bound) (cpq.hpp:137-138,
+    // 283; that figure is kept for MemoryStats); concurrent admissions arrive
+    // in bursts of up to one per thread before AT can move, and spare
+    // capacity absorbs them without the exact-histogram fallback.  Results do
+    // not depend on the capacity.
+    {
+        const uint32_t cnt_bytes = ((it.words + 15) & ~15u) * 4;
+        const uint32_t room = (p.tile_bits / 8 + p.ht_slots * 8 - cnt_bytes) / 8;
+        it.ht_cap = min(kHtMaxSlots, 1u << (31 - __clz(room)));
+        sm.ht = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sm.cnt) + cnt_bytes);
+    }
     const uint32_t S = d.S, nd = d.nd, G = d.G;
     const uint32_t nsb = min(kSpanBatch, S);
 
