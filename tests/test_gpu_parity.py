@@ -257,3 +257,22 @@ def test_dense_containers_are_result_invariant(gpu, oracle, density, monkeypatch
             for tb in (0, 4096, 32768):
                 assert_same(ix.query(ds.queries, config(selector=sel, tile_bytes=tb)), want,
                             f"density {density} sel {sel} tile {tb}")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tie_heavy_many_tiles(gpu, oracle, seed, monkeypatch):
+    # Few tokens per dim: long lists, and thousands of objects tied at the
+    # k-th count.  Small tiles give each query dozens of (query, tile) items,
+    # so later tiles start their gate above the lower tiles' counts (ties lose
+    # on id) and the merge prunes below the published floor; every variant
+    # must still equal the oracle bit for bit.
+    ds = synth.random_instance(n=20_000 + 3001 * seed, dims=3, tokens=3 + seed % 3, max_kw=6, queries=32,
+                               max_items=6, max_span=2, max_k=300, seed=100 + seed)
+    want = oracle.index(ds.csr).execute(ds.queries)
+    for density in ("0", "0.05"):
+        monkeypatch.setenv("GENIE_DENSE_MIN_DENSITY", density)
+        ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+        for tb in (4096, 8192, 0):
+            for rep in range(2):  # concurrent tiles finish in a different order each run
+                assert_same(ix.query(ds.queries, config(tile_bytes=tb)), want,
+                            f"seed {seed} density {density} tile {tb} rep {rep}")
