@@ -144,6 +144,7 @@ class Workload:
     points into the batch's items (C3-C5) and is part of every step."""
 
     lsh = None  # engine.Encoder for C3-C5
+    _pinned = None  # e2e host buffers (host_encode)
 
     def __init__(self, args, rank, world, dev, local):
         import torch
@@ -251,16 +252,27 @@ class Workload:
         return 1
 
     def host_encode(self):
-        """e2e: host query points/sets -> tokens through the public API."""
-        from paper_1603_08390_b200 import engine as E
+        """e2e: host query points/sets (pinned) -> tokens (pinned) through the
+        public API; the batch's lo/hi views the token buffer."""
+        if self._pinned is None:
+            import torch
 
+            from paper_1603_08390_b200 import engine as E
+
+            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+            Q = len(self.batch)
+            tok = pin(np.zeros((Q, self.m), np.uint32))
+            sk = E.point_queries(tok, self.k)
+            flat = tok.reshape(-1)
+            src = ((pin(self.ds.query_set_off.astype(np.uint64)), pin(self.ds.query_elems.astype(np.uint64)))
+                   if self.name == "minhash" else (pin(self.ds.query_points),))
+            self._pinned = (tok, src, E.QueryBatch(pin(sk.qid), pin(sk.k), pin(sk.item_off), pin(sk.dim), flat, flat))
+        tok, src, batch = self._pinned
         if self.name == "minhash":
-            t = self.lsh.encode_sets(self.ds.query_set_off, self.ds.query_elems)
-            h2d = self.ds.query_set_off.nbytes + self.ds.query_elems.nbytes
+            self.lsh.encode_sets(src[0], src[1], out=tok)
         else:
-            t = self.lsh.encode(self.ds.query_points)
-            h2d = self.ds.query_points.nbytes
-        return E.point_queries(t, self.k), h2d, t.nbytes
+            self.lsh.encode(src[0], out=tok)
+        return batch, sum(a.nbytes for a in src), tok.nbytes
 
     def cpu_csr(self):
         if self.m is None:
@@ -437,6 +449,9 @@ def main_genie(args):
             dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     st = ix.status()
+    if os.environ.get("GENIE_PHASE_REPORT"):  # instrumented library (tools/phase_timers.py)
+        from tools.phase_timers import report
+        print(report(ix, int(stats["work_items"])), file=sys.stderr)
     total_ms = float(np.sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], device=dev)

@@ -67,14 +67,26 @@ __global__ void k_build_bitmap(const uint32_t* post, uint64_t b, uint64_t e, uin
     }
 }
 
-static double dense_density() {
+// Lists covering at least 1/64 of the objects carry a bitmap (at most twice
+// their posting bytes).  Whether a query uses it depends on its counter width
+// (k_cut): W = 4 from density 1/32, W >= 8 from 1/64 -- measured break-even of
+// the bitmap adds (bit-sliced past 2W lists) against one shared atomic per
+// posting.  GENIE_DENSE_MIN_DENSITY=<d> overrides both with one fixed
+// threshold (0 disables the containers).
+static double dense_density(genie_index* ix) {
     const char* v = std::getenv("GENIE_DENSE_MIN_DENSITY");
-    if (!v || !*v) return 0.125;  // break-even with the posting scan is ~1/6 - 1/10
+    if (!v || !*v) {
+        ix->dense_inv[0] = 32;
+        ix->dense_inv[1] = 64;
+        ix->dense_inv[2] = 64;
+        return 1.0 / 64;
+    }
+    ix->dense_inv[0] = ix->dense_inv[1] = ix->dense_inv[2] = 0;
     return std::atof(v);
 }
 
 void build_dense_containers(genie_index* ix, const uint64_t* h_off) {
-    const double dens = dense_density();
+    const double dens = dense_density(ix);
     std::vector<int32_t> slot(ix->K, -1);
     std::vector<uint64_t> dense_keys;
     if (dens > 0.0 && ix->n >= 1024) {

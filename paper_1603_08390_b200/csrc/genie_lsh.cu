@@ -28,6 +28,10 @@ struct genie_encoder {
     genie_lsh_config cfg{};
     genie::DevBuf<double> a, b, inv;       // p-stable: a[m*dims], b[m]; RBH: pitch, shift, 1/pitch
     genie::DevBuf<unsigned long long> hash_seed, rehash_seed;
+    // host-API staging, grown on demand and kept (no allocation per call)
+    genie::DevBuf<float> ws_points;
+    genie::DevBuf<uint32_t> ws_tokens;
+    genie::DevBuf<uint64_t> ws_off, ws_elems;
     cudaStream_t stream = nullptr;
 };
 
@@ -420,8 +424,8 @@ int genie_lsh_encode(genie_encoder* enc, const float* points, uint64_t n, uint32
     return guarded(err, errlen, [&]() -> int {
         ensure_device(enc->device);
         const genie_lsh_config& c = enc->cfg;
-        DevBuf<float> dp;
-        DevBuf<uint32_t> dt;
+        DevBuf<float>& dp = enc->ws_points;
+        DevBuf<uint32_t>& dt = enc->ws_tokens;
         dp.reserve(n * c.dims);
         dt.reserve(n * c.m);
         if (n) GENIE_CUDA(cudaMemcpyAsync(dp.p, points, n * c.dims * sizeof(float), cudaMemcpyHostToDevice, enc->stream));
@@ -460,13 +464,14 @@ int genie_minhash_encode(genie_encoder* enc, const uint64_t* set_off, const uint
         const uint64_t ne = set_off[n_sets] - set_off[0];
         std::vector<uint64_t> off(set_off, set_off + n_sets + 1);
         for (auto& o : off) o -= set_off[0];
-        DevBuf<uint64_t> doff, del;
-        DevBuf<uint32_t> dt;
+        DevBuf<uint64_t>& doff = enc->ws_off;
+        DevBuf<uint64_t>& del = enc->ws_elems;
+        DevBuf<uint32_t>& dt = enc->ws_tokens;
         doff.reserve(n_sets + 1);
         del.reserve(ne);
         dt.reserve(n_sets * c.m);
-        GENIE_CUDA(cudaMemcpy(doff.p, off.data(), (n_sets + 1) * 8, cudaMemcpyHostToDevice));
-        if (ne) GENIE_CUDA(cudaMemcpy(del.p, elems + set_off[0], ne * 8, cudaMemcpyHostToDevice));
+        GENIE_CUDA(cudaMemcpyAsync(doff.p, off.data(), (n_sets + 1) * 8, cudaMemcpyHostToDevice, enc->stream));
+        if (ne) GENIE_CUDA(cudaMemcpyAsync(del.p, elems + set_off[0], ne * 8, cudaMemcpyHostToDevice, enc->stream));
         char e2[256];
         const int rc = genie_minhash_encode_device(enc, doff.p, del.p, n_sets, dt.p, enc->stream, e2, sizeof(e2));
         if (rc) throw Error(rc, e2);

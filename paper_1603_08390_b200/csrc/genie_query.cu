@@ -48,6 +48,7 @@ struct BatchParams {
     const int32_t* key_dense;  // [K] dense-container slot or -1
     const uint32_t* bitmaps;   // [n_dense][bitmap_words]
     uint32_t bitmap_words, n_dense;
+    uint32_t dense_inv[3];  // per width class W = 4, 8, 16: use a bitmap iff len * inv >= n (0: always)
     uint64_t K;
     uint32_t n;
     uint32_t id_offset;
@@ -69,7 +70,7 @@ struct BatchParams {
     uint32_t ht_slots;
     uint32_t *it_kb, *it_nk, *it_sbase;
     uint64_t* span_beg;
-    uint32_t* span_key;
+    int32_t* span_dense;  // [spans] bitmap slot used for the span's list, or -1
     uint32_t* cuts;
     uint32_t *work_q, *work_t;
     uint32_t* tile_len;
@@ -283,8 +284,14 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
         const uint32_t len = static_cast<uint32_t>(p.key_off[j + 1] - beg);
         if (lane == 0) {
             p.span_beg[g] = beg;
-            p.span_key[g] = static_cast<uint32_t>(j);
-            if (p.n_dense && p.key_dense[j] >= 0) atomicAdd(&p.q_nd[q], 1u);  // dense spans per query
+            // the list's bitmap replaces its posting scan when the list is dense
+            // enough for this query's counter width (bit-sliced / lane-wise
+            // adds per 32 objects vs. an atomic per posting)
+            int32_t ds = p.n_dense ? p.key_dense[j] : -1;
+            const uint32_t inv = p.dense_inv[wclass(p.q_W[q])];
+            if (ds >= 0 && inv && uint64_t(len) * inv < p.n) ds = -1;
+            p.span_dense[g] = ds;
+            if (ds >= 0) atomicAdd(&p.q_nd[q], 1u);  // dense spans per query
         }
         const uint32_t nt = p.q_ntiles[q];
         const uint32_t T = p.tile_bits / p.q_W[q];
@@ -845,11 +852,35 @@ __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const S
     return T;
 }
 
+// Carry-save adder: l = a ^ b ^ c (sum), h = majority (carry); two LOP3s.
+__device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
+    const uint32_t u = a ^ b;
+    h = (a & b) | (u & c);
+    l = u ^ c;
+}
+
+// Counter-level counts of one thread's counter words (for the c-PQ catch-up).
+template <int W, int NW>
+__device__ __forceinline__ void count_levels(const uint32_t (&acc)[NW], uint32_t at0, uint32_t nlv,
+                                             uint32_t (&lv)[kLvl]) {
+#pragma unroll
+    for (uint32_t l = 0; l < kLvl; ++l) {
+        if (l < nlv) {
+#pragma unroll
+            for (int j = 0; j < NW; ++j) lv[l] += __popc(Swar<W>::ge(acc[j], at0 + l));
+        }
+    }
+}
+
 // Dense phase (interleaved layout): every thread owns whole 32-object blocks
 // and initialises their counters as the sum of the query's dense bitmaps
-// (plain 16-byte stores, no atomics, no zeroing pass).  With the gate on it
-// also counts, in registers, the objects reaching each level
-// v in [at0, at0 + 8) (Swar::ge + popc), for the c-PQ catch-up below.
+// (plain 16-byte stores, no atomics, no zeroing pass).  Few lists: each adds
+// its bits lane by lane (W shift-and-mask-adds per 32 objects).  Many lists
+// (nd >= 2W): bit-sliced counting -- a Harley-Seal tree of carry-save adders
+// folds 8 bitmaps at a time into bit planes of the count (about 3 logic ops
+// per list per 32 objects), transposed into counters once per block.  With
+// the gate on it also counts, in registers, the objects reaching each level
+// v in [at0, at0 + kLvl) (Swar::ge + popc), for the c-PQ catch-up below.
 template <int W>
 __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb, uint32_t nd,
                            uint32_t at0, uint32_t nlv) {
@@ -859,7 +890,61 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
     const uint32_t bw0 = it.tile_lo >> 5;
     const uint32_t nblk = it.words / W;
     uint32_t lv[kLvl] = {0, 0, 0, 0};
-    for (uint32_t b0 = threadIdx.x * BPT; b0 < nblk; b0 += blockDim.x * BPT) {
+    if constexpr (W <= 8) {
+        if (nd >= 2 * W) {
+            for (uint32_t blk = threadIdx.x; blk < nblk; blk += blockDim.x) {
+                const uint32_t* col = p.bitmaps + bw0 + blk;
+                uint32_t P[W];  // bit planes of the dense count (< 2^W: it is at most the bound)
+#pragma unroll
+                for (int i = 0; i < W; ++i) P[i] = 0;
+                uint32_t d = 0;
+                for (; d + 8 <= nd; d += 8) {
+                    uint32_t a[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a[u] = __ldg(col + size_t(sb.dense()[d + u]) * p.bitmap_words);
+                    uint32_t twosA, twosB, foursA, foursB, eights;
+                    csa(twosA, P[0], P[0], a[0], a[1]);
+                    csa(twosB, P[0], P[0], a[2], a[3]);
+                    csa(foursA, P[1], P[1], twosA, twosB);
+                    csa(twosA, P[0], P[0], a[4], a[5]);
+                    csa(twosB, P[0], P[0], a[6], a[7]);
+                    csa(foursB, P[1], P[1], twosA, twosB);
+                    csa(eights, P[2], P[2], foursA, foursB);
+                    uint32_t c = eights;  // weight 8: ripple into the planes above
+#pragma unroll
+                    for (int i = 3; i < W; ++i) {
+                        const uint32_t t = P[i] & c;
+                        P[i] ^= c;
+                        c = t;
+                    }
+                }
+                for (; d < nd; ++d) {
+                    uint32_t c = __ldg(col + size_t(sb.dense()[d]) * p.bitmap_words);
+#pragma unroll
+                    for (int i = 0; i < W; ++i) {
+                        const uint32_t t = P[i] & c;
+                        P[i] ^= c;
+                        c = t;
+                    }
+                }
+                // planes -> interleaved counters: word m, lane l holds object l * W + m
+                uint32_t acc[W];
+#pragma unroll
+                for (int m = 0; m < W; ++m) {
+                    uint32_t x = 0;
+#pragma unroll
+                    for (int i = 0; i < W; ++i) x |= ((P[i] >> m) & Sw::kOnes) << i;
+                    acc[m] = x;
+                }
+                uint4* dst = reinterpret_cast<uint4*>(sm.cnt + blk * W);
+#pragma unroll
+                for (int j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                if (nlv) count_levels<W, W>(acc, at0, nlv, lv);
+            }
+            nd = 0;  // done: skip the lane-wise path
+        }
+    }
+    for (uint32_t b0 = threadIdx.x * BPT; nd && b0 < nblk; b0 += blockDim.x * BPT) {
         uint32_t acc[NW];
 #pragma unroll
         for (uint32_t j = 0; j < NW; ++j) acc[j] = 0;
@@ -907,15 +992,7 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
         uint4* dst = reinterpret_cast<uint4*>(sm.cnt + b0 * W);
 #pragma unroll
         for (uint32_t j = 0; j < NW; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-        if (nlv) {
-#pragma unroll
-            for (uint32_t l = 0; l < kLvl; ++l) {
-                if (l < nlv) {
-#pragma unroll
-                    for (uint32_t j = 0; j < NW; ++j) lv[l] += __popc(Sw::ge(acc[j], at0 + l));
-                }
-            }
-        }
+        if (nlv) count_levels<W, NW>(acc, at0, nlv, lv);
     }
     // (the blocks of a tile come in whole thread steps: tiles are multiples
     // of 32 * BPT objects and bitmap rows are padded to 16 bytes)
@@ -1067,7 +1144,7 @@ __device__ __forceinline__ void stage_one(const BatchParams& p, const StageArgs&
         beg = p.span_beg[a.sbq + s] + c[0];
         len = c[1] - c[0];
         if (a.dense) {
-            dslot = p.key_dense[p.span_key[a.sbq + s]];
+            dslot = p.span_dense[a.sbq + s];
             if (dslot >= 0) len = 0;  // the list's bitmap covers this tile: no posting scan
         }
     }
@@ -1461,7 +1538,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
     }
 }
 
-__global__ void __launch_bounds__(kScanThreads, 1024 / kScanThreads)
+__global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     k_scan(BatchParams p, uint32_t tile_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
     (void)tile_bytes;
@@ -1864,7 +1941,7 @@ static void reserve_workspace(genie_index* ix, uint32_t Q, uint32_t items, uint3
                            4096);
     if (want_spans > w.cap_spans) {
         w.span_beg.reserve(want_spans);
-        w.span_key.reserve(want_spans);
+        w.span_dense.reserve(want_spans);
         w.cap_spans = want_spans;
     }
     if (want_cuts > w.cap_cuts) {
@@ -1891,7 +1968,7 @@ static void grow_from_status(genie_index* ix) {
     if (h[ST_TOTAL_SPANS] > w.cap_spans) {
         w.cap_spans = h[ST_TOTAL_SPANS] + (h[ST_TOTAL_SPANS] >> 2);
         w.span_beg.reserve(w.cap_spans);
-        w.span_key.reserve(w.cap_spans);
+        w.span_dense.reserve(w.cap_spans);
     }
     if (h[ST_TOTAL_CUTS] > w.cap_cuts) {
         w.cap_cuts = h[ST_TOTAL_CUTS] + (h[ST_TOTAL_CUTS] >> 2);
@@ -1922,7 +1999,7 @@ static uint32_t auto_tile_bytes() {
         int smem_sm = 0, reserved = 0;
         GENIE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
         GENIE_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev));
-        const int per_cta = smem_sm / 2 - reserved - static_cast<int>(smem_off::kHt) - static_cast<int>(kHtSlots * 8);
+        const int per_cta = smem_sm / static_cast<int>(kScanCtasPerSm) - reserved - static_cast<int>(smem_off::kHt) - static_cast<int>(kHtSlots * 8);
         tb_cached = per_cta > 4096 ? static_cast<uint32_t>(per_cta) : 4096u;
         dev_cached = dev;
     }
@@ -2038,11 +2115,12 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.it_nk = w.it_nk.p;
     p.it_sbase = w.it_sbase.p;
     p.span_beg = w.span_beg.p;
-    p.span_key = w.span_key.p;
+    p.span_dense = w.span_dense.p;
     p.key_dense = ix->key_dense.p;
     p.bitmaps = ix->bitmaps.p;
     p.bitmap_words = ix->bitmap_words;
     p.n_dense = ix->n_dense;
+    for (int c = 0; c < 3; ++c) p.dense_inv[c] = ix->dense_inv[c];
     p.cuts = w.cuts.p;
     p.work_q = w.work_q.p;
     p.work_t = w.work_t.p;

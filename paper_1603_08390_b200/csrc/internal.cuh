@@ -13,7 +13,11 @@ namespace genie {
 #ifndef GENIE_SCAN_UNROLL
 #define GENIE_SCAN_UNROLL 2
 #endif
+#ifndef GENIE_SCAN_CTAS
+#define GENIE_SCAN_CTAS (1024 / GENIE_SCAN_THREADS)
+#endif
 constexpr uint32_t kScanThreads = GENIE_SCAN_THREADS;  // threads per scan CTA
+constexpr uint32_t kScanCtasPerSm = GENIE_SCAN_CTAS;   // resident scan CTAs per SM (registers, tile size)
 constexpr uint32_t kSpanBatch = 256;          // spans staged in shared memory per pass (x2 buffers)
 constexpr uint32_t kHtSlots = 1024;           // shared-memory Robin Hood table, minimum (8 KB; >= 4 x 256-bin histograms)
 constexpr uint32_t kHtMaxSlots = 4096;        // ... and maximum (items whose counters leave room)
@@ -72,7 +76,7 @@ struct Workspace {
     DevBuf<uint32_t> it_kb, it_nk, it_sbase;
     // spans / cuts / work / tiles
     DevBuf<uint64_t> span_beg;
-    DevBuf<uint32_t> span_key;
+    DevBuf<int32_t> span_dense;
     DevBuf<uint32_t> cuts;
     DevBuf<uint32_t> work_q, work_t;
     DevBuf<uint32_t> tile_len;
@@ -111,6 +115,7 @@ struct genie_index {
     genie::DevBuf<int32_t> key_dense;   // [K] slot in `bitmaps` or -1
     genie::DevBuf<uint32_t> bitmaps;    // [n_dense][bitmap_words]
     uint32_t n_dense = 0, bitmap_words = 0;
+    uint32_t dense_inv[3] = {0, 0, 0};  // query-time density rule per counter width (W = 4, 8, 16)
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
     genie::Workspace ws;

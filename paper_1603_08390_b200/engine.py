@@ -417,10 +417,12 @@ class Encoder:
         except Exception:
             pass
 
-    def encode(self, points: np.ndarray) -> np.ndarray:
+    def encode(self, points: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
         pts = np.ascontiguousarray(points, dtype=np.float32)
         n = pts.shape[0]
-        out = np.zeros((n, self.cfg.m), np.uint32)
+        if out is None:
+            out = np.zeros((n, self.cfg.m), np.uint32)
+        assert out.shape == (n, self.cfg.m) and out.dtype == np.uint32 and out.flags.c_contiguous
         err = _errbuf()
         check(self._lib.genie_lsh_encode(self._h, _ptr(pts, C.c_float), n, _ptr(out, C.c_uint32), err, len(err)),
               err)
@@ -432,11 +434,13 @@ class Encoder:
                                                 C.c_void_p(d_tokens.data_ptr()), C.c_void_p(stream or 0), err,
                                                 len(err)), err)
 
-    def encode_sets(self, set_off: np.ndarray, elems: np.ndarray) -> np.ndarray:
+    def encode_sets(self, set_off: np.ndarray, elems: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
         off = np.ascontiguousarray(set_off, np.uint64)
         el = np.ascontiguousarray(elems, np.uint64)
         n = off.shape[0] - 1
-        out = np.zeros((n, self.cfg.m), np.uint32)
+        if out is None:
+            out = np.zeros((n, self.cfg.m), np.uint32)
+        assert out.shape == (n, self.cfg.m) and out.dtype == np.uint32 and out.flags.c_contiguous
         err = _errbuf()
         check(self._lib.genie_minhash_encode(self._h, _ptr(off, C.c_uint64), _ptr(el, C.c_uint64), n,
                                              _ptr(out, C.c_uint32), err, len(err)), err)
