@@ -363,7 +363,9 @@ enum ScalarSlot {
     SC_BASE = 23,       // base level of the tile's record
     SC_ADM_CALLS = 24,  // instrumented builds only
     SC_ADM_PASS = 25,
-    SC_WORDS = 26
+    SC_WMAX = 26,       // instrumented builds: slowest / fastest scan warp of the item
+    SC_WMIN = 27,
+    SC_WORDS = 28
 };
 static_assert(SC_WORDS <= 32, "scalar area");
 
@@ -859,19 +861,6 @@ __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32
     l = u ^ c;
 }
 
-// Counter-level counts of one thread's counter words (for the c-PQ catch-up).
-template <int W, int NW>
-__device__ __forceinline__ void count_levels(const uint32_t (&acc)[NW], uint32_t at0, uint32_t nlv,
-                                             uint32_t (&lv)[kLvl]) {
-#pragma unroll
-    for (uint32_t l = 0; l < kLvl; ++l) {
-        if (l < nlv) {
-#pragma unroll
-            for (int j = 0; j < NW; ++j) lv[l] += __popc(Swar<W>::ge(acc[j], at0 + l));
-        }
-    }
-}
-
 // Dense phase (interleaved layout): every thread owns whole 32-object blocks
 // and initialises their counters as the sum of the query's dense bitmaps
 // (plain 16-byte stores, no atomics, no zeroing pass).  Few lists: each adds
@@ -927,6 +916,25 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
                         c = t;
                     }
                 }
+                if (nlv) {  // objects of the block counting >= v: comparator on the planes
+#pragma unroll
+                    for (uint32_t l = 0; l < kLvl; ++l) {
+                        if (l < nlv) {
+                            const uint32_t v = at0 + l;
+                            uint32_t ge = 0, eq = 0xffffffffu;
+#pragma unroll
+                            for (int i = W - 1; i >= 0; --i) {
+                                if ((v >> i) & 1u) {
+                                    eq &= P[i];
+                                } else {
+                                    ge |= eq & P[i];
+                                    eq &= ~P[i];
+                                }
+                            }
+                            lv[l] += __popc(ge | eq);
+                        }
+                    }
+                }
                 // planes -> interleaved counters: word m, lane l holds object l * W + m
                 uint32_t acc[W];
 #pragma unroll
@@ -939,7 +947,6 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
                 uint4* dst = reinterpret_cast<uint4*>(sm.cnt + blk * W);
 #pragma unroll
                 for (int j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-                if (nlv) count_levels<W, W>(acc, at0, nlv, lv);
             }
             nd = 0;  // done: skip the lane-wise path
         }
@@ -992,7 +999,16 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
         uint4* dst = reinterpret_cast<uint4*>(sm.cnt + b0 * W);
 #pragma unroll
         for (uint32_t j = 0; j < NW; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-        if (nlv) count_levels<W, NW>(acc, at0, nlv, lv);
+        if (nlv) {  // counts <= nd < 2W < 2^(W-1): one add and one mask per level
+#pragma unroll
+            for (uint32_t l = 0; l < kLvl; ++l) {
+                if (l < nlv) {
+                    const uint32_t bias = Sw::kHigh - (at0 + l) * Sw::kOnes;
+#pragma unroll
+                    for (uint32_t j = 0; j < NW; ++j) lv[l] += __popc((acc[j] + bias) & Sw::kHigh);
+                }
+            }
+        }
     }
     // (the blocks of a tile come in whole thread steps: tiles are multiples
     // of 32 * BPT objects and bitmap rows are padded to 16 bytes)
@@ -1238,7 +1254,12 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
         if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_PREP], static_cast<unsigned long long>(clock64() - t_setup));
     } else {
         scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1);
-        if (threadIdx.x == 32) atomicAdd(&p.st[ST_T_WARP1], static_cast<unsigned long long>(clock64() - t_setup));
+        const uint32_t dt = static_cast<uint32_t>(clock64() - t_setup);
+        if (threadIdx.x == 32) atomicAdd(&p.st[ST_T_WARP1], static_cast<unsigned long long>(dt));
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(&sm.scal[SC_WMAX], dt);
+            atomicMin(&sm.scal[SC_WMIN], dt);
+        }
     }
 #else
     if (threadIdx.x < 32) prepare_item(p, sm, b ^ 1u, total);
@@ -1255,6 +1276,12 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
     }
 #ifdef GENIE_PHASE_TIMERS
     const long long t_scanned = clock64();
+    if (threadIdx.x == 0) {
+        atomicAdd(&p.st[ST_T_WMAX], static_cast<unsigned long long>(sm.scal[SC_WMAX]));
+        atomicAdd(&p.st[ST_T_WMIN], static_cast<unsigned long long>(sm.scal[SC_WMIN]));
+        sm.scal[SC_WMAX] = 0;
+        sm.scal[SC_WMIN] = 0xffffffffu;
+    }
 #endif
     // ---- select: the tile's exact top-k
     if (it.gate && !sm.scal[SC_OVF]) {
@@ -1552,6 +1579,8 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     if (threadIdx.x == 0) {
         sm.scal[SC_ADM_CALLS] = 0;
         sm.scal[SC_ADM_PASS] = 0;
+        sm.scal[SC_WMAX] = 0;
+        sm.scal[SC_WMIN] = 0xffffffffu;
     }
     __syncthreads();
     for (uint32_t iter = 0;; ++iter) {
