@@ -871,16 +871,18 @@ __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32
 // the gate on it also counts, in registers, the objects reaching each level
 // v in [at0, at0 + kLvl) (Swar::ge + popc), for the c-PQ catch-up below.
 template <int W>
-__device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb, uint32_t nd,
-                           uint32_t at0, uint32_t nlv) {
+__device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb,
+                               uint32_t nd, uint32_t at0, uint32_t nlv, bool& csa_path) {
     using Sw = Swar<W>;
     constexpr uint32_t BPT = W == 4 ? 4 : (W == 8 ? 2 : 1);  // blocks per thread step (16 words)
     constexpr uint32_t NW = BPT * W;
     const uint32_t bw0 = it.tile_lo >> 5;
     const uint32_t nblk = it.words / W;
     uint32_t lv[kLvl] = {0, 0, 0, 0};
+    csa_path = false;
     if constexpr (W <= 8) {
         if (nd >= 2 * W) {
+            csa_path = true;
             for (uint32_t blk = threadIdx.x; blk < nblk; blk += blockDim.x) {
                 const uint32_t* col = p.bitmaps + bw0 + blk;
                 uint32_t P[W];  // bit planes of the dense count (< 2^W: it is at most the bound)
@@ -951,26 +953,24 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
             nd = 0;  // done: skip the lane-wise path
         }
     }
-    for (uint32_t b0 = threadIdx.x * BPT; nd && b0 < nblk; b0 += blockDim.x * BPT) {
+    // Lane-wise path: a warp step covers 32 * BPT consecutive blocks; lane l
+    // owns blocks base + 32 j (j < BPT), so every bitmap load (one word per
+    // lane) and every 16-byte counter store of the warp is contiguous.
+    const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (uint32_t wt = threadIdx.x >> 5; nd && wt * 32 * BPT < nblk; wt += nwarps) {
+        const uint32_t base = wt * 32 * BPT + lane;
         uint32_t acc[NW];
 #pragma unroll
         for (uint32_t j = 0; j < NW; ++j) acc[j] = 0;
-        const uint32_t* col = p.bitmaps + bw0 + b0;
+        const uint32_t* col = p.bitmaps + bw0 + base;
         uint32_t d = 0;
         for (; d + 4 <= nd; d += 4) {  // four lists' loads in flight
             uint32_t b[4][BPT];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t* src = col + size_t(sb.dense()[d + u]) * p.bitmap_words;
-                if constexpr (BPT == 4) {
-                    const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
-                    b[u][0] = x.x, b[u][1] = x.y, b[u][2] = x.z, b[u][3] = x.w;
-                } else if constexpr (BPT == 2) {
-                    const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
-                    b[u][0] = x.x, b[u][1] = x.y;
-                } else {
-                    b[u][0] = __ldg(src);
-                }
+#pragma unroll
+                for (uint32_t i = 0; i < BPT; ++i) b[u][i] = base + 32 * i < nblk ? __ldg(src + 32 * i) : 0u;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -982,23 +982,22 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
         for (; d < nd; ++d) {
             const uint32_t* src = col + size_t(sb.dense()[d]) * p.bitmap_words;
             uint32_t b[BPT];
-            if constexpr (BPT == 4) {
-                const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
-                b[0] = x.x, b[1] = x.y, b[2] = x.z, b[3] = x.w;
-            } else if constexpr (BPT == 2) {
-                const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
-                b[0] = x.x, b[1] = x.y;
-            } else {
-                b[0] = __ldg(src);
-            }
+#pragma unroll
+            for (uint32_t i = 0; i < BPT; ++i) b[i] = base + 32 * i < nblk ? __ldg(src + 32 * i) : 0u;
 #pragma unroll
             for (uint32_t i = 0; i < BPT; ++i)
 #pragma unroll
                 for (uint32_t m = 0; m < W; ++m) acc[i * W + m] += (b[i] >> m) & Sw::kOnes;
         }
-        uint4* dst = reinterpret_cast<uint4*>(sm.cnt + b0 * W);
 #pragma unroll
-        for (uint32_t j = 0; j < NW; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        for (uint32_t i = 0; i < BPT; ++i) {
+            if (base + 32 * i < nblk) {
+                uint4* dst = reinterpret_cast<uint4*>(sm.cnt + (base + 32 * i) * W);
+#pragma unroll
+                for (uint32_t j = 0; j < W; j += 4)
+                    dst[j / 4] = make_uint4(acc[i * W + j], acc[i * W + j + 1], acc[i * W + j + 2], acc[i * W + j + 3]);
+            }
+        }
         if (nlv) {  // counts <= nd < 2W < 2^(W-1): one add and one mask per level
 #pragma unroll
             for (uint32_t l = 0; l < kLvl; ++l) {
@@ -1010,8 +1009,9 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
             }
         }
     }
-    // (the blocks of a tile come in whole thread steps: tiles are multiples
-    // of 32 * BPT objects and bitmap rows are padded to 16 bytes)
+    uint32_t reach = 0;  // levels at0 + l (l < reach) that some object of this thread's blocks reaches
+#pragma unroll
+    for (uint32_t l = 0; l < kLvl; ++l) reach += (l < nlv && lv[l]) ? 1u : 0u;
     if (nlv) {
 #pragma unroll
         for (uint32_t l = 0; l < kLvl; ++l) {
@@ -1022,6 +1022,7 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
         }
     }
     __syncthreads();
+    return reach;
 }
 
 // Brings the c-PQ state to what one gated update per (dense list, member
@@ -1030,8 +1031,8 @@ __device__ void dense_init(const BatchParams& p, const ItemCtx& it, const ScanSm
 // again); every object at or above the new AT -- fewer than k -- enters the
 // table and adds one to ZA[v] for each level v in [AT, count].
 template <int W>
-__device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, uint32_t dmax,
-                           uint32_t nlv) {
+__device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, uint32_t dmax, uint32_t nlv,
+                           uint32_t reach, bool csa_path) {
     using Sw = Swar<W>;
     using L = Lay<W, true>;
     uint32_t j = 0;
@@ -1056,16 +1057,32 @@ __device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, 
         a = lo;
     }
     if (threadIdx.x == 0) sm.scal[SC_AT] = a;
-    if (a <= dmax) {
-        for (uint32_t wi = threadIdx.x; wi < it.words; wi += blockDim.x) {
-            const uint32_t x = sm.cnt[wi];
-            uint32_t m = Sw::ge(x, a);
-            while (m) {
-                const uint32_t l = (__ffs(m) - 1) / W;
-                m &= m - 1;
-                const uint32_t c = (x >> (l * W)) & L::kMask;
-                if (!ht_insert(sm.ht, it.ht_cap, L::obj(wi, l), c, a)) sm.scal[SC_OVF] = 1;
-                for (uint32_t v = a; v <= c; ++v) atomicAdd(&sm.za[v], 1u);
+    // A thread re-reads only its own dense_init blocks, and only when they
+    // may hold an object at or above a (its level counts say so, or do not
+    // reach that high): the fewer than k objects sit in a few blocks.
+    if (a <= dmax && (a - at0 < reach || reach == nlv)) {
+        constexpr uint32_t BPT = W == 4 ? 4 : (W == 8 ? 2 : 1);
+        const uint32_t nblk = it.words / W;
+        // blocks of this thread: csa path blk = tid + k * blockDim; lane-wise
+        // path blk = (warp + k * nwarps) * 32 * BPT + lane + 32 i
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t first = csa_path ? threadIdx.x : (threadIdx.x >> 5) * 32 * BPT + lane;
+        const uint32_t stride = csa_path ? blockDim.x : (blockDim.x >> 5) * 32 * BPT;
+        const uint32_t per = csa_path ? 1u : BPT;
+        for (uint32_t b0 = first; b0 < nblk; b0 += stride) {
+            for (uint32_t i = 0; i < per && b0 + 32 * i < nblk; ++i) {
+                const uint32_t blk = b0 + 32 * i;
+                for (uint32_t wi = blk * W; wi < blk * W + W; ++wi) {
+                    const uint32_t x = sm.cnt[wi];
+                    uint32_t m = Sw::ge(x, a);
+                    while (m) {
+                        const uint32_t l = (__ffs(m) - 1) / W;
+                        m &= m - 1;
+                        const uint32_t c = (x >> (l * W)) & L::kMask;
+                        if (!ht_insert(sm.ht, it.ht_cap, L::obj(wi, l), c, a)) sm.scal[SC_OVF] = 1;
+                        for (uint32_t v = a; v <= c; ++v) atomicAdd(&sm.za[v], 1u);
+                    }
+                }
             }
         }
     }
@@ -1554,10 +1571,14 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
 #ifdef GENIE_PHASE_TIMERS
         const long long t_d = clock64();
 #endif
-        dense_init<W>(p, it, sm, sm.sb(b), nd, at0, nlv);
-        if (it.gate && at0 <= dmax) dense_gate<W>(it, sm, at0, dmax, nlv);
+        bool csa_path;
+        const uint32_t reach = dense_init<W>(p, it, sm, sm.sb(b), nd, at0, nlv, csa_path);
+        if (it.gate && at0 <= dmax) dense_gate<W>(it, sm, at0, dmax, nlv, reach, csa_path);
 #ifdef GENIE_PHASE_TIMERS
-        if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_DENSE], static_cast<unsigned long long>(clock64() - t_d));
+        if (threadIdx.x == 0) {
+            atomicAdd(&p.st[ST_T_DENSE], static_cast<unsigned long long>(clock64() - t_d));
+            atomicAdd(&p.st[ST_DENSE_ND], static_cast<unsigned long long>(nd) | (csa_path ? (1ull << 40) : 0ull));
+        }
 #endif
         scan_and_select<W, true>(p, it, sm, b, S, nsb, G, total);
     } else {
