@@ -878,7 +878,7 @@ __device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const Sc
     constexpr uint32_t NW = BPT * W;
     const uint32_t bw0 = it.tile_lo >> 5;
     const uint32_t nblk = it.words / W;
-    uint32_t lv[kLvl] = {0, 0, 0, 0};
+    uint32_t lv[kLvl] = {};
     csa_path = false;
     if constexpr (W <= 8) {
         if (nd >= 2 * W) {

@@ -28,7 +28,10 @@ constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shar
 constexpr uint32_t kMergeThreads = 512;
 constexpr uint32_t kSortCap = 8192;           // merge entries sorted in shared memory
 constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit (guided scheduling)
-constexpr uint32_t kLvl = 4;                  // dense-phase c-PQ levels counted in registers
+#ifndef GENIE_DENSE_LEVELS
+#define GENIE_DENSE_LEVELS 2
+#endif
+constexpr uint32_t kLvl = GENIE_DENSE_LEVELS;  // dense-phase c-PQ levels counted in registers
 constexpr int kScanUnroll = GENIE_SCAN_UNROLL;               // 128-posting groups loaded per warp pass
 constexpr uint32_t kStaticGroups = 64;        // <= this many 128-posting groups per warp: static split
 constexpr uint64_t kEmptySlot = ~0ull;
