@@ -327,7 +327,8 @@ struct StageBuf {
 struct ItemDesc {
     uint32_t valid, q, t, kq, bound, W, cap, nt, S, nd, G, a0;
     uint64_t out_base;
-    uint32_t pad[2];
+    uint32_t tile_slot;  // q_tile_base[q] + t: the item's tile_len / tile_rec slot
+    uint32_t pad;
 };
 
 // Shared memory of a scan CTA.  Everything but the counters sits at a fixed
@@ -359,6 +360,9 @@ enum ScalarSlot {
     SC_FLOOR = 10,
     SC_NDENSE = 11,
     SC_G = 12,       // groups of the first staged batch
+    SC_PF_ITEM = 13, // next work item claimed ahead by prepare_item, its query and tile
+    SC_PF_Q = 14,
+    SC_PF_T = 15,
     SC_LVL = 16,     // 8 dense-phase level counts
     SC_BASE = 23,       // base level of the tile's record
     SC_ADM_CALLS = 24,  // instrumented builds only
@@ -523,7 +527,7 @@ struct Swar {
 };
 
 struct ItemCtx {
-    uint32_t q, t, kq, bound, tile_lo, tile_n, words, ht_cap, cap;
+    uint32_t q, t, kq, bound, tile_lo, tile_n, words, ht_cap, cap, slot;
     uint64_t out_base;
     bool gate;
 };
@@ -1344,7 +1348,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
         if (threadIdx.x == 0) sm.scal[SC_BASE] = T_t;
     }
     __syncthreads();
-    if (threadIdx.x == 0) p.tile_len[p.q_tile_base[it.q] + it.t] = sm.scal[SC_NOUT];
+    if (threadIdx.x == 0) p.tile_len[it.slot] = sm.scal[SC_NOUT];
     if (it.gate && threadIdx.x < 32) {
         // the tile's record for the later tiles of its query (gate_start):
         // base level b (every emitted entry counts >= b) and n[j] = #emitted
@@ -1354,7 +1358,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
         uint32_t top = 0;  // entries counting >= b + kRecLevels
         for (uint32_t c = b + kRecLevels + lane; c <= it.bound; c += 32) top += sm.ehist[c];
         top = warp_sum(top);
-        uint32_t* rec = p.tile_rec + uint64_t(p.q_tile_base[it.q] + it.t) * kRecWords;
+        uint32_t* rec = p.tile_rec + uint64_t(it.slot) * kRecWords;
         if (lane == 0) {
             uint32_t n = top;
             for (int j = kRecLevels - 1; j >= 0; --j) {
@@ -1394,13 +1398,13 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
 // final counts, and a record read half-written or still zero only
 // under-counts.  Called by one whole warp.  Returns max(F, c_low + 1).
 __device__ __forceinline__ uint32_t gate_start(const BatchParams& p, uint32_t q, uint32_t t, uint32_t kq,
-                                               uint32_t bound) {
+                                               uint32_t bound, uint32_t tbase) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t F = __ldcg(p.q_floor + q);
     uint32_t tot[kRecLevels];  // entries of lower tiles counting >= F + j
 #pragma unroll
     for (int j = 0; j < kRecLevels; ++j) tot[j] = 0;
-    const uint32_t* base = p.tile_rec + uint64_t(p.q_tile_base[q]) * kRecWords;
+    const uint32_t* base = p.tile_rec + uint64_t(tbase) * kRecWords;
     for (uint32_t l = lane; l < t; l += 32) {
         const uint4* r4 = reinterpret_cast<const uint4*>(base + uint64_t(l) * kRecWords);
         uint32_t r[kRecWords];
@@ -1443,48 +1447,30 @@ __device__ __forceinline__ uint32_t fetch_item(const BatchParams& p, uint64_t to
 __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint64_t total) {
     const uint32_t lane = threadIdx.x & 31;
     ItemDesc* d = sm.desc + buf;
-    uint32_t item = 0;
-    if (lane == 0) item = fetch_item(p, total);
-    item = __shfl_sync(0xffffffffu, item, 0);
+    // the item was claimed (and its query / tile read) by the previous call
+    const uint32_t item = sm.scal[SC_PF_ITEM];
     if (item == 0xffffffffu) {
         if (lane == 0) d->valid = 0;
         return;
     }
-#ifdef GENIE_PHASE_TIMERS
-    const long long tl0 = clock64();
-    const uint32_t q = *reinterpret_cast<const volatile uint32_t*>(p.work_q + item);
-    if (q == 0x7fffffffu) asm volatile("trap;");  // waits for q
-    const long long tl1 = clock64();
-    if (lane == 0) {
-        atomicAdd(&p.st[ST_T_LAT], static_cast<unsigned long long>(tl1 - tl0));
-        atomicAdd(&p.st[ST_T_LATN], 1ull);
-    }
-    const uint32_t t = p.work_t[item];
-#else
-    const uint32_t q = p.work_q[item], t = p.work_t[item];
-#endif
+    const uint32_t q = sm.scal[SC_PF_Q], t = sm.scal[SC_PF_T];
+    // claim the one after it now (consumed at the end)
+    uint32_t nitem = 0xffffffffu;
+    if (lane == 0) nitem = fetch_item(p, total);
     uint32_t S;
     const StageArgs sa = stage_args(p, q, S);
     const uint32_t W = p.q_W[q];
     const uint32_t kq = p.k[q];
     const uint32_t bound = static_cast<uint32_t>(p.q_bound[q] < 1 ? 1 : p.q_bound[q]);
+    const uint32_t tbase = p.q_tile_base[q];
     const bool gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
-#ifdef GENIE_PHASE_TIMERS
-    const long long tg0 = clock64();
-    const uint32_t a0 = gate ? gate_start(p, q, t, kq, bound) : 0u;
-    if (a0 == 0x7fffffffu) asm volatile("trap;");
-    const long long tg1 = clock64();
+    const uint32_t a0 = gate ? gate_start(p, q, t, kq, bound, tbase) : 0u;
     const uint32_t G = stage_warp(p, sa, sm.sb(buf), t, 0, min(kSpanBatch, S));
-    if (G == 0x7fffffffu) asm volatile("trap;");
-    const long long tg2 = clock64();
-    if (lane == 0) {
-        atomicAdd(&p.st[ST_T_GATE], static_cast<unsigned long long>(tg1 - tg0));
-        atomicAdd(&p.st[ST_T_STAGE], static_cast<unsigned long long>(tg2 - tg1));
+    uint32_t nq = 0, ntile = 0;
+    if (nitem != 0xffffffffu) {
+        nq = p.work_q[nitem];
+        ntile = p.work_t[nitem];
     }
-#else
-    const uint32_t a0 = gate ? gate_start(p, q, t, kq, bound) : 0u;
-    const uint32_t G = stage_warp(p, sa, sm.sb(buf), t, 0, min(kSpanBatch, S));
-#endif
     if (lane == 0) {
         const uint32_t cap = p.q_cap[q];
         d->q = q;
@@ -1499,7 +1485,11 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         d->G = G;
         d->a0 = a0;
         d->out_base = p.q_out_base[q] + uint64_t(t) * cap;
+        d->tile_slot = tbase + t;
         d->valid = 1;
+        sm.scal[SC_PF_ITEM] = nitem;
+        sm.scal[SC_PF_Q] = nq;
+        sm.scal[SC_PF_T] = ntile;
     }
 }
 
@@ -1520,6 +1510,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
     it.tile_n = min(T, p.n - it.tile_lo);
     it.words = ((it.tile_n + 31) >> 5) * W;  // whole 32-object blocks
     it.cap = d.cap;
+    it.slot = d.tile_slot;
     it.out_base = d.out_base;
     it.gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
     // The table takes the shared memory after the item's counters (whole
@@ -1595,6 +1586,15 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     const uint64_t total = p.st[ST_TOTAL_WORK];
     // item i runs from desc[i & 1]; its scan phase prepares item i + 1 into
     // the other descriptor / stage buffer (prepare_item)
+    if (threadIdx.x == 0) {
+        const uint32_t i0 = fetch_item(p, total);
+        sm.scal[SC_PF_ITEM] = i0;
+        if (i0 != 0xffffffffu) {
+            sm.scal[SC_PF_Q] = p.work_q[i0];
+            sm.scal[SC_PF_T] = p.work_t[i0];
+        }
+    }
+    __syncwarp();
     if (threadIdx.x < 32) prepare_item(p, sm, 0, total);
     for (uint32_t i = threadIdx.x; i < kHistBins; i += blockDim.x) sm.ehist[i] = 0;
     if (threadIdx.x == 0) {
