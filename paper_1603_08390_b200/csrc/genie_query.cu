@@ -573,86 +573,6 @@ __device__ __forceinline__ uint32_t atom_add_shared(uint32_t addr, uint32_t v) {
     return old;
 }
 
-// Count every posting of [ua, ub) (absolute positions) into the tile's
-// shared counters; with the gate on, feed the c-PQ with each new value.
-//
-// Per posting: one shared atomicAdd of 1 << shift on the packed word (exact:
-// the query's max_count_bound keeps every counter below 2^W, so no carry
-// crosses lanes -- the reference's CAS loop, cpq.hpp:70-88, is not needed).
-// Addresses are 32-bit shared-window offsets with the tile origin folded into
-// the base (the tile origin is a multiple of 32 objects, so both layouts map
-// absolute ids linearly across 32-object blocks).  The gate test "old value
-// >= AT - 1" is done on the word shifted so the counter sits in the top W
-// bits, as one max over the four postings of a 16-byte group and one compare.
-template <int W, bool GATE, bool IL>
-__device__ __forceinline__ void scan_range(const uint32_t* __restrict__ postings, uint64_t ua,
-                                           uint64_t ub, const ItemCtx& it, const ScanSmem& sm) {
-    using L = Lay<W, IL>;
-    constexpr uint32_t kPer = 32 / W, kTop = 32 - W;
-    constexpr int UNR = kScanUnroll;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t* base = postings + (ua & ~3ull);
-    const uint32_t lo = static_cast<uint32_t>(ua & 3ull);
-    const uint32_t len = static_cast<uint32_t>(ub - (ua & ~3ull));
-    // byte address of the word holding absolute id x: cbase + word(x) * 4 (mod 2^32)
-    const uint32_t cbase = smem_u32(sm.cnt) - (L::word(it.tile_lo) << 2);
-    volatile uint32_t* s_at = sm.scal + SC_AT;
-    uint32_t gate = 0;
-    if constexpr (GATE) gate = (*s_at - 1) << kTop;
-    for (uint32_t off = lane * 4; off < len; off += 128 * UNR) {
-        uint4 v[UNR];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const uint32_t o = off + u * 128;
-            v[u] = o < len ? ldg_stream_v4(base + o) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const uint32_t o = off + u * 128;
-            const uint32_t x[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-            if (o >= len) continue;  // past the end for this lane
-            uint32_t old[4];
-            uint32_t m = 0xfu;
-            uint32_t top = 0;
-            if (o >= lo && o + 4 <= len) {  // full group: unconditional atomics
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    // r = kTop - shift: the counter's distance from the top of the word
-                    const uint32_t r = ((~L::lane(x[e])) & (kPer - 1)) * W;
-                    old[e] = atom_add_shared(cbase + (L::word(x[e]) << 2), (1u << kTop) >> r);
-                    if constexpr (GATE) top = max(top, old[e] << r);
-                }
-            } else {  // edge of the range: positions in [lo, len); others add 0 to a
-                      // private word (one per lane: no bank conflicts)
-                const uint32_t hi_n = min(len - o, 4u);
-                const uint32_t lo_n = lo > o ? lo - o : 0u;
-                m = ((1u << hi_n) - 1u) & ~((1u << lo_n) - 1u);
-                const uint32_t word0 = smem_u32(sm.cnt) + lane * 4;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const uint32_t r = ((~L::lane(x[e])) & (kPer - 1)) * W;
-                    const bool ok = (m >> e) & 1u;
-                    old[e] = atom_add_shared(ok ? cbase + (L::word(x[e]) << 2) : word0,
-                                             ok ? (1u << kTop) >> r : 0u);
-                    if constexpr (GATE) top = max(top, ok ? old[e] << r : 0u);
-                }
-            }
-            if constexpr (GATE) {
-                if (top >= gate) {  // some new value may pass: check each
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const uint32_t r = ((~L::lane(x[e])) & (kPer - 1)) * W;
-                        if ((m & (1u << e)) && (old[e] << r) >= gate)
-                            gate = cpq_admit<W>(sm.ht, sm.za, sm.scal, it.ht_cap, it.bound, it.kq,
-                                                x[e] - it.tile_lo, old[e], kTop - r);
-                    }
-                }
-                gate = (*s_at - 1) << kTop;
-            }
-        }
-    }
-}
-
 __device__ __forceinline__ void emit(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
                                      uint32_t local, uint32_t count) {
     const uint32_t pos = atomicAdd(&sm.scal[SC_NOUT], 1u);
@@ -1093,35 +1013,125 @@ __device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, 
     __syncthreads();
 }
 
+// Count the postings of one warp's groups [g0, g1) of the staged slices into
+// the tile's shared counters; with the gate on, feed the c-PQ with each new
+// value.  A group is an absolute 128-posting (512-byte) block of the postings
+// array intersected with its slice; lane l owns the 16 bytes at 4l.  Up to
+// kScanUnroll groups are loaded before any of them is counted, so a warp's
+// share costs one memory round trip per pass whatever slices it spans.
+//
+// Per posting: one shared atomicAdd of 1 << shift on the packed word (exact:
+// the query's max_count_bound keeps every counter below 2^W, so no carry
+// crosses lanes -- the reference's CAS loop, cpq.hpp:70-88, is not needed).
+// Addresses are 32-bit shared-window offsets with the tile origin folded into
+// the base (the tile origin is a multiple of 32 objects, so both layouts map
+// absolute ids linearly across 32-object blocks).  The gate test "old value
+// >= AT - 1" is done on the word shifted so the counter sits in the top W
+// bits, as one max over the four postings of a lane's group and one compare.
+template <int W, bool GATE, bool IL>
+__device__ __forceinline__ void scan_warp_groups(const uint32_t* __restrict__ postings, const ItemCtx& it,
+                                                 const ScanSmem& sm, const StageBuf& sb, uint32_t nsb, uint32_t G,
+                                                 uint32_t g0, uint32_t g1) {
+    using L = Lay<W, IL>;
+    constexpr uint32_t kPer = 32 / W, kTop = 32 - W;
+    constexpr int UNR = kScanUnroll;
+    if (g0 >= g1) return;
+    const uint32_t lane = threadIdx.x & 31;
+    // byte address of the word holding absolute id x: cbase + word(x) * 4 (mod 2^32)
+    const uint32_t cbase = smem_u32(sm.cnt) - (L::word(it.tile_lo) << 2);
+    const uint32_t word0 = smem_u32(sm.cnt) + lane * 4;  // private target of masked-off lanes
+    volatile uint32_t* s_at = sm.scal + SC_AT;
+    // slice holding group g0: last si with upref[si] <= g0 (empty slices share
+    // the next slice's prefix, so this is the non-empty one)
+    uint32_t si;
+    {
+        uint32_t lo = 0, hi = nsb;
+        while (lo < hi) {
+            const uint32_t m = (lo + hi) >> 1;
+            if (sb.upref()[m] <= g0) lo = m + 1;
+            else hi = m;
+        }
+        si = lo - 1;
+    }
+    uint64_t s_beg = sb.beg()[si];
+    uint64_t s_end = s_beg + sb.len()[si];
+    uint64_t s_blk = (s_beg >> 7) - sb.upref()[si];  // absolute block of group g: s_blk + g
+    uint32_t s_next = si + 1 < nsb ? sb.upref()[si + 1] : G;
+    uint32_t gate = 0;
+    if constexpr (GATE) gate = (*s_at - 1) << kTop;
+    for (uint32_t gb = g0; gb < g1; gb += UNR) {
+        uint4 v[UNR];
+        uint32_t msk = 0;  // 4 bits per group: the lane's positions inside the slice
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t g = gb + u;
+            v[u] = make_uint4(0, 0, 0, 0);
+            if (g < g1) {
+                while (g >= s_next) {  // warp-uniform slice advance
+                    ++si;
+                    s_beg = sb.beg()[si];
+                    s_end = s_beg + sb.len()[si];
+                    s_blk = (s_beg >> 7) - sb.upref()[si];
+                    s_next = si + 1 < nsb ? sb.upref()[si + 1] : G;
+                }
+                const uint64_t pos = ((s_blk + g) << 7) + lane * 4;
+                if (pos + 4 > s_beg && pos < s_end) {
+                    v[u] = ldg_stream_v4(postings + pos);
+                    const uint32_t lo_n = s_beg > pos ? static_cast<uint32_t>(s_beg - pos) : 0u;
+                    const uint32_t hi_n = s_end - pos < 4 ? static_cast<uint32_t>(s_end - pos) : 4u;
+                    msk |= (((1u << hi_n) - 1u) & ~((1u << lo_n) - 1u)) << (4 * u);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t m = (msk >> (4 * u)) & 0xfu;
+            if (!m) continue;
+            const uint32_t x[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            uint32_t old[4];
+            uint32_t top = 0;
+            if (m == 0xfu) {  // whole 16 bytes inside the slice: unconditional atomics
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    // r = kTop - shift: the counter's distance from the top of the word
+                    const uint32_t r = ((~L::lane(x[e])) & (kPer - 1)) * W;
+                    old[e] = atom_add_shared(cbase + (L::word(x[e]) << 2), (1u << kTop) >> r);
+                    if constexpr (GATE) top = max(top, old[e] << r);
+                }
+            } else {  // slice edge: masked-off positions add 0 to a private word
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t r = ((~L::lane(x[e])) & (kPer - 1)) * W;
+                    const bool ok = (m >> e) & 1u;
+                    old[e] = atom_add_shared(ok ? cbase + (L::word(x[e]) << 2) : word0,
+                                             ok ? (1u << kTop) >> r : 0u);
+                    if constexpr (GATE) top = max(top, ok ? old[e] << r : 0u);
+                }
+            }
+            if constexpr (GATE) {
+                if (top >= gate) {  // some new value may pass: check each
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t r = ((~L::lane(x[e])) & (kPer - 1)) * W;
+                        if ((m & (1u << e)) && (old[e] << r) >= gate)
+                            gate = cpq_admit<W>(sm.ht, sm.za, sm.scal, it.ht_cap, it.bound, it.kq,
+                                                x[e] - it.tile_lo, old[e], kTop - r);
+                    }
+                }
+                gate = (*s_at - 1) << kTop;
+            }
+        }
+    }
+}
+
+
 // One warp's share [g0, g1) of the staged slices' 128-posting groups.
 template <int W, bool IL>
 __device__ __forceinline__ void scan_group_range(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
                                                  const StageBuf& sb, uint32_t nsb, uint32_t G, uint32_t g0,
                                                  uint32_t g1) {
-    if (g0 >= g1) return;
-    // slice holding group g0: last si with upref[si] <= g0 (empty slices share
-    // the next slice's prefix, so this is the non-empty one)
-    uint32_t lo = 0, hi = nsb;
-    while (lo < hi) {
-        const uint32_t m = (lo + hi) >> 1;
-        if (sb.upref()[m] <= g0) lo = m + 1;
-        else hi = m;
-    }
-    uint32_t si = lo - 1;
-    for (;;) {
-        const uint64_t beg = sb.beg()[si];
-        const uint64_t end = beg + sb.len()[si];
-        const uint32_t gs = (si + 1 < nsb ? sb.upref()[si + 1] : G);  // slice's group end
-        const uint32_t take = min(g1, gs) - g0;
-        const uint64_t gb = (beg >> 7) + (g0 - sb.upref()[si]);
-        const uint64_t ua = max(beg, gb << 7);
-        const uint64_t ub = min(end, (gb + take) << 7);
-        if (it.gate) scan_range<W, true, IL>(p.postings, ua, ub, it, sm);
-        else scan_range<W, false, IL>(p.postings, ua, ub, it, sm);
-        g0 += take;
-        if (g0 >= g1) break;
-        while (si + 1 < nsb && sb.upref()[si + 1] <= g0) ++si;
-    }
+    if (it.gate) scan_warp_groups<W, true, IL>(p.postings, it, sm, sb, nsb, G, g0, g1);
+    else scan_warp_groups<W, false, IL>(p.postings, it, sm, sb, nsb, G, g0, g1);
 }
 
 // The sparse (posting-list) part of the tile.  Few groups per warp: a static
