@@ -881,6 +881,52 @@ __device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const Sc
     // owns blocks base + 32 j (j < BPT), so every bitmap load (one word per
     // lane) and every 16-byte counter store of the warp is contiguous.
     const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    if (nd && nd <= 3) {
+        // up to three lists (most C2 items): the level counts come straight
+        // from the bitmap words -- count >= 1, 2, 3 is OR, majority, AND
+        for (uint32_t wt = threadIdx.x >> 5; wt * 32 * BPT < nblk; wt += nwarps) {
+            const uint32_t base = wt * 32 * BPT + lane;
+            const uint32_t* col = p.bitmaps + bw0 + base;
+            uint32_t b[3][BPT];
+#pragma unroll
+            for (uint32_t u = 0; u < 3; ++u) {
+                const bool ok = u < nd;
+                const uint32_t* src = col + size_t(sb.dense()[ok ? u : 0]) * p.bitmap_words;
+#pragma unroll
+                for (uint32_t i = 0; i < BPT; ++i) b[u][i] = ok && base + 32 * i < nblk ? __ldg(src + 32 * i) : 0u;
+            }
+#pragma unroll
+            for (uint32_t i = 0; i < BPT; ++i) {
+                uint32_t acc[W];
+#pragma unroll
+                for (uint32_t m = 0; m < W; ++m) acc[m] = (b[0][i] >> m) & Sw::kOnes;
+#pragma unroll
+                for (uint32_t u = 1; u < 3; ++u) {
+                    if (u < nd) {
+#pragma unroll
+                        for (uint32_t m = 0; m < W; ++m) acc[m] += (b[u][i] >> m) & Sw::kOnes;
+                    }
+                }
+                if (base + 32 * i < nblk) {
+                    uint4* dst = reinterpret_cast<uint4*>(sm.cnt + (base + 32 * i) * W);
+#pragma unroll
+                    for (uint32_t j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                }
+                if (nlv) {
+                    const uint32_t x = b[0][i], y = b[1][i], z = b[2][i];
+                    const uint32_t ge1 = x | y | z, ge2 = (x & y) | (x & z) | (y & z), ge3 = x & y & z;
+#pragma unroll
+                    for (uint32_t l = 0; l < kLvl; ++l) {
+                        if (l < nlv) {
+                            const uint32_t v = at0 + l;
+                            lv[l] += __popc(v == 1 ? ge1 : (v == 2 ? ge2 : (v == 3 ? ge3 : 0u)));
+                        }
+                    }
+                }
+            }
+        }
+        nd = 0;  // done: skip the general lane-wise path
+    }
     for (uint32_t wt = threadIdx.x >> 5; nd && wt * 32 * BPT < nblk; wt += nwarps) {
         const uint32_t base = wt * 32 * BPT + lane;
         uint32_t acc[NW];
@@ -1343,7 +1389,16 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
         // the floor): fewer than k objects reach the floor here; they are all
         // in the table and nothing below the floor can make the global top-k.
         if (thr > 0 && thr >= floor) {
+#ifdef GENIE_PHASE_TIMERS
+            const long long tt0 = clock64();
             if (n_above < it.kq) emit_ties<W, IL>(p, it, sm, thr, it.kq - n_above);
+            if (threadIdx.x == 0) {
+                atomicAdd(&p.st[ST_T_GATE], 1ull);
+                atomicAdd(&p.st[ST_T_STAGE], static_cast<unsigned long long>(clock64() - tt0));
+            }
+#else
+            if (n_above < it.kq) emit_ties<W, IL>(p, it, sm, thr, it.kq - n_above);
+#endif
             if (threadIdx.x == 0) {
                 atomicMax(&p.q_floor[it.q], thr);
                 sm.scal[SC_BASE] = thr;

@@ -65,7 +65,7 @@ enum StatusWord : int {
     ST_T_WARP1 = 27,
     ST_T_LAT = 28,      // latency of one dependent global load in prepare_item (cycles, count)
     ST_T_LATN = 29,
-    ST_T_GATE = 30,     // prepare_item: gate start / span staging cycles
+    ST_T_GATE = 30,     // instrumented: items that tie-fill / cycles of their tie fill
     ST_T_STAGE = 31,
     ST_DENSE_ND = 17,   // instrumented: sum of dense lists per dense item | bit-sliced items << 40
     ST_T_WMAX = 18,     // instrumented: sum over items of the slowest / fastest scan warp (cycles)

@@ -25,7 +25,7 @@ def report(ix, items: int) -> str:
             f"extract={100*w[22]/tot:.1f}% | cycles/item setup={w[20]/items:.0f} dense={w[23]/items:.0f} "
             f"scan={w[21]/items:.0f} extract={w[22]/items:.0f} | admits/item calls={w[24]/items:.0f} "
             f"pass={w[25]/items:.0f} | prep={w[26]/items:.0f} warp1={w[27]/items:.0f} "
-            f"(gate={w[30]/items:.0f} stage={w[31]/items:.0f}) load_lat={w[28]/max(1, w[29]):.0f} "
+            f"tie-fill items={int(w[30])} cycles each={w[31]/max(1, w[30]):.0f} "
             f"scan warps max={w[18]/items:.0f} min={w[19]/items:.0f} | dense lists total={int(w[17]) & ((1 << 40) - 1)} "
             f"bit-sliced items={int(w[17]) >> 40}")
 
