@@ -796,7 +796,7 @@ __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32
 // v in [at0, at0 + kLvl) (Swar::ge + popc), for the c-PQ catch-up below.
 template <int W>
 __device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb,
-                               uint32_t nd, uint32_t at0, uint32_t nlv, bool& csa_path) {
+                               uint32_t nd, uint32_t at0, uint32_t nlv, bool& csa_path, long long* t_work = nullptr) {
     using Sw = Swar<W>;
     constexpr uint32_t BPT = W == 4 ? 4 : (W == 8 ? 2 : 1);  // blocks per thread step (16 words)
     constexpr uint32_t NW = BPT * W;
@@ -991,6 +991,7 @@ __device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const Sc
             }
         }
     }
+    if (t_work) *t_work = clock64();
     __syncthreads();
     return reach;
 }
@@ -1628,12 +1629,21 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
         const long long t_d = clock64();
 #endif
         bool csa_path;
+#ifdef GENIE_PHASE_TIMERS
+        long long t_di = 0;
+        const uint32_t reach = dense_init<W>(p, it, sm, sm.sb(b), nd, at0, nlv, csa_path, &t_di);
+        const long long t_db = clock64();
+#else
         const uint32_t reach = dense_init<W>(p, it, sm, sm.sb(b), nd, at0, nlv, csa_path);
+#endif
         if (it.gate && at0 <= dmax) dense_gate<W>(it, sm, at0, dmax, nlv, reach, csa_path);
 #ifdef GENIE_PHASE_TIMERS
         if (threadIdx.x == 0) {
             atomicAdd(&p.st[ST_T_DENSE], static_cast<unsigned long long>(clock64() - t_d));
-            atomicAdd(&p.st[ST_DENSE_ND], static_cast<unsigned long long>(nd) | (csa_path ? (1ull << 40) : 0ull));
+            atomicAdd(&p.st[ST_DENSE_ND],
+                      static_cast<unsigned long long>(nd) | (1ull << 32) | (csa_path ? (1ull << 48) : 0ull));
+            atomicAdd(&p.st[ST_T_LAT], static_cast<unsigned long long>(t_di - t_d));
+            atomicAdd(&p.st[ST_T_LATN], static_cast<unsigned long long>(t_db - t_d));
         }
 #endif
         scan_and_select<W, true>(p, it, sm, b, S, nsb, G, total);

@@ -26,8 +26,10 @@ def report(ix, items: int) -> str:
             f"scan={w[21]/items:.0f} extract={w[22]/items:.0f} | admits/item calls={w[24]/items:.0f} "
             f"pass={w[25]/items:.0f} | prep={w[26]/items:.0f} warp1={w[27]/items:.0f} "
             f"tie-fill items={int(w[30])} cycles each={w[31]/max(1, w[30]):.0f} "
-            f"scan warps max={w[18]/items:.0f} min={w[19]/items:.0f} | dense lists total={int(w[17]) & ((1 << 40) - 1)} "
-            f"bit-sliced items={int(w[17]) >> 40}")
+            f"scan warps max={w[18]/items:.0f} min={w[19]/items:.0f} | dense items={(int(w[17]) >> 32) & 0xffff} "
+            f"lists={int(w[17]) & 0xffffffff} bit-sliced={int(w[17]) >> 48} | per dense item: thread-0 work "
+            f"{w[28]/max(1, (int(w[17]) >> 32) & 0xffff):.0f} init+barrier {w[29]/max(1, (int(w[17]) >> 32) & 0xffff):.0f} "
+            f"total {w[23]/max(1, (int(w[17]) >> 32) & 0xffff):.0f}")
 
 
 if __name__ == "__main__":
