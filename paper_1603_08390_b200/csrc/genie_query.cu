@@ -882,44 +882,49 @@ __device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const Sc
     // lane) and every 16-byte counter store of the warp is contiguous.
     const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     if (nd && nd <= 3) {
-        // up to three lists (most C2 items): the level counts come straight
-        // from the bitmap words -- count >= 1, 2, 3 is OR, majority, AND
+        // up to three lists (most C2 items): a full adder turns the bitmap
+        // words x, y, z into the two bit planes of the count (sum, carry),
+        // spread into the counter words once; the level counts come from the
+        // same words (count >= 1, 2, 3 is OR, majority, AND)
+        const uint32_t* rows[3];
+#pragma unroll
+        for (uint32_t u = 0; u < 3; ++u) rows[u] = p.bitmaps + bw0 + lane + size_t(sb.dense()[u < nd ? u : 0]) * p.bitmap_words;
         for (uint32_t wt = threadIdx.x >> 5; wt * 32 * BPT < nblk; wt += nwarps) {
             const uint32_t base = wt * 32 * BPT + lane;
-            const uint32_t* col = p.bitmaps + bw0 + base;
+            const bool full = (wt + 1) * 32 * BPT <= nblk;
             uint32_t b[3][BPT];
 #pragma unroll
             for (uint32_t u = 0; u < 3; ++u) {
-                const bool ok = u < nd;
-                const uint32_t* src = col + size_t(sb.dense()[ok ? u : 0]) * p.bitmap_words;
+                const uint32_t* src = rows[u] + wt * 32 * BPT;
 #pragma unroll
-                for (uint32_t i = 0; i < BPT; ++i) b[u][i] = ok && base + 32 * i < nblk ? __ldg(src + 32 * i) : 0u;
+                for (uint32_t i = 0; i < BPT; ++i)
+                    b[u][i] = u < nd && (full || base + 32 * i < nblk) ? __ldg(src + 32 * i) : 0u;
             }
 #pragma unroll
             for (uint32_t i = 0; i < BPT; ++i) {
-                uint32_t acc[W];
+                const uint32_t x = b[0][i], y = b[1][i], z = b[2][i];
+                const uint32_t s0 = x ^ y ^ z, s1 = (x & y) | (x & z) | (y & z);
+                if (full || base + 32 * i < nblk) {
+                    uint32_t acc[W];
 #pragma unroll
-                for (uint32_t m = 0; m < W; ++m) acc[m] = (b[0][i] >> m) & Sw::kOnes;
-#pragma unroll
-                for (uint32_t u = 1; u < 3; ++u) {
-                    if (u < nd) {
-#pragma unroll
-                        for (uint32_t m = 0; m < W; ++m) acc[m] += (b[u][i] >> m) & Sw::kOnes;
+                    for (uint32_t m = 0; m < W; ++m) {
+                        if constexpr (W <= 4) {
+                            acc[m] = ((s0 >> m) & Sw::kOnes) | (((s1 >> m) & Sw::kOnes) << 1);
+                        } else {
+                            acc[m] = ((s0 >> m) & Sw::kOnes) + (((s1 >> m) & Sw::kOnes) << 1);
+                        }
                     }
-                }
-                if (base + 32 * i < nblk) {
                     uint4* dst = reinterpret_cast<uint4*>(sm.cnt + (base + 32 * i) * W);
 #pragma unroll
                     for (uint32_t j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
                 }
                 if (nlv) {
-                    const uint32_t x = b[0][i], y = b[1][i], z = b[2][i];
-                    const uint32_t ge1 = x | y | z, ge2 = (x & y) | (x & z) | (y & z), ge3 = x & y & z;
+                    const uint32_t ge1 = x | y | z, ge3 = x & y & z;
 #pragma unroll
                     for (uint32_t l = 0; l < kLvl; ++l) {
                         if (l < nlv) {
                             const uint32_t v = at0 + l;
-                            lv[l] += __popc(v == 1 ? ge1 : (v == 2 ? ge2 : (v == 3 ? ge3 : 0u)));
+                            lv[l] += __popc(v == 1 ? ge1 : (v == 2 ? s1 : (v == 3 ? ge3 : 0u)));
                         }
                     }
                 }
