@@ -1744,7 +1744,8 @@ __device__ __forceinline__ uint32_t nlists_of(const MergeSrc& m, uint32_t q) {
 // merge_topk (engine.hpp:158-177) for unions of at most kSortCap entries:
 // concatenate, bitonic sort by (count desc, id asc), truncate to k,
 // threshold = k-th count if at least k entries else 0.
-__global__ void __launch_bounds__(kMergeThreads, 1) k_merge(MergeSrc m) {
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_merge(MergeSrc m, uint32_t cap) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
     __shared__ unsigned long long sums[32];
@@ -1775,13 +1776,13 @@ __global__ void __launch_bounds__(kMergeThreads, 1) k_merge(MergeSrc m) {
                     if (lane == 0 && mask) base = atomicAdd(&s_pos, static_cast<uint32_t>(__popc(mask)));
                     base = __shfl_sync(0xffffffffu, base, 0);
                     const uint32_t pos = base + __popc(mask & ((1u << lane) - 1u));
-                    if (keep && pos < kSortCap) keys[pos] = order_key(x.id, x.count);
+                    if (keep && pos < cap) keys[pos] = order_key(x.id, x.count);
                 }
             }
         }
         __syncthreads();
         const uint32_t filled = s_pos;
-        if (filled > kSortCap) {  // large union: radix selection path
+        if (filled > cap) {  // large union: radix selection path (k_merge_big)
             if (threadIdx.x == 0) {
                 m.q_big[q] = 1;
                 atomicAdd(&m.st[ST_MERGE_BIG], 1ull);
@@ -2299,14 +2300,18 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         const size_t msmem = kSortCap * sizeof(uint64_t);
         static thread_local bool mconf = false;
         if (!mconf) {
-            GENIE_CUDA(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(msmem)));
+            GENIE_CUDA(cudaFuncSetAttribute(k_merge<kMergeSmallThreads>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kMergeSmallCap * sizeof(uint64_t))));
             GENIE_CUDA(cudaFuncSetAttribute(k_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(msmem)));
             mconf = true;
         }
         const uint32_t mgrid = std::min<uint32_t>(Q, sms * 4);
-        k_merge<<<mgrid, kMergeThreads, msmem, s>>>(m);
+        // one small CTA per query: after the floors prune them, unions are a
+        // few k entries, so all queries merge concurrently; larger unions are
+        // left to k_merge_big
+        k_merge<kMergeSmallThreads><<<Q, kMergeSmallThreads, kMergeSmallCap * sizeof(uint64_t), s>>>(m, kMergeSmallCap);
         k_merge_big<<<mgrid, kMergeThreads, msmem, s>>>(m);
         launches += 2;
         if (max_k > kSortCap) {
@@ -2398,13 +2403,13 @@ void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entr
     m.out_thr = d_out_thr;
     k_init_status<<<1, 32, 0, s>>>(w.status.p);
     const size_t msmem = kSortCap * sizeof(uint64_t);
-    GENIE_CUDA(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GENIE_CUDA(cudaFuncSetAttribute(k_merge<kMergeThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(msmem)));
     GENIE_CUDA(cudaFuncSetAttribute(k_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(msmem)));
     const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(Q, ix->sms * 4));
     if (Q) {
-        k_merge<<<grid, kMergeThreads, msmem, s>>>(m);
+        k_merge<kMergeThreads><<<grid, kMergeThreads, msmem, s>>>(m, kSortCap);
         k_merge_big<<<grid, kMergeThreads, msmem, s>>>(m);
         if (max_k > kSortCap) segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, 0, s);
     }

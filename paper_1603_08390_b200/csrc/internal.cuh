@@ -26,6 +26,8 @@ constexpr int kRecLevels = 4;                 // levels in a tile's record (gate
 constexpr uint32_t kRecWords = 8;             // record: base level + kRecLevels counts, padded to 16 B
 constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shared memory (W <= 8)
 constexpr uint32_t kMergeThreads = 512;
+constexpr uint32_t kMergeSmallThreads = 256;   // per-query merge CTAs of a batch
+constexpr uint32_t kMergeSmallCap = 4096;      // their key capacity (<= 16 x threads)
 constexpr uint32_t kSortCap = 8192;           // merge entries sorted in shared memory
 constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit (guided scheduling)
 #ifndef GENIE_DENSE_LEVELS
