@@ -237,8 +237,10 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
 // width classes follow each other and queries keep request order.  Items of
 // the same tile read the same slice of every hot list, so the hot slice of
 // the index stays L2-resident while the batch sweeps it.
-__global__ void k_worklist(BatchParams p) {
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_worklist(BatchParams p) {
+    // one warp per query, lanes over its tiles
+    const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
     if (q >= p.Q || p.st[ST_OVERFLOW]) return;
     const uint32_t nt = p.q_ntiles[q];
     if (!nt) return;
@@ -249,7 +251,8 @@ __global__ void k_worklist(BatchParams p) {
         ntc[i] = p.n ? ntiles_for(p.n, p.tile_bits, 4u << i) : 0;
     }
     const uint32_t rank = p.q_rank[q];
-    for (uint32_t t = 0; t < nt; ++t) {
+    const uint32_t tbase = p.q_tile_base[q];
+    for (uint32_t t = lane; t < nt; t += 32) {
         uint64_t item = rank;
         for (int i = 0; i < 3; ++i) {
             item += cnt[i] * (uint64_t(t) < ntc[i] ? uint64_t(t) : ntc[i]);
@@ -257,7 +260,7 @@ __global__ void k_worklist(BatchParams p) {
         }
         p.work_q[item] = q;
         p.work_t[item] = t;
-        uint4* rec = reinterpret_cast<uint4*>(p.tile_rec + uint64_t(p.q_tile_base[q] + t) * kRecWords);
+        uint4* rec = reinterpret_cast<uint4*>(p.tile_rec + uint64_t(tbase + t) * kRecWords);
 #pragma unroll
         for (uint32_t j = 0; j < kRecWords / 4; ++j) rec[j] = make_uint4(0, 0, 0, 0);
     }
@@ -282,17 +285,20 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
         const uint64_t j = p.it_kb[it] + (s - p.it_sbase[it]);
         const uint64_t beg = p.key_off[j];
         const uint32_t len = static_cast<uint32_t>(p.key_off[j + 1] - beg);
+        // the list's bitmap replaces its posting scan when the list is dense
+        // enough for this query's counter width (bit-sliced / lane-wise adds
+        // per 32 objects vs. an atomic per posting)
+        int32_t ds = p.n_dense ? p.key_dense[j] : -1;
+        const uint32_t inv = p.dense_inv[wclass(p.q_W[q])];
+        if (ds >= 0 && inv && uint64_t(len) * inv < p.n) ds = -1;
         if (lane == 0) {
             p.span_beg[g] = beg;
-            // the list's bitmap replaces its posting scan when the list is dense
-            // enough for this query's counter width (bit-sliced / lane-wise
-            // adds per 32 objects vs. an atomic per posting)
-            int32_t ds = p.n_dense ? p.key_dense[j] : -1;
-            const uint32_t inv = p.dense_inv[wclass(p.q_W[q])];
-            if (ds >= 0 && inv && uint64_t(len) * inv < p.n) ds = -1;
             p.span_dense[g] = ds;
             if (ds >= 0) atomicAdd(&p.q_nd[q], 1u);  // dense spans per query
         }
+        // k_scan uses the bitmaps when all of the query's spans fit one staging
+        // batch; then this list needs no tile cuts
+        if (ds >= 0 && p.q_S[q] <= kSpanBatch) continue;
         const uint32_t nt = p.q_ntiles[q];
         const uint32_t T = p.tile_bits / p.q_W[q];
         uint32_t* cut = p.cuts + p.q_cut_base[q] + uint64_t(s) * (nt + 1);
@@ -1239,13 +1245,17 @@ __device__ __forceinline__ void stage_one(const BatchParams& p, const StageArgs&
         beg = p.key_off[kb];
         len = static_cast<uint32_t>(p.key_off[kb + p.it_nk[it_i]] - beg);
     } else {
+        if (a.dense) {
+            dslot = p.span_dense[a.sbq + s];
+            if (dslot >= 0) {  // the list's bitmap covers this tile: no posting scan (and no cuts)
+                beg = 0;
+                len = 0;
+                return;
+            }
+        }
         const uint32_t* c = p.cuts + a.cb + uint64_t(s) * (a.nt + 1) + t;
         beg = p.span_beg[a.sbq + s] + c[0];
         len = c[1] - c[0];
-        if (a.dense) {
-            dslot = p.span_dense[a.sbq + s];
-            if (dslot >= 0) len = 0;  // the list's bitmap covers this tile: no posting scan
-        }
     }
 }
 
@@ -2273,7 +2283,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     if (Q) {
         k_resolve<<<(Q * 32 + 255) / 256, 256, 0, s>>>(p);
         k_plan<<<1, 1024, 0, s>>>(p);
-        k_worklist<<<(Q + 255) / 256, 256, 0, s>>>(p);
+        k_worklist<<<(Q * 32 + 255) / 256, 256, 0, s>>>(p);
         launches += 3;
         const int sms = ix->sms;
         k_cut<<<sms * 8, 256, 0, s>>>(p);
