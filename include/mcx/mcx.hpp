@@ -14,12 +14,16 @@
 #pragma once
 
 #include <algorithm>
+#include <cctype>
 #include <cstdint>
 #include <memory>
 #include <optional>
+#include <set>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
+#include <unordered_map>
 #include <vector>
 
 #include "genie/genie.h"
@@ -383,6 +387,62 @@ inline BatchResult execute_partitioned(std::span<const IndexPartition> partition
 }
 
 // ------------------------------------------------------------------ lsh.hpp
+
+// ------------------------------------------------------------------ documents
+// tokenize_document / DocumentCodec (sa.hpp:341-408): lowercased whitespace
+// words minus stop words, deduplicated; token = rank in the sorted build
+// vocabulary, dim 0 (the Tweets adapter).
+
+inline std::vector<std::string> tokenize_document(std::string_view text,
+                                                  const std::set<std::string>& stop_words = {}) {
+    std::set<std::string> words;
+    std::string cur;
+    auto flush = [&] {
+        if (!cur.empty() && !stop_words.contains(cur)) words.insert(cur);
+        cur.clear();
+    };
+    for (const char ch : text) {
+        if (std::isspace(static_cast<unsigned char>(ch))) flush();
+        else cur.push_back(static_cast<char>(std::tolower(static_cast<unsigned char>(ch))));
+    }
+    flush();
+    return {words.begin(), words.end()};
+}
+
+class DocumentCodec {
+public:
+    static DocumentCodec build(std::span<const std::string> corpus, std::set<std::string> stop_words = {}) {
+        DocumentCodec c;
+        c.stop_ = std::move(stop_words);
+        std::set<std::string> all;
+        for (const auto& doc : corpus)
+            for (auto& w : tokenize_document(doc, c.stop_)) all.insert(std::move(w));
+        Token t = 0;
+        for (const auto& w : all) c.vocab_.emplace(w, t++);
+        return c;
+    }
+    std::size_t vocabulary_size() const noexcept { return vocab_.size(); }
+    ObjectRecord encode(std::string_view text, ObjectId id) const {
+        std::vector<Keyword> kws;
+        for (const auto& w : tokenize_document(text, stop_)) {
+            const auto it = vocab_.find(w);
+            if (it == vocab_.end()) throw ContractError("document word outside the vocabulary");
+            kws.push_back(Keyword{0, it->second});
+        }
+        return ObjectRecord(id, std::move(kws));
+    }
+    std::optional<Query> encode_query(std::string_view text, std::uint32_t k, std::uint32_t query_id = 0) const {
+        std::vector<QueryItem> items;
+        for (const auto& w : tokenize_document(text, stop_))
+            if (const auto it = vocab_.find(w); it != vocab_.end()) items.push_back(QueryItem::point(0, it->second));
+        if (items.empty()) return std::nullopt;
+        return Query(query_id, std::move(items), k);
+    }
+
+private:
+    std::set<std::string> stop_;
+    std::unordered_map<std::string, Token> vocab_;
+};
 
 enum class LshFamily { p_stable, random_binning };
 

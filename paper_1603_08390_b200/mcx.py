@@ -153,6 +153,70 @@ def encode_relational_query(schema: RelationalSchema, ranges: Sequence[Attribute
     return Query(query_id, items, k)
 
 
+# --------------------------------------------------------------------- sa.hpp
+
+
+def tokenize_document(text: str, stop_words: Iterable[str] = ()) -> List[str]:
+    """Lowercased whitespace-separated words minus stop words, deduplicated and
+    sorted (tokenize_document, sa.hpp:341-359).  Whitespace and lowercasing are
+    the C locale's (ASCII), as std::isspace / std::tolower there."""
+    stop = set(stop_words)
+    words = set()
+    cur: List[str] = []
+
+    def flush():
+        if cur:
+            w = "".join(cur)
+            if w not in stop:
+                words.add(w)
+            cur.clear()
+
+    for ch in text:
+        if ch in " \t\n\v\f\r":
+            flush()
+        else:
+            cur.append(ch.lower() if "A" <= ch <= "Z" else ch)
+    flush()
+    return sorted(words)
+
+
+class DocumentCodec:
+    """Word vocabulary for bag-of-words documents (DocumentCodec, sa.hpp:361-408):
+    token = the word's rank in the sorted build-corpus vocabulary, all on dim 0,
+    so the match count of two encoded documents is the size of their word-set
+    intersection (the Tweets workload)."""
+
+    def __init__(self):
+        self._stop: set = set()
+        self._vocab: dict = {}
+
+    @staticmethod
+    def build(corpus: Iterable[str], stop_words: Iterable[str] = ()) -> "DocumentCodec":
+        c = DocumentCodec()
+        c._stop = set(stop_words)
+        words = set()
+        for doc in corpus:
+            words.update(tokenize_document(doc, c._stop))
+        c._vocab = {w: i for i, w in enumerate(sorted(words))}
+        return c
+
+    def vocabulary_size(self) -> int:
+        return len(self._vocab)
+
+    def encode(self, text: str, id: int) -> ObjectRecord:
+        kws = []
+        for w in tokenize_document(text, self._stop):
+            if w not in self._vocab:
+                raise ContractError("document word outside the vocabulary")
+            kws.append(Keyword(0, self._vocab[w]))
+        return ObjectRecord(id, kws)
+
+    def encode_query(self, text: str, k: int, query_id: int = 0) -> Optional[Query]:
+        """Words outside the vocabulary are dropped; None when nothing is left."""
+        items = [QueryItem.point(0, self._vocab[w]) for w in tokenize_document(text, self._stop) if w in self._vocab]
+        return Query(query_id, items, k) if items else None
+
+
 # -------------------------------------------------------------------- cpq.hpp
 
 

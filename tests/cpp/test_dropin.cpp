@@ -127,6 +127,20 @@ int main() {
     const std::vector<float> p = {0.1f, -2.0f, 3.0f, 0.7f};
     CHECK(match_count_reference(enc.encode_query_point(p, 1), enc.encode_point(p, 0)) == 16);
 
+    // documents (test_sa.cpp:208-226): DocumentCodec -> engine
+    CHECK(tokenize_document("a b a").size() == 2);
+    CHECK(tokenize_document("The the THE").size() == 1);
+    CHECK(tokenize_document("the cat", {"the"}).size() == 1);
+    const std::vector<std::string> corpus = {"big data engine", "data data lake"};
+    const DocumentCodec codec = DocumentCodec::build(corpus);
+    std::vector<ObjectRecord> docs = {codec.encode(corpus[0], 0), codec.encode(corpus[1], 1)};
+    const auto dq = codec.encode_query("engine data", 2);
+    CHECK(dq.has_value() && match_count_reference(*dq, docs[0]) == 2 && match_count_reference(*dq, docs[1]) == 1);
+    CHECK(!codec.encode_query("unseen words only", 1).has_value());
+    const auto dres = execute_batch(build_index(docs), std::vector<Query>{*dq});
+    CHECK(dres.results[0].entries.size() == 2 && dres.results[0].entries[0] == (TopKEntry{0, 2}) &&
+          dres.results[0].entries[1] == (TopKEntry{1, 1}) && dres.results[0].threshold == 1);
+
     std::printf(failures ? "dropin: %d failures\n" : "dropin: ok\n", failures);
     return failures ? 1 : 0;
 }

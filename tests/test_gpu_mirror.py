@@ -110,3 +110,24 @@ def test_lsh_identical_point_matches_itself(gpu):
     q = enc.encode_query_point(p, 1)
     assert len(obj.keywords()) == 16 and len(q.items) == 16
     assert mcx.match_count_reference(q, obj) == 16
+
+
+def test_documents_through_the_engine(gpu):
+    # DocumentCodec (sa.hpp:361-408) -> build_index -> execute_batch: the top-k
+    # of word-set intersections, equal to the full scan (the Tweets adapter)
+    rng = random.Random(23)
+    vocab = [f"w{i}" for i in range(60)] + ["The", "THE", "the"]
+    docs = [" ".join(rng.choice(vocab) for _ in range(rng.randint(1, 12))) for _ in range(700)]
+    codec = mcx.DocumentCodec.build(docs, stop_words={"the"})
+    objects = [codec.encode(d, i) for i, d in enumerate(docs)]
+    queries = []
+    for q in range(40):
+        text = " ".join(rng.choice(vocab + ["unseen"]) for _ in range(rng.randint(1, 8)))
+        query = codec.encode_query(text, 1 + rng.randrange(30), q)
+        if query is not None:
+            queries.append(query)
+    index = mcx.build_index(objects)
+    batch = mcx.execute_batch(index, queries)
+    for q, query in enumerate(queries):
+        ent, thr = oracle_result(query, objects)
+        assert batch.results[q].entries == ent and batch.results[q].threshold == thr

@@ -154,3 +154,50 @@ def test_lsh_parameter_sampling_equals_reference():
         w, sigma = (float(x) for x in g[name + "_wsig"])
         a, b, hs, rs = E.lsh_sample(E.lsh_config(fam, m, dims, seed, domain, w=w, sigma=sigma))
         assert np.array_equal(a, g[name + "_a"]) and np.array_equal(b, g[name + "_b"]) and np.array_equal(rs, g[name + "_rs"])
+
+
+def test_documents_deduplicate_and_intersect():
+    # test_sa.cpp:208-226 (tokenize_document / DocumentCodec, sa.hpp:341-408)
+    from paper_1603_08390_b200 import mcx
+
+    assert len(mcx.tokenize_document("a b a")) == 2
+    assert len(mcx.tokenize_document("The the THE")) == 1
+    assert len(mcx.tokenize_document("the cat", {"the"})) == 1
+    corpus = ["big data engine", "data data lake"]
+    codec = mcx.DocumentCodec.build(corpus)
+    assert codec.vocabulary_size() == 4
+    d0, d1 = codec.encode(corpus[0], 0), codec.encode(corpus[1], 1)
+    q = codec.encode_query("engine data", 2)
+    assert q is not None
+    assert mcx.match_count_reference(q, d0) == 2 and mcx.match_count_reference(q, d1) == 1
+    assert mcx.match_count_reference(codec.encode_query(corpus[0], 1), d0) == 3
+    assert codec.encode_query("unseen words only", 1) is None
+    with pytest.raises(mcx.ContractError):
+        codec.encode("unseen", 5)
+
+
+def test_document_match_counts_equal_set_intersections():
+    # test_sa.cpp:228-256
+    import random
+
+    from paper_1603_08390_b200 import mcx
+
+    rng = random.Random(17)
+    words = ["red", "green", "blue", "cyan", "teal", "gray", "pink", "gold", "jade", "rust"]
+    for _ in range(100):
+        def pick():
+            s = set()
+            n = 1 + rng.randrange(6)
+            while len(s) < n:
+                s.add(words[rng.randrange(len(words))])
+            return " ".join(sorted(s)) + " ", s
+        doc_text, doc_set = pick()
+        q_text, q_set = pick()
+        codec = mcx.DocumentCodec.build([doc_text])
+        obj = codec.encode(doc_text, 0)
+        query = codec.encode_query(q_text, 1)
+        common = len(q_set & doc_set)
+        if query is None:
+            assert common == 0
+        else:
+            assert mcx.match_count_reference(query, obj) == common
