@@ -1089,7 +1089,7 @@ __device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, 
 template <int W, bool GATE, bool IL>
 __device__ __forceinline__ void scan_warp_groups(const uint32_t* __restrict__ postings, const ItemCtx& it,
                                                  const ScanSmem& sm, const StageBuf& sb, uint32_t nsb, uint32_t G,
-                                                 uint32_t g0, uint32_t g1) {
+                                                 uint32_t g0, uint32_t g1, uint32_t stride) {
     using L = Lay<W, IL>;
     constexpr uint32_t kPer = 32 / W, kTop = 32 - W;
     constexpr int UNR = kScanUnroll;
@@ -1117,12 +1117,12 @@ __device__ __forceinline__ void scan_warp_groups(const uint32_t* __restrict__ po
     uint32_t s_next = si + 1 < nsb ? sb.upref()[si + 1] : G;
     uint32_t gate = 0;
     if constexpr (GATE) gate = (*s_at - 1) << kTop;
-    for (uint32_t gb = g0; gb < g1; gb += UNR) {
+    for (uint32_t gb = g0; gb < g1; gb += UNR * stride) {
         uint4 v[UNR];
         uint32_t msk = 0;  // 4 bits per group: the lane's positions inside the slice
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-            const uint32_t g = gb + u;
+            const uint32_t g = gb + u * stride;
             v[u] = make_uint4(0, 0, 0, 0);
             if (g < g1) {
                 while (g >= s_next) {  // warp-uniform slice advance
@@ -1187,9 +1187,9 @@ __device__ __forceinline__ void scan_warp_groups(const uint32_t* __restrict__ po
 template <int W, bool IL>
 __device__ __forceinline__ void scan_group_range(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
                                                  const StageBuf& sb, uint32_t nsb, uint32_t G, uint32_t g0,
-                                                 uint32_t g1) {
-    if (it.gate) scan_warp_groups<W, true, IL>(p.postings, it, sm, sb, nsb, G, g0, g1);
-    else scan_warp_groups<W, false, IL>(p.postings, it, sm, sb, nsb, G, g0, g1);
+                                                 uint32_t g1, uint32_t stride = 1) {
+    if (it.gate) scan_warp_groups<W, true, IL>(p.postings, it, sm, sb, nsb, G, g0, g1, stride);
+    else scan_warp_groups<W, false, IL>(p.postings, it, sm, sb, nsb, G, g0, g1, stride);
 }
 
 // The sparse (posting-list) part of the tile.  Few groups per warp: a static
@@ -1204,9 +1204,14 @@ __device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanS
     const uint32_t warp = (threadIdx.x >> 5) - wfirst;
     const uint32_t nwarps = (blockDim.x >> 5) - wfirst;
     if (G <= kStaticGroups * nwarps) {
+#if GENIE_SCAN_STRIDED
+        // round-robin groups: every warp's share mixes hot (L2) and cold lists
+        scan_group_range<W, IL>(p, it, sm, sb, nsb, G, warp, G, nwarps);
+#else
         const uint32_t g0 = static_cast<uint32_t>(uint64_t(G) * warp / nwarps);
         const uint32_t g1 = static_cast<uint32_t>(uint64_t(G) * (warp + 1) / nwarps);
         scan_group_range<W, IL>(p, it, sm, sb, nsb, G, g0, g1);
+#endif
         return;
     }
     const uint32_t max_chunk = max(1u, unit >> 7);

@@ -34,6 +34,9 @@ constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit (gu
 #define GENIE_DENSE_LEVELS 2
 #endif
 constexpr uint32_t kLvl = GENIE_DENSE_LEVELS;  // dense-phase c-PQ levels counted in registers
+#ifndef GENIE_SCAN_STRIDED
+#define GENIE_SCAN_STRIDED 0
+#endif
 constexpr int kScanUnroll = GENIE_SCAN_UNROLL;               // 128-posting groups loaded per warp pass
 constexpr uint32_t kStaticGroups = 64;        // <= this many 128-posting groups per warp: static split
 constexpr uint64_t kEmptySlot = ~0ull;
