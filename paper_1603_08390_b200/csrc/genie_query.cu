@@ -321,12 +321,17 @@ struct StageBuf {
     uint8_t* base;
     // slice start (absolute posting position)
     __device__ __forceinline__ uint64_t* beg() const { return reinterpret_cast<uint64_t*>(base); }
-    // slice length (0 for dense spans)
-    __device__ __forceinline__ uint32_t* len() const { return reinterpret_cast<uint32_t*>(base + kSpanBatch * 8); }
+    // postings before each slice (kSpanBatch + 1 entries): slice i has
+    // ppref[i + 1] - ppref[i] postings (0 for dense spans)
+    __device__ __forceinline__ uint32_t* ppref() const { return reinterpret_cast<uint32_t*>(base + kSpanBatch * 8); }
     // rank of the slice's first 128-posting group
-    __device__ __forceinline__ uint32_t* upref() const { return reinterpret_cast<uint32_t*>(base + kSpanBatch * 12); }
+    __device__ __forceinline__ uint32_t* upref() const {
+        return reinterpret_cast<uint32_t*>(base + kSpanBatch * 12 + 16);
+    }
     // dense-container slots of the staged spans, in span order
-    __device__ __forceinline__ uint32_t* dense() const { return reinterpret_cast<uint32_t*>(base + kSpanBatch * 16); }
+    __device__ __forceinline__ uint32_t* dense() const {
+        return reinterpret_cast<uint32_t*>(base + kSpanBatch * 16 + 16);
+    }
 };
 
 // One work item as prepared by warp 0 (prepare_item); 64 bytes.
@@ -334,7 +339,7 @@ struct ItemDesc {
     uint32_t valid, q, t, kq, bound, W, cap, nt, S, nd, G, a0;
     uint64_t out_base;
     uint32_t tile_slot;  // q_tile_base[q] + t: the item's tile_len / tile_rec slot
-    uint32_t pad;
+    uint32_t ptot;       // postings of the first staged batch
 };
 
 // Shared memory of a scan CTA.  Everything but the counters sits at a fixed
@@ -349,7 +354,7 @@ struct ScanSmem {
     uint32_t* scal;            // scalars
     ItemDesc* desc;            // [2]
     uint8_t* stage;            // 2 x StageBuf
-    __device__ __forceinline__ StageBuf sb(uint32_t b) const { return StageBuf{stage + b * (kSpanBatch * 20)}; }
+    __device__ __forceinline__ StageBuf sb(uint32_t b) const { return StageBuf{stage + b * (kSpanBatch * 20 + 16)}; }
 };
 
 enum ScalarSlot {
@@ -386,7 +391,7 @@ constexpr uint32_t kDesc = kSums + 256;                        // 2 x ItemDesc
 constexpr uint32_t kZa = kDesc + 2 * sizeof(ItemDesc);         // kZaMax u32
 constexpr uint32_t kEhist = kZa + kZaMax * 4;                  // kHistBins u32
 constexpr uint32_t kStage = kEhist + kHistBins * 4;            // 2 x StageBuf
-constexpr uint32_t kStageBytes = kSpanBatch * (8 + 4 + 4 + 4);
+constexpr uint32_t kStageBytes = kSpanBatch * (8 + 4 + 4 + 4) + 16;
 constexpr uint32_t kHt = kStage + 2 * kStageBytes;             // ht_slots u64, then the tile
 static_assert(kHt % 16 == 0, "16-byte aligned table");
 }  // namespace smem_off
@@ -400,7 +405,7 @@ __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t ht_slots) {
     s.za = reinterpret_cast<uint32_t*>(base + kZa);
     s.ehist = reinterpret_cast<uint32_t*>(base + kEhist);
     s.stage = base + kStage;
-    static_assert(kStageBytes == kSpanBatch * 20, "stage buffer layout");
+    static_assert(kStageBytes == kSpanBatch * 20 + 16, "stage buffer layout");
     s.cnt = reinterpret_cast<uint32_t*>(base + kHt);
     s.ht = nullptr;  // per item: right after the item's counters (process_item)
     (void)ht_slots;
@@ -1112,7 +1117,7 @@ __device__ __forceinline__ void scan_warp_groups(const uint32_t* __restrict__ po
         si = lo - 1;
     }
     uint64_t s_beg = sb.beg()[si];
-    uint64_t s_end = s_beg + sb.len()[si];
+    uint64_t s_end = s_beg + (sb.ppref()[si + 1] - sb.ppref()[si]);
     uint64_t s_blk = (s_beg >> 7) - sb.upref()[si];  // absolute block of group g: s_blk + g
     uint32_t s_next = si + 1 < nsb ? sb.upref()[si + 1] : G;
     uint32_t gate = 0;
@@ -1128,7 +1133,7 @@ __device__ __forceinline__ void scan_warp_groups(const uint32_t* __restrict__ po
                 while (g >= s_next) {  // warp-uniform slice advance
                     ++si;
                     s_beg = sb.beg()[si];
-                    s_end = s_beg + sb.len()[si];
+                    s_end = s_beg + (sb.ppref()[si + 1] - sb.ppref()[si]);
                     s_blk = (s_beg >> 7) - sb.upref()[si];
                     s_next = si + 1 < nsb ? sb.upref()[si + 1] : G;
                 }
@@ -1183,6 +1188,67 @@ __device__ __forceinline__ void scan_warp_groups(const uint32_t* __restrict__ po
 }
 
 
+// Compact mode for tiles whose slices are short (average 128-posting group
+// less than half full, e.g. minHash: ~10 postings per list per tile): the
+// warp's share is a contiguous run [r0, r1) of the item's postings counted
+// across its slices; lane l takes postings r0 + l + 32 j, one 4-byte id each,
+// so every shared atomic instruction carries 32 real postings.  Each lane
+// tracks the slice of its position (ppref: postings before each slice).
+template <int W, bool GATE, bool IL>
+__device__ __forceinline__ void scan_compact(const uint32_t* __restrict__ postings, const ItemCtx& it,
+                                             const ScanSmem& sm, const StageBuf& sb, uint32_t nsb, uint32_t r0,
+                                             uint32_t r1) {
+    using L = Lay<W, IL>;
+    constexpr uint32_t kPer = 32 / W, kTop = 32 - W;
+    constexpr int UNR = 4;
+    if (r0 >= r1) return;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t cbase = smem_u32(sm.cnt) - (L::word(it.tile_lo) << 2);
+    volatile uint32_t* s_at = sm.scal + SC_AT;
+    const uint32_t* pp = sb.ppref();
+    // slice of this lane's first position: last si with ppref[si] <= r
+    uint32_t si;
+    {
+        const uint32_t r = min(r0 + lane, r1 - 1);
+        uint32_t lo = 0, hi = nsb;
+        while (lo < hi) {
+            const uint32_t m = (lo + hi) >> 1;
+            if (pp[m] <= r) lo = m + 1;
+            else hi = m;
+        }
+        si = lo - 1;
+    }
+    uint32_t gate = 0;
+    if constexpr (GATE) gate = (*s_at - 1) << kTop;
+    for (uint32_t base = r0; base < r1; base += 32 * UNR) {
+        uint32_t x[UNR];
+        uint32_t ok = 0;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t r = base + u * 32 + lane;
+            x[u] = 0;
+            if (r < r1) {
+                while (pp[si + 1] <= r) ++si;  // the slices ahead (empty ones skipped)
+                x[u] = __ldg(postings + sb.beg()[si] + (r - pp[si]));
+                ok |= 1u << u;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            if (!((ok >> u) & 1u)) continue;
+            const uint32_t r = ((~L::lane(x[u])) & (kPer - 1)) * W;
+            const uint32_t old = atom_add_shared(cbase + (L::word(x[u]) << 2), (1u << kTop) >> r);
+            if constexpr (GATE) {
+                if ((old << r) >= gate) {
+                    gate = cpq_admit<W>(sm.ht, sm.za, sm.scal, it.ht_cap, it.bound, it.kq, x[u] - it.tile_lo, old,
+                                        kTop - r);
+                }
+                gate = (*s_at - 1) << kTop;
+            }
+        }
+    }
+}
+
 // One warp's share [g0, g1) of the staged slices' 128-posting groups.
 template <int W, bool IL>
 __device__ __forceinline__ void scan_group_range(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
@@ -1198,11 +1264,18 @@ __device__ __forceinline__ void scan_group_range(const BatchParams& p, const Ite
 // end-of-tile barrier together).
 template <int W, bool IL>
 __device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb,
-                            uint32_t nsb, uint32_t G, uint32_t unit, uint32_t wfirst) {
+                            uint32_t nsb, uint32_t G, uint32_t unit, uint32_t wfirst, uint32_t ptot = 0) {
     // warps [wfirst, nwarps) scan
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (threadIdx.x >> 5) - wfirst;
     const uint32_t nwarps = (blockDim.x >> 5) - wfirst;
+    if (ptot && uint64_t(ptot) * kCompactFillInv < uint64_t(G) * 128) {  // short slices: compact mode
+        const uint32_t r0 = static_cast<uint32_t>(uint64_t(ptot) * warp / nwarps);
+        const uint32_t r1 = static_cast<uint32_t>(uint64_t(ptot) * (warp + 1) / nwarps);
+        if (it.gate) scan_compact<W, true, IL>(p.postings, it, sm, sb, nsb, r0, r1);
+        else scan_compact<W, false, IL>(p.postings, it, sm, sb, nsb, r0, r1);
+        return;
+    }
     if (G <= kStaticGroups * nwarps) {
 #if GENIE_SCAN_STRIDED
         // round-robin groups: every warp's share mixes hot (L2) and cold lists
@@ -1268,7 +1341,7 @@ __device__ __forceinline__ void stage_one(const BatchParams& p, const StageArgs&
 __device__ __forceinline__ uint32_t stage_warp(const BatchParams& p, const StageArgs& a, const StageBuf& sb,
                                                uint32_t t, uint32_t s0, uint32_t nsb) {
     const uint32_t lane = threadIdx.x & 31;
-    uint32_t carry = 0, dcarry = 0;
+    uint32_t carry = 0, dcarry = 0, pcarry = 0;
     for (uint32_t c0 = 0; c0 < nsb; c0 += 32) {
         const uint32_t i = c0 + lane;
         uint64_t beg = 0;
@@ -1279,16 +1352,19 @@ __device__ __forceinline__ uint32_t stage_warp(const BatchParams& p, const Stage
             groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
         }
         const uint32_t incl = warp_inclusive_scan(groups);
+        const uint32_t pincl = warp_inclusive_scan(len);
         const uint32_t dm = __ballot_sync(0xffffffffu, dslot >= 0);
         if (i < nsb) {
             sb.beg()[i] = beg;
-            sb.len()[i] = len;
             sb.upref()[i] = carry + incl - groups;
+            sb.ppref()[i] = pcarry + pincl - len;
             if (dslot >= 0) sb.dense()[dcarry + __popc(dm & ((1u << lane) - 1u))] = static_cast<uint32_t>(dslot);
         }
         carry += __shfl_sync(0xffffffffu, incl, 31);
+        pcarry += __shfl_sync(0xffffffffu, pincl, 31);
         dcarry += __popc(dm);
     }
+    if (lane == 0) sb.ppref()[nsb] = pcarry;  // postings of the batch
     return carry;
 }
 
@@ -1303,13 +1379,16 @@ __device__ __forceinline__ uint32_t stage_block(const BatchParams& p, const Stag
         stage_one(p, a, t, s0 + threadIdx.x, beg, len, dslot);
         groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
     }
-    // one scan of (dense flag << 40 | groups): group ranks and dense slots
+    // one scan of (dense flag << 40 | groups): group ranks and dense slots;
+    // one of the lengths: posting prefix
     const unsigned long long v = (static_cast<unsigned long long>(dslot >= 0) << 40) | groups;
-    unsigned long long total;
+    unsigned long long total, ptotal;
     const unsigned long long ex = block_exclusive_scan<unsigned long long>(v, sm.sums, total);
+    const unsigned long long pex = block_exclusive_scan<unsigned long long>(len, sm.sums, ptotal);
+    if (threadIdx.x == 0) sb.ppref()[nsb] = static_cast<uint32_t>(ptotal);
     if (threadIdx.x < nsb) {
         sb.beg()[threadIdx.x] = beg;
-        sb.len()[threadIdx.x] = len;
+        sb.ppref()[threadIdx.x] = static_cast<uint32_t>(pex);
         sb.upref()[threadIdx.x] = static_cast<uint32_t>(ex & ((1ull << 40) - 1));
         if (dslot >= 0) sb.dense()[ex >> 40] = static_cast<uint32_t>(dslot);
     }
@@ -1340,7 +1419,7 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
 
 template <int W, bool IL>
 __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t b,
-                                uint32_t S, uint32_t nsb, uint32_t G, uint64_t total) {
+                                uint32_t S, uint32_t nsb, uint32_t G, uint32_t ptot, uint64_t total) {
     using L = Lay<W, IL>;
 #ifdef GENIE_PHASE_TIMERS
     const long long t_setup = clock64();
@@ -1351,7 +1430,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
         prepare_item(p, sm, b ^ 1u, total);
         if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_PREP], static_cast<unsigned long long>(clock64() - t_setup));
     } else {
-        scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1);
+        scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1, ptot);
         const uint32_t dt = static_cast<uint32_t>(clock64() - t_setup);
         if (threadIdx.x == 32) atomicAdd(&p.st[ST_T_WARP1], static_cast<unsigned long long>(dt));
         if ((threadIdx.x & 31) == 0) {
@@ -1361,7 +1440,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
     }
 #else
     if (threadIdx.x < 32) prepare_item(p, sm, b ^ 1u, total);
-    else scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1);
+    else scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1, ptot);
 #endif
     __syncthreads();
     for (uint32_t s0 = kSpanBatch; s0 < S; s0 += kSpanBatch) {  // long queries: further batches
@@ -1569,6 +1648,7 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         d->S = S;
         d->nd = sa.dense ? p.q_nd[q] : 0u;
         d->G = G;
+        d->ptot = sm.sb(buf).ppref()[min(kSpanBatch, S)];
         d->a0 = a0;
         d->out_base = p.q_out_base[q] + uint64_t(t) * cap;
         d->tile_slot = tbase + t;
@@ -1613,7 +1693,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
         it.ht_cap = min(kHtMaxSlots, 1u << (31 - __clz(room)));
         sm.ht = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sm.cnt) + cnt_bytes);
     }
-    const uint32_t S = d.S, nd = d.nd, G = d.G;
+    const uint32_t S = d.S, nd = d.nd, G = d.G, ptot = d.ptot;
     const uint32_t nsb = min(kSpanBatch, S);
 
     // setup (cpq.hpp:281-292): empty table and ZA, AT at the gate start
@@ -1666,9 +1746,9 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
             atomicAdd(&p.st[ST_T_LATN], static_cast<unsigned long long>(t_db - t_d));
         }
 #endif
-        scan_and_select<W, true>(p, it, sm, b, S, nsb, G, total);
+        scan_and_select<W, true>(p, it, sm, b, S, nsb, G, ptot, total);
     } else {
-        scan_and_select<W, false>(p, it, sm, b, S, nsb, G, total);
+        scan_and_select<W, false>(p, it, sm, b, S, nsb, G, ptot, total);
     }
 }
 
