@@ -350,7 +350,6 @@ struct ScanSmem {
     uint64_t* ht;              // Robin Hood table / histogram scratch
     uint32_t* za;              // ZipperArray, levels [0, bound]
     unsigned long long* sums;  // block scan scratch (32)
-    uint32_t* ehist;           // [kHistBins] counts of this item's emitted entries
     uint32_t* scal;            // scalars
     ItemDesc* desc;            // [2]
     uint8_t* stage;            // 2 x StageBuf
@@ -375,7 +374,6 @@ enum ScalarSlot {
     SC_PF_Q = 14,
     SC_PF_T = 15,
     SC_LVL = 16,     // 8 dense-phase level counts
-    SC_BASE = 23,       // base level of the tile's record
     SC_ADM_CALLS = 24,  // instrumented builds only
     SC_ADM_PASS = 25,
     SC_WMAX = 26,       // instrumented builds: slowest / fastest scan warp of the item
@@ -389,8 +387,7 @@ constexpr uint32_t kScal = 0;                                  // SC_WORDS u32 (
 constexpr uint32_t kSums = 128;                                // 32 u64
 constexpr uint32_t kDesc = kSums + 256;                        // 2 x ItemDesc
 constexpr uint32_t kZa = kDesc + 2 * sizeof(ItemDesc);         // kZaMax u32
-constexpr uint32_t kEhist = kZa + kZaMax * 4;                  // kHistBins u32
-constexpr uint32_t kStage = kEhist + kHistBins * 4;            // 2 x StageBuf
+constexpr uint32_t kStage = kZa + kZaMax * 4;                  // 2 x StageBuf
 constexpr uint32_t kStageBytes = kSpanBatch * (8 + 4 + 4 + 4) + 16;
 constexpr uint32_t kHt = kStage + 2 * kStageBytes;             // ht_slots u64, then the tile
 static_assert(kHt % 16 == 0, "16-byte aligned table");
@@ -403,7 +400,6 @@ __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t ht_slots) {
     s.sums = reinterpret_cast<unsigned long long*>(base + kSums);
     s.desc = reinterpret_cast<ItemDesc*>(base + kDesc);
     s.za = reinterpret_cast<uint32_t*>(base + kZa);
-    s.ehist = reinterpret_cast<uint32_t*>(base + kEhist);
     s.stage = base + kStage;
     static_assert(kStageBytes == kSpanBatch * 20 + 16, "stage buffer layout");
     s.cnt = reinterpret_cast<uint32_t*>(base + kHt);
@@ -539,6 +535,7 @@ struct Swar {
 
 struct ItemCtx {
     uint32_t q, t, kq, bound, tile_lo, tile_n, words, ht_cap, cap, slot;
+    uint32_t rec_b;  // base level of the tile's record (every emitted entry counts >= rec_b)
     uint64_t out_base;
     bool gate;
 };
@@ -587,7 +584,12 @@ __device__ __forceinline__ uint32_t atom_add_shared(uint32_t addr, uint32_t v) {
 __device__ __forceinline__ void emit(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
                                      uint32_t local, uint32_t count) {
     const uint32_t pos = atomicAdd(&sm.scal[SC_NOUT], 1u);
-    if (it.gate) atomicAdd(&sm.ehist[count], 1u);  // count <= bound < kHistBins (W <= 8)
+    if (it.gate) {  // the tile's record: #emitted entries counting >= rec_b + j
+        uint32_t* rec = p.tile_rec + uint64_t(it.slot) * kRecWords;
+#pragma unroll
+        for (int j = 0; j < kRecLevels; ++j)
+            if (count >= it.rec_b + j) atomicAdd(rec + 1 + j, 1u);
+    }
     genie_entry e;
     e.id = local + it.tile_lo;
     e.count = count;
@@ -681,7 +683,8 @@ __device__ void emit_ties(const BatchParams& p, const ItemCtx& it, const ScanSme
 // tile, zeros included (0 if fewer than k non-zero), then every count > T
 // and the first ties at T in ascending id.
 template <int W, bool IL>
-__device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm) {
+__device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it0, const ScanSmem& sm) {
+    ItemCtx it = it0;  // rec_b is set once T is known
     using L = Lay<W, IL>;
     constexpr uint32_t kPer = 32 / W;
     const int nsub = static_cast<int>(it.ht_cap * 8 / 1024);  // 256-bin sub-histograms in the table's space
@@ -758,6 +761,8 @@ __device__ uint32_t hist_select(const BatchParams& p, const ItemCtx& it, const S
         T = (W == 16) ? ((hi_sel << 8) | sel) : sel;
         above = static_cast<uint32_t>(cum);
     }
+    it.rec_b = max(T, 1u);
+    if (it.gate && threadIdx.x == 0) p.tile_rec[uint64_t(it.slot) * kRecWords] = it.rec_b;
     // emit: every count > T, then ties at T (T > 0) in ascending id; one
     // 32-object block per thread per step (both layouts keep a block in W
     // consecutive words)
@@ -1465,6 +1470,13 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
         uint32_t a = sm.scal[SC_AT];  // every thread finishes AT (cpq.hpp:383-389)
         while (a <= it.bound && sm.za[a] >= it.kq) ++a;
         const uint32_t thr = a - 1;  // cpq.hpp:310-311
+        const uint32_t floor = sm.scal[SC_FLOOR];
+        // The tile's record for the later tiles of its query (gate_start):
+        // base level b and, counted by emit(), n[j] = #emitted entries
+        // counting >= b + j (any prefix of those adds is a valid under-count)
+        ItemCtx itr = it;
+        itr.rec_b = max((thr > 0 && thr >= floor) ? thr : floor, 1u);
+        if (threadIdx.x == 0) p.tile_rec[uint64_t(it.slot) * kRecWords] = itr.rec_b;
         // table entries above the threshold (all touched ids when thr == 0);
         // an id may own a stale slot -- only the slot holding its final
         // count is reported (cpq.hpp:212-222, 391-406)
@@ -1478,12 +1490,11 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
                 if (w == kEmptySlot) continue;
                 const uint32_t id = uint32_t(w >> 32), v = uint32_t(w >> 16) & 0xffffu;
                 const uint32_t c = L::get(sm.cnt, id);
-                if (v == c && c > thr) emit(p, it, sm, id, c);
+                if (v == c && c > thr) emit(p, itr, sm, id, c);
             }
         }
         __syncthreads();
         const uint32_t n_above = sm.scal[SC_NOUT];
-        const uint32_t floor = sm.scal[SC_FLOOR];
         // thr >= floor: thr is the tile's true k-th count -> tie fill and
         // publish it as the query's new floor.  thr < floor (AT never left
         // the floor): fewer than k objects reach the floor here; they are all
@@ -1491,52 +1502,23 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
         if (thr > 0 && thr >= floor) {
 #ifdef GENIE_PHASE_TIMERS
             const long long tt0 = clock64();
-            if (n_above < it.kq) emit_ties<W, IL>(p, it, sm, thr, it.kq - n_above);
+            if (n_above < it.kq) emit_ties<W, IL>(p, itr, sm, thr, it.kq - n_above);
             if (threadIdx.x == 0) {
                 atomicAdd(&p.st[ST_T_GATE], 1ull);
                 atomicAdd(&p.st[ST_T_STAGE], static_cast<unsigned long long>(clock64() - tt0));
             }
 #else
-            if (n_above < it.kq) emit_ties<W, IL>(p, it, sm, thr, it.kq - n_above);
+            if (n_above < it.kq) emit_ties<W, IL>(p, itr, sm, thr, it.kq - n_above);
 #endif
-            if (threadIdx.x == 0) {
-                atomicMax(&p.q_floor[it.q], thr);
-                sm.scal[SC_BASE] = thr;
-            }
-        } else if (threadIdx.x == 0) {
-            sm.scal[SC_BASE] = floor;
+            if (threadIdx.x == 0) atomicMax(&p.q_floor[it.q], thr);
         }
     } else {
         if (it.gate && threadIdx.x == 0) atomicAdd(&p.st[ST_FALLBACK], 1ull);
         const uint32_t T_t = hist_select<W, IL>(p, it, sm);
         if (it.gate && T_t > 0 && threadIdx.x == 0) atomicMax(&p.q_floor[it.q], T_t);
-        if (threadIdx.x == 0) sm.scal[SC_BASE] = T_t;
     }
     __syncthreads();
     if (threadIdx.x == 0) p.tile_len[it.slot] = sm.scal[SC_NOUT];
-    if (it.gate && threadIdx.x < 32) {
-        // the tile's record for the later tiles of its query (gate_start):
-        // base level b (every emitted entry counts >= b) and n[j] = #emitted
-        // entries counting >= b + j, j < kRecLevels
-        const uint32_t lane = threadIdx.x;
-        const uint32_t b = max(sm.scal[SC_BASE], 1u);
-        uint32_t top = 0;  // entries counting >= b + kRecLevels
-        for (uint32_t c = b + kRecLevels + lane; c <= it.bound; c += 32) top += sm.ehist[c];
-        top = warp_sum(top);
-        uint32_t* rec = p.tile_rec + uint64_t(it.slot) * kRecWords;
-        if (lane == 0) {
-            uint32_t n = top;
-            for (int j = kRecLevels - 1; j >= 0; --j) {
-                const uint32_t c = b + j;
-                n += c <= it.bound ? sm.ehist[c] : 0u;
-                rec[1 + j] = n;
-            }
-            rec[0] = b;
-        }
-        __syncwarp();
-        for (uint32_t c = b + lane; c <= it.bound; c += 32) sm.ehist[c] = 0;
-        for (uint32_t c = lane; c < b && c <= it.bound; c += 32) sm.ehist[c] = 0;
-    }
 #ifdef GENIE_PHASE_TIMERS
     if (threadIdx.x == 0) {
         const long long t_end = clock64();
@@ -1771,7 +1753,6 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     }
     __syncwarp();
     if (threadIdx.x < 32) prepare_item(p, sm, 0, total);
-    for (uint32_t i = threadIdx.x; i < kHistBins; i += blockDim.x) sm.ehist[i] = 0;
     if (threadIdx.x == 0) {
         sm.scal[SC_ADM_CALLS] = 0;
         sm.scal[SC_ADM_PASS] = 0;
