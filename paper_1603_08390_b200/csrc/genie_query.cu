@@ -378,7 +378,8 @@ enum ScalarSlot {
     SC_ADM_PASS = 25,
     SC_WMAX = 26,       // instrumented builds: slowest / fastest scan warp of the item
     SC_WMIN = 27,
-    SC_WORDS = 28
+    SC_PF1 = 28,        // second set of the SC_PF_* slots (item, query, tile), by buffer parity
+    SC_WORDS = 31
 };
 static_assert(SC_WORDS <= 32, "scalar area");
 
@@ -1421,6 +1422,8 @@ __device__ __forceinline__ StageArgs stage_args(const BatchParams& p, uint32_t q
 }
 
 __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint64_t total);
+__device__ void prepare_gate(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint32_t item, uint32_t q,
+                             uint32_t t);
 
 template <int W, bool IL>
 __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t b,
@@ -1430,12 +1433,21 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
     const long long t_setup = clock64();
 #endif
     // warps 1.. scan this item's postings while warp 0 prepares the next item
+#if GENIE_GATE_WARP1
+    constexpr uint32_t kScanWarp0 = 2;  // warp 0 prepares, warp 1 computes the gate start
+    if (threadIdx.x >= 32 && threadIdx.x < 64) {
+        const uint32_t pf = (b ^ 1u) ? SC_PF1 : SC_PF_ITEM;
+        prepare_gate(p, sm, b ^ 1u, sm.scal[pf], sm.scal[pf + 1], sm.scal[pf + 2]);
+    } else
+#else
+    constexpr uint32_t kScanWarp0 = 1;
+#endif
 #ifdef GENIE_PHASE_TIMERS
     if (threadIdx.x < 32) {
         prepare_item(p, sm, b ^ 1u, total);
         if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_PREP], static_cast<unsigned long long>(clock64() - t_setup));
     } else {
-        scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1, ptot);
+        scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, kScanWarp0, ptot);
         const uint32_t dt = static_cast<uint32_t>(clock64() - t_setup);
         if (threadIdx.x == 32) atomicAdd(&p.st[ST_T_WARP1], static_cast<unsigned long long>(dt));
         if ((threadIdx.x & 31) == 0) {
@@ -1445,7 +1457,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
     }
 #else
     if (threadIdx.x < 32) prepare_item(p, sm, b ^ 1u, total);
-    else scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, 1, ptot);
+    else scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, kScanWarp0, ptot);
 #endif
     __syncthreads();
     for (uint32_t s0 = kSpanBatch; s0 < S; s0 += kSpanBatch) {  // long queries: further batches
@@ -1594,13 +1606,15 @@ __device__ __forceinline__ uint32_t fetch_item(const BatchParams& p, uint64_t to
 __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint64_t total) {
     const uint32_t lane = threadIdx.x & 31;
     ItemDesc* d = sm.desc + buf;
-    // the item was claimed (and its query / tile read) by the previous call
-    const uint32_t item = sm.scal[SC_PF_ITEM];
+    // the item was claimed (and its query / tile read) by the previous call,
+    // into the slot set of this buffer; this call's claim goes to the other
+    const uint32_t pf = buf ? SC_PF1 : SC_PF_ITEM, pf_next = buf ? SC_PF_ITEM : SC_PF1;
+    const uint32_t item = sm.scal[pf];
     if (item == 0xffffffffu) {
         if (lane == 0) d->valid = 0;
         return;
     }
-    const uint32_t q = sm.scal[SC_PF_Q], t = sm.scal[SC_PF_T];
+    const uint32_t q = sm.scal[pf + 1], t = sm.scal[pf + 2];
     // claim the one after it now (consumed at the end)
     uint32_t nitem = 0xffffffffu;
     if (lane == 0) nitem = fetch_item(p, total);
@@ -1610,16 +1624,23 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     const uint32_t kq = p.k[q];
     const uint32_t bound = static_cast<uint32_t>(p.q_bound[q] < 1 ? 1 : p.q_bound[q]);
     const uint32_t tbase = p.q_tile_base[q];
+    const uint32_t cap = p.q_cap[q];
+    const uint32_t ndq = p.q_nd[q];
+    const uint64_t obase = p.q_out_base[q];
+#if GENIE_GATE_WARP1
+    // warp 1 computes the gate start meanwhile (prepare_gate)
+    const uint32_t G = stage_warp(p, sa, sm.sb(buf), t, 0, min(kSpanBatch, S));
+#else
     const bool gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
     const uint32_t a0 = gate ? gate_start(p, q, t, kq, bound, tbase) : 0u;
     const uint32_t G = stage_warp(p, sa, sm.sb(buf), t, 0, min(kSpanBatch, S));
+#endif
     uint32_t nq = 0, ntile = 0;
     if (nitem != 0xffffffffu) {
         nq = p.work_q[nitem];
         ntile = p.work_t[nitem];
     }
     if (lane == 0) {
-        const uint32_t cap = p.q_cap[q];
         d->q = q;
         d->t = t;
         d->kq = kq;
@@ -1628,17 +1649,34 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         d->cap = cap;
         d->nt = sa.nt;
         d->S = S;
-        d->nd = sa.dense ? p.q_nd[q] : 0u;
+        d->nd = sa.dense ? ndq : 0u;
         d->G = G;
         d->ptot = sm.sb(buf).ppref()[min(kSpanBatch, S)];
+#if !GENIE_GATE_WARP1
         d->a0 = a0;
-        d->out_base = p.q_out_base[q] + uint64_t(t) * cap;
+#endif
+        d->out_base = obase + uint64_t(t) * cap;
         d->tile_slot = tbase + t;
         d->valid = 1;
-        sm.scal[SC_PF_ITEM] = nitem;
-        sm.scal[SC_PF_Q] = nq;
-        sm.scal[SC_PF_T] = ntile;
+        sm.scal[pf_next] = nitem;
+        sm.scal[pf_next + 1] = nq;
+        sm.scal[pf_next + 2] = ntile;
     }
+}
+
+// Warp 1: the gate start of the item warp 0 is preparing (same claimed item,
+// read from the prefetch slots before warp 0 moves them on).
+__device__ void prepare_gate(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint32_t item, uint32_t q,
+                             uint32_t t) {
+    if (item == 0xffffffffu) return;
+    const uint32_t W = p.q_W[q];
+    const bool gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
+    uint32_t a0 = 0;
+    if (gate) {
+        const uint64_t qb = p.q_bound[q];
+        a0 = gate_start(p, q, t, p.k[q], static_cast<uint32_t>(qb < 1 ? 1 : qb), p.q_tile_base[q]);
+    }
+    if ((threadIdx.x & 31) == 0) sm.desc[buf].a0 = a0;
 }
 
 template <int W>
@@ -1751,7 +1789,11 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
             sm.scal[SC_PF_T] = p.work_t[i0];
         }
     }
-    __syncwarp();
+    __syncthreads();
+#if GENIE_GATE_WARP1
+    if (threadIdx.x >= 32 && threadIdx.x < 64)
+        prepare_gate(p, sm, 0, sm.scal[SC_PF_ITEM], sm.scal[SC_PF_ITEM + 1], sm.scal[SC_PF_ITEM + 2]);
+#endif
     if (threadIdx.x < 32) prepare_item(p, sm, 0, total);
     if (threadIdx.x == 0) {
         sm.scal[SC_ADM_CALLS] = 0;
