@@ -357,23 +357,16 @@ struct ScanSmem {
 };
 
 enum ScalarSlot {
-    SC_ITEM = 0,
-    SC_AT = 1,
-    SC_OVF = 2,
-    SC_NOUT = 3,
-    SC_UCTR = 4,
-    SC_U = 5,
-    SC_TIES = 6,
-    SC_T = 7,
-    SC_ABOVE = 8,
-    SC_DONE = 9,
-    SC_FLOOR = 10,
-    SC_NDENSE = 11,
-    SC_G = 12,       // groups of the first staged batch
-    SC_PF_ITEM = 13, // next work item claimed ahead by prepare_item, its query and tile
+    SC_AT = 1,          // live AuditThreshold
+    SC_OVF = 2,         // table overflow -> histogram fallback
+    SC_NOUT = 3,        // entries emitted by the item
+    SC_UCTR = 4,        // guided-scheduling cursor
+    SC_T = 7,           // hist_select scratch
+    SC_FLOOR = 10,      // gate start of the item
+    SC_PF_ITEM = 13,    // next work item claimed ahead by prepare_item, its query and tile
     SC_PF_Q = 14,
     SC_PF_T = 15,
-    SC_LVL = 16,     // 8 dense-phase level counts
+    SC_LVL = 16,        // dense-phase level counts (kLvl <= 8)
     SC_ADM_CALLS = 24,  // instrumented builds only
     SC_ADM_PASS = 25,
     SC_WMAX = 26,       // instrumented builds: slowest / fastest scan warp of the item

@@ -21,7 +21,6 @@ constexpr uint32_t kScanCtasPerSm = GENIE_SCAN_CTAS;   // resident scan CTAs per
 constexpr uint32_t kSpanBatch = 256;          // spans staged in shared memory per pass (x2 buffers)
 constexpr uint32_t kHtSlots = 1024;           // shared-memory Robin Hood table, minimum (8 KB; >= 4 x 256-bin histograms)
 constexpr uint32_t kHtMaxSlots = 4096;        // ... and maximum (items whose counters leave room)
-constexpr uint32_t kHistBins = 256;           // emitted-count histogram of a gated tile (counts <= 255)
 constexpr int kRecLevels = 4;                 // levels in a tile's record (gate_start)
 constexpr uint32_t kRecWords = 8;             // record: base level + kRecLevels counts, padded to 16 B
 constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shared memory (W <= 8)
