@@ -817,6 +817,92 @@ __device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const Sc
     if constexpr (W <= 8) {
         if (nd >= 2 * W) {
             csa_path = true;
+#if GENIE_CSA_PAIR
+          if constexpr (W == 8) {
+            // two consecutive blocks per thread: one 8-byte bitmap load per list
+            const uint32_t bwq = p.bitmap_words / 2;
+            for (uint32_t blk = 2 * threadIdx.x; blk < nblk; blk += 2 * blockDim.x) {
+                const uint2* col = reinterpret_cast<const uint2*>(p.bitmaps + bw0 + blk);
+                uint32_t P[2][W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) P[0][i] = P[1][i] = 0;
+                uint32_t d = 0;
+                for (; d + 8 <= nd; d += 8) {
+                    uint2 a[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a[u] = __ldg(col + size_t(sb.dense()[d + u]) * bwq);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t x[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) x[u] = h ? a[u].y : a[u].x;
+                        uint32_t twosA, twosB, foursA, foursB, eights;
+                        csa(twosA, P[h][0], P[h][0], x[0], x[1]);
+                        csa(twosB, P[h][0], P[h][0], x[2], x[3]);
+                        csa(foursA, P[h][1], P[h][1], twosA, twosB);
+                        csa(twosA, P[h][0], P[h][0], x[4], x[5]);
+                        csa(twosB, P[h][0], P[h][0], x[6], x[7]);
+                        csa(foursB, P[h][1], P[h][1], twosA, twosB);
+                        csa(eights, P[h][2], P[h][2], foursA, foursB);
+                        uint32_t c = eights;
+#pragma unroll
+                        for (int i = 3; i < W; ++i) {
+                            const uint32_t t = P[h][i] & c;
+                            P[h][i] ^= c;
+                            c = t;
+                        }
+                    }
+                }
+                for (; d < nd; ++d) {
+                    const uint2 a = __ldg(col + size_t(sb.dense()[d]) * bwq);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t c = h ? a.y : a.x;
+#pragma unroll
+                        for (int i = 0; i < W; ++i) {
+                            const uint32_t t = P[h][i] & c;
+                            P[h][i] ^= c;
+                            c = t;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (blk + h >= nblk) break;
+                    if (nlv) {
+#pragma unroll
+                        for (uint32_t l = 0; l < kLvl; ++l) {
+                            if (l < nlv) {
+                                const uint32_t v = at0 + l;
+                                uint32_t ge = 0, eq = 0xffffffffu;
+#pragma unroll
+                                for (int i = W - 1; i >= 0; --i) {
+                                    if ((v >> i) & 1u) {
+                                        eq &= P[h][i];
+                                    } else {
+                                        ge |= eq & P[h][i];
+                                        eq &= ~P[h][i];
+                                    }
+                                }
+                                lv[l] += __popc(ge | eq);
+                            }
+                        }
+                    }
+                    uint32_t acc[W];
+#pragma unroll
+                    for (int m = 0; m < W; ++m) {
+                        uint32_t x = 0;
+#pragma unroll
+                        for (int i = 0; i < W; ++i) x |= ((P[h][i] >> m) & Sw::kOnes) << i;
+                        acc[m] = x;
+                    }
+                    uint4* dst = reinterpret_cast<uint4*>(sm.cnt + (blk + h) * W);
+#pragma unroll
+                    for (int j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                }
+            }
+          } else
+#endif
             for (uint32_t blk = threadIdx.x; blk < nblk; blk += blockDim.x) {
                 const uint32_t* col = p.bitmaps + bw0 + blk;
                 uint32_t P[W];  // bit planes of the dense count (< 2^W: it is at most the bound)
@@ -1052,12 +1138,14 @@ __device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, 
         // blocks of this thread: csa path blk = tid + k * blockDim; lane-wise
         // path blk = (warp + k * nwarps) * 32 * BPT + lane + 32 i
         const uint32_t lane = threadIdx.x & 31;
-        const uint32_t first = csa_path ? threadIdx.x : (threadIdx.x >> 5) * 32 * BPT + lane;
-        const uint32_t stride = csa_path ? blockDim.x : (blockDim.x >> 5) * 32 * BPT;
-        const uint32_t per = csa_path ? 1u : BPT;
+        const bool pair = GENIE_CSA_PAIR && csa_path && W == 8;
+        const uint32_t first = pair ? 2 * threadIdx.x : (csa_path ? threadIdx.x : (threadIdx.x >> 5) * 32 * BPT + lane);
+        const uint32_t stride = pair ? 2 * blockDim.x : (csa_path ? blockDim.x : (blockDim.x >> 5) * 32 * BPT);
+        const uint32_t per = pair ? 2u : (csa_path ? 1u : BPT);
+        const uint32_t step = pair ? 1u : 32u;
         for (uint32_t b0 = first; b0 < nblk; b0 += stride) {
-            for (uint32_t i = 0; i < per && b0 + 32 * i < nblk; ++i) {
-                const uint32_t blk = b0 + 32 * i;
+            for (uint32_t i = 0; i < per && b0 + step * i < nblk; ++i) {
+                const uint32_t blk = b0 + step * i;
                 for (uint32_t wi = blk * W; wi < blk * W + W; ++wi) {
                     const uint32_t x = sm.cnt[wi];
                     uint32_t m = Sw::ge(x, a);

@@ -45,6 +45,9 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #ifndef GENIE_GATE_WARP1
 #define GENIE_GATE_WARP1 0
 #endif
+#ifndef GENIE_CSA_PAIR
+#define GENIE_CSA_PAIR 1
+#endif
 constexpr int kScanUnroll = GENIE_SCAN_UNROLL;               // 128-posting groups loaded per warp pass
 constexpr uint32_t kStaticGroups = 64;        // <= this many 128-posting groups per warp: static split
 constexpr uint64_t kEmptySlot = ~0ull;
