@@ -817,7 +817,88 @@ __device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const Sc
     if constexpr (W <= 8) {
         if (nd >= 2 * W) {
             csa_path = true;
-#if GENIE_CSA_PAIR
+#if GENIE_CSA_QUAD
+          if constexpr (W == 8) {
+            // four consecutive blocks per thread: one 16-byte bitmap load per list
+            const uint32_t bwq = p.bitmap_words / 4;
+            for (uint32_t blk = 4 * threadIdx.x; blk < nblk; blk += 4 * blockDim.x) {
+                const uint4* col = reinterpret_cast<const uint4*>(p.bitmaps + bw0 + blk);
+                uint32_t P[4][W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) P[0][i] = P[1][i] = P[2][i] = P[3][i] = 0;
+                uint32_t d = 0;
+                for (; d + 4 <= nd; d += 4) {
+                    uint4 a[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) a[u] = __ldg(col + size_t(sb.dense()[d + u]) * bwq);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        uint32_t x[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) x[u] = h == 0 ? a[u].x : (h == 1 ? a[u].y : (h == 2 ? a[u].z : a[u].w));
+                        uint32_t twosA, twosB, fours;
+                        csa(twosA, P[h][0], P[h][0], x[0], x[1]);
+                        csa(twosB, P[h][0], P[h][0], x[2], x[3]);
+                        csa(fours, P[h][1], P[h][1], twosA, twosB);
+                        uint32_t c = fours;
+#pragma unroll
+                        for (int i = 2; i < W; ++i) {
+                            const uint32_t t = P[h][i] & c;
+                            P[h][i] ^= c;
+                            c = t;
+                        }
+                    }
+                }
+                for (; d < nd; ++d) {
+                    const uint4 a = __ldg(col + size_t(sb.dense()[d]) * bwq);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        uint32_t c = h == 0 ? a.x : (h == 1 ? a.y : (h == 2 ? a.z : a.w));
+#pragma unroll
+                        for (int i = 0; i < W; ++i) {
+                            const uint32_t t = P[h][i] & c;
+                            P[h][i] ^= c;
+                            c = t;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    if (blk + h >= nblk) break;
+                    if (nlv) {
+#pragma unroll
+                        for (uint32_t l = 0; l < kLvl; ++l) {
+                            if (l < nlv) {
+                                const uint32_t v = at0 + l;
+                                uint32_t ge = 0, eq = 0xffffffffu;
+#pragma unroll
+                                for (int i = W - 1; i >= 0; --i) {
+                                    if ((v >> i) & 1u) {
+                                        eq &= P[h][i];
+                                    } else {
+                                        ge |= eq & P[h][i];
+                                        eq &= ~P[h][i];
+                                    }
+                                }
+                                lv[l] += __popc(ge | eq);
+                            }
+                        }
+                    }
+                    uint32_t acc[W];
+#pragma unroll
+                    for (int m = 0; m < W; ++m) {
+                        uint32_t x = 0;
+#pragma unroll
+                        for (int i = 0; i < W; ++i) x |= ((P[h][i] >> m) & Sw::kOnes) << i;
+                        acc[m] = x;
+                    }
+                    uint4* dst = reinterpret_cast<uint4*>(sm.cnt + (blk + h) * W);
+#pragma unroll
+                    for (int j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                }
+            }
+          } else
+#elif GENIE_CSA_PAIR
           if constexpr (W == 8) {
             // two consecutive blocks per thread: one 8-byte bitmap load per list
             const uint32_t bwq = p.bitmap_words / 2;
@@ -1138,10 +1219,11 @@ __device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, 
         // blocks of this thread: csa path blk = tid + k * blockDim; lane-wise
         // path blk = (warp + k * nwarps) * 32 * BPT + lane + 32 i
         const uint32_t lane = threadIdx.x & 31;
-        const bool pair = GENIE_CSA_PAIR && csa_path && W == 8;
-        const uint32_t first = pair ? 2 * threadIdx.x : (csa_path ? threadIdx.x : (threadIdx.x >> 5) * 32 * BPT + lane);
-        const uint32_t stride = pair ? 2 * blockDim.x : (csa_path ? blockDim.x : (blockDim.x >> 5) * 32 * BPT);
-        const uint32_t per = pair ? 2u : (csa_path ? 1u : BPT);
+        constexpr uint32_t kGrp = GENIE_CSA_QUAD ? 4u : (GENIE_CSA_PAIR ? 2u : 1u);  // csa blocks per thread
+        const bool pair = kGrp > 1 && csa_path && W == 8;
+        const uint32_t first = pair ? kGrp * threadIdx.x : (csa_path ? threadIdx.x : (threadIdx.x >> 5) * 32 * BPT + lane);
+        const uint32_t stride = pair ? kGrp * blockDim.x : (csa_path ? blockDim.x : (blockDim.x >> 5) * 32 * BPT);
+        const uint32_t per = pair ? kGrp : (csa_path ? 1u : BPT);
         const uint32_t step = pair ? 1u : 32u;
         for (uint32_t b0 = first; b0 < nblk; b0 += stride) {
             for (uint32_t i = 0; i < per && b0 + step * i < nblk; ++i) {
@@ -2339,7 +2421,7 @@ static uint32_t auto_tile_bytes() {
 static uint32_t tile_bits_of(const genie_config& cfg) {
     uint32_t tb = cfg.tile_bytes ? cfg.tile_bytes : auto_tile_bytes();
     tb = std::max<uint32_t>(4096, std::min<uint32_t>(tb, 160u << 10));
-    tb &= ~63u;  // tiles of whole 32-object blocks in 16-byte bitmap steps for every W
+    tb &= ~127u;  // tiles of whole 32-object blocks in 16-byte bitmap steps for every W
     return tb * 8;
 }
 

@@ -45,6 +45,9 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #ifndef GENIE_GATE_WARP1
 #define GENIE_GATE_WARP1 0
 #endif
+#ifndef GENIE_CSA_QUAD
+#define GENIE_CSA_QUAD 0
+#endif
 #ifndef GENIE_CSA_PAIR
 #define GENIE_CSA_PAIR 1
 #endif
