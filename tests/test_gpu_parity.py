@@ -276,3 +276,40 @@ def test_tie_heavy_many_tiles(gpu, oracle, seed, monkeypatch):
             for rep in range(2):  # concurrent tiles finish in a different order each run
                 assert_same(ix.query(ds.queries, config(tile_bytes=tb)), want,
                             f"seed {seed} density {density} tile {tb} rep {rep}")
+
+
+@pytest.mark.parametrize("tile_bytes", [4096, 16384, 0])
+def test_many_spans_per_query(gpu, oracle, tile_bytes):
+    # Range items over a dim of 1500 tokens: a query resolves to up to ~1200
+    # keyword lists, more than one staging batch (256 spans), so the further
+    # batches are staged block-wide; short lists also select the compact
+    # (one id per lane) scan.  Multi-tile at the small tile sizes.
+    rng = np.random.default_rng(77)
+    n, ntok = 30_000, 1500
+    kw = rng.integers(1, 4, size=n)
+    off = np.concatenate([[0], np.cumsum(kw)]).astype(np.uint64)
+    dims = rng.integers(0, 2, size=int(off[-1])).astype(np.uint16)
+    toks = rng.integers(0, ntok, size=int(off[-1])).astype(np.uint32)
+    # one keyword per (object, dim): drop duplicates by making dim 1 tokens distinct per object
+    for i in range(n):
+        a, b = int(off[i]), int(off[i + 1])
+        dims[a:b] = np.arange(b - a) % 2
+        if b - a == 3:
+            dims[b - 1] = 2
+    csr = synth.csr_from_objects(n, off, dims, toks)
+    Q = 12
+    qdim, qlo, qhi, qoff = [], [], [], [0]
+    for q in range(Q):
+        for _ in range(1 + q % 3):
+            lo = int(rng.integers(0, ntok // 2))
+            qdim.append(int(rng.integers(0, 2)))
+            qlo.append(lo)
+            qhi.append(min(ntok - 1, lo + int(rng.integers(200, 700))))
+        qoff.append(len(qdim))
+    qb = QueryBatch(np.arange(Q, dtype=np.uint32), np.array([1 + 37 * q for q in range(Q)], np.uint32),
+                    np.array(qoff, np.uint64), np.array(qdim, np.uint16), np.array(qlo, np.uint32),
+                    np.array(qhi, np.uint32))
+    want = oracle.index(csr).execute(qb)
+    ix = DeviceIndex.from_csr(csr, device=gpu)
+    for sel in (0, 1):
+        assert_same(ix.query(qb, config(selector=sel, tile_bytes=tile_bytes)), want, f"spans tile {tile_bytes} sel {sel}")
