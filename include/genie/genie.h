@@ -124,6 +124,25 @@ int genie_index_create_shard(uint32_t num_objects, uint64_t num_keys, const uint
                              uint32_t id_begin, uint32_t id_end, int device, genie_index** out,
                              char* err, size_t errlen);
 
+/* MCIX index files (the reference's on-disk format, index_io.hpp:27-154).
+ * genie_mcix_parse: validates an image exactly as deserialize_index does
+ * (index_io.hpp:84-146; failures are GENIE_ERR_DATA with its messages) and
+ * returns it as CSR -- call once with null arrays for the sizes, then with
+ * keys[K], key_off[K+1], postings[P].
+ * genie_index_load_mcix: parse + genie_index_create (load_index's product
+ * straight into device memory, index_io.hpp:148-154).
+ * genie_mcix_serialize: the image serialize_index (index_io.hpp:63-82) writes
+ * for the index build_index makes from this CSR with split threshold `split`
+ * (0 = no splitting; index.hpp:229-238); *size in/out (null out: size only). */
+int genie_mcix_parse(const uint8_t* data, uint64_t size, uint32_t* num_objects, uint64_t* num_keys,
+                     uint64_t* num_postings, uint64_t* keys, uint64_t* key_off, uint32_t* postings,
+                     char* err, size_t errlen);
+int genie_index_load_mcix(const uint8_t* data, uint64_t size, int device, genie_index** out, char* err,
+                          size_t errlen);
+int genie_mcix_serialize(uint32_t num_objects, uint64_t num_keys, const uint64_t* keys, const uint64_t* key_off,
+                         const uint32_t* postings, uint32_t split, uint8_t* out, uint64_t* size, char* err,
+                         size_t errlen);
+
 void genie_index_destroy(genie_index* ix);
 
 /* Index facts: num_objects, keys, postings, id_offset, device. */

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cctype>
+#include <cstdio>
 #include <cstdint>
 #include <memory>
 #include <optional>
@@ -163,6 +164,9 @@ public:
     std::size_t keyword_count() const noexcept { return keys_.size(); }
     const std::vector<ObjectId>& list_array() const noexcept { return post_; }
     std::optional<std::uint32_t> split_threshold() const noexcept { return split_; }
+    // the CSR image: packed keywords (ascending) and their postings offsets
+    const std::vector<std::uint64_t>& packed_keys() const noexcept { return keys_; }
+    const std::vector<std::uint64_t>& key_offsets() const noexcept { return off_; }
 
     // spans of every indexed keyword inside the item's range (index.hpp:86-96)
     std::vector<PostingsSpan> lookup(const QueryItem& item) const {
@@ -229,6 +233,61 @@ inline InvertedIndex build_index(std::span<const ObjectRecord> objects,
     }
     if (!pairs.empty()) off.push_back(post.size());
     return InvertedIndex(n, std::move(keys), std::move(off), std::move(post), split_threshold, device);
+}
+
+// ------------------------------------------------------------------ index_io
+// MCIX files (index_io.hpp:27-154) through the C ABI: the same bytes as the
+// reference's serialize_index for the same build, the same validation and
+// DataError messages on load.  A loaded index keeps whole-list spans (the
+// file's span cut is a build-time choice; results do not depend on it).
+
+inline std::vector<std::uint8_t> serialize_index(const InvertedIndex& index) {
+    char err[512] = {};
+    std::uint64_t size = 0;
+    const auto& k = index.packed_keys();
+    const auto& o = index.key_offsets();
+    const auto& p = index.list_array();
+    const std::uint32_t split = index.split_threshold().value_or(0);
+    detail::check(genie_mcix_serialize(index.num_objects(), k.size(), k.data(), o.data(), p.data(), split, nullptr,
+                                       &size, err, sizeof(err)),
+                  err);
+    std::vector<std::uint8_t> out(size);
+    detail::check(genie_mcix_serialize(index.num_objects(), k.size(), k.data(), o.data(), p.data(), split, out.data(),
+                                       &size, err, sizeof(err)),
+                  err);
+    return out;
+}
+
+inline InvertedIndex deserialize_index(const std::uint8_t* data, std::size_t size, int device = 0) {
+    char err[512] = {};
+    std::uint32_t n = 0;
+    std::uint64_t K = 0, P = 0;
+    detail::check(genie_mcix_parse(data, size, &n, &K, &P, nullptr, nullptr, nullptr, err, sizeof(err)), err);
+    std::vector<std::uint64_t> keys(K), off(K + 1);
+    std::vector<ObjectId> post(P);
+    detail::check(genie_mcix_parse(data, size, nullptr, nullptr, nullptr, keys.data(), off.data(), post.data(), err,
+                                   sizeof(err)),
+                  err);
+    return InvertedIndex(n, std::move(keys), std::move(off), std::move(post), std::nullopt, device);
+}
+
+inline void save_index(const InvertedIndex& index, const std::string& path) {
+    const auto bytes = serialize_index(index);
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw DataError("cannot open " + path + " for writing");
+    const bool ok = std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size();
+    std::fclose(f);
+    if (!ok) throw DataError("failed writing " + path);
+}
+
+inline InvertedIndex load_index(const std::string& path, int device = 0) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw DataError("cannot open " + path);
+    std::vector<std::uint8_t> bytes;
+    std::uint8_t buf[1 << 16];
+    for (std::size_t got; (got = std::fread(buf, 1, sizeof(buf), f)) > 0;) bytes.insert(bytes.end(), buf, buf + got);
+    std::fclose(f);
+    return deserialize_index(bytes.data(), bytes.size(), device);
 }
 
 struct IndexPartition {

@@ -218,9 +218,18 @@ class RefLib:
                                         f64p, u64p, *E]
         L.mcxref_kernel_width.restype = C.c_double
         L.mcxref_kernel_width.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_uint64]
+        L.mcxref_index_serialize.argtypes = [vp, vp, u64p, *E]
+        L.mcxref_deserialize.argtypes = [vp, C.c_uint64, *E]
         L.mcxref_hash_results.restype = C.c_uint64
         L.mcxref_hash_results.argtypes = [C.c_uint32, u32p, u32p, u32p, C.c_uint32, u32p, u32p]
         self.L = L
+
+    def deserialize_status(self, image: bytes):
+        """(status, message) deserialize_index (index_io.hpp:84-146) gives an image."""
+        buf = (C.c_uint8 * max(1, len(image))).from_buffer_copy(image or b"\0")
+        err = C.create_string_buffer(512)
+        rc = self.L.mcxref_deserialize(C.cast(buf, vp), len(image), err, 512)
+        return rc, err.value.decode()
 
     def hardware_threads(self) -> int:
         return int(self.L.mcxref_hardware_threads())
@@ -309,6 +318,15 @@ class RefIndex:
             self.lib.L.mcxref_index_free(self.h)
         except Exception:
             pass
+
+    def serialize(self) -> bytes:
+        """serialize_index (index_io.hpp:63-82) of the reference index."""
+        L = self.lib.L
+        size, err = C.c_uint64(0), C.create_string_buffer(512)
+        RefLib._check(L.mcxref_index_serialize(self.h, None, C.byref(size), err, 512), err)
+        out = (C.c_uint8 * max(1, size.value))()
+        RefLib._check(L.mcxref_index_serialize(self.h, C.cast(out, vp), C.byref(size), err, 512), err)
+        return bytes(out)[: size.value]
 
     def shape(self):
         K, P, S = C.c_uint64(), C.c_uint64(), C.c_uint64()

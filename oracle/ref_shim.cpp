@@ -197,6 +197,24 @@ void mcxref_index_export(void* p, std::uint64_t* keys, std::uint32_t* first_span
     std::memcpy(postings, l.data(), l.size() * sizeof(std::uint32_t));
 }
 
+// serialize_index (index_io.hpp:63-82): size query with out == nullptr.
+int mcxref_index_serialize(void* p, std::uint8_t* out, std::uint64_t* size, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const auto img = mcx::serialize_index(static_cast<RefIndex*>(p)->index);
+        if (out) {
+            if (*size < img.size()) throw mcx::ContractError("serialize buffer too small");
+            std::memcpy(out, img.data(), img.size());
+        }
+        *size = img.size();
+    });
+}
+
+// deserialize_index (index_io.hpp:84-146) of an image: the status and message
+// the reference produces for it (0 when it loads).
+int mcxref_deserialize(const std::uint8_t* data, std::uint64_t size, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { (void)mcx::deserialize_index(data, size); });
+}
+
 std::uint32_t mcxref_max_multiplicity(void* p, std::uint16_t dim) {
     return static_cast<RefIndex*>(p)->index.max_multiplicity(dim);
 }

@@ -213,6 +213,17 @@ class DeviceIndex:
         return cls(h.value, lib)
 
     @classmethod
+    def from_mcix(cls, image, device: int = 0) -> "DeviceIndex":
+        """load_index (index_io.hpp:148-154): an MCIX image (bytes or a path)
+        validated like deserialize_index and uploaded as the device CSR."""
+        data = _mcix_bytes(image)
+        lib = N.engine()
+        h, err = C.c_void_p(), _errbuf()
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        check(lib.genie_index_load_mcix(C.cast(buf, C.c_void_p), len(data), device, C.byref(h), err, len(err)), err)
+        return cls(h.value, lib)
+
+    @classmethod
     def shard(cls, csr: CSR, id_begin: int, id_end: int, device: int = 0) -> "DeviceIndex":
         """Object-id range [id_begin, id_end) of a full CSR (one partition of
         partition_dataset, index.hpp:263-291), ids rebased, offset kept."""
@@ -452,6 +463,45 @@ class Encoder:
                                                     C.c_void_p(d_elems.data_ptr()), int(d_off.shape[0]) - 1,
                                                     C.c_void_p(d_tokens.data_ptr()), C.c_void_p(stream or 0), err,
                                                     len(err)), err)
+
+
+def _mcix_bytes(image) -> bytes:
+    if isinstance(image, (bytes, bytearray, memoryview)):
+        return bytes(image)
+    with open(image, "rb") as f:
+        return f.read()
+
+
+def mcix_parse(image) -> CSR:
+    """deserialize_index (index_io.hpp:84-146) as CSR, on the host (no GPU):
+    the same validation and DataError messages as the reference."""
+    data = _mcix_bytes(image)
+    lib = N.engine()
+    buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+    n, K, P, err = C.c_uint32(), C.c_uint64(), C.c_uint64(), _errbuf()
+    check(lib.genie_mcix_parse(C.cast(buf, C.c_void_p), len(data), C.byref(n), C.byref(K), C.byref(P), None, None,
+                               None, err, len(err)), err)
+    keys = np.zeros(K.value, np.uint64)
+    off = np.zeros(K.value + 1, np.uint64)
+    post = np.zeros(max(1, P.value), np.uint32)
+    check(lib.genie_mcix_parse(C.cast(buf, C.c_void_p), len(data), None, None, None, _ptr(keys, C.c_uint64),
+                               _ptr(off, C.c_uint64), _ptr(post, C.c_uint32), err, len(err)), err)
+    return CSR(n.value, keys, off, post[:P.value])
+
+
+def mcix_serialize(csr: CSR, split: Optional[int] = 4096) -> bytes:
+    """serialize_index (index_io.hpp:63-82) of build_index(objects, split)
+    (index.hpp:190-250) for the objects this CSR holds; split None = whole
+    lists (the reference's default build)."""
+    lib = N.engine()
+    size, err = C.c_uint64(0), _errbuf()
+    key_off = csr.key_off if csr.key_off.size else np.zeros(1, np.uint64)
+    args = (csr.n, csr.num_keys, _ptr(csr.keys, C.c_uint64), _ptr(key_off, C.c_uint64),
+            _ptr(csr.postings, C.c_uint32), 0 if split is None else int(split))
+    check(lib.genie_mcix_serialize(*args, None, C.byref(size), err, len(err)), err)
+    out = (C.c_uint8 * max(1, size.value))()
+    check(lib.genie_mcix_serialize(*args, C.cast(out, C.c_void_p), C.byref(size), err, len(err)), err)
+    return bytes(out)[: size.value]
 
 
 def point_queries(tokens: np.ndarray, k: int, first_id: int = 0) -> QueryBatch:

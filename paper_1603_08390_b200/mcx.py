@@ -398,6 +398,30 @@ def build_index(objects: Sequence[ObjectRecord], split_threshold: Optional[int] 
     return InvertedIndex(csr, split_threshold, device)
 
 
+# ---------------------------------------------------------------- index_io.hpp
+# MCIX files (index_io.hpp:27-154): the reference's bytes for the same build,
+# its validation and DataError messages on load.  A loaded index keeps
+# whole-list spans (the file's span cut is a build-time choice).
+
+
+def serialize_index(index: InvertedIndex) -> bytes:
+    return E.mcix_serialize(index.csr, index.split_threshold())
+
+
+def deserialize_index(data: bytes, device: int = 0) -> InvertedIndex:
+    return InvertedIndex(E.mcix_parse(data), None, device)
+
+
+def save_index(index: InvertedIndex, path: str) -> None:
+    with open(path, "wb") as f:
+        f.write(serialize_index(index))
+
+
+def load_index(path: str, device: int = 0) -> InvertedIndex:
+    with open(path, "rb") as f:
+        return deserialize_index(f.read(), device)
+
+
 @dataclass
 class IndexPartition:
     """index.hpp:254-259"""

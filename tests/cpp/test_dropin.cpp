@@ -141,6 +141,22 @@ int main() {
     CHECK(dres.results[0].entries.size() == 2 && dres.results[0].entries[0] == (TopKEntry{0, 2}) &&
           dres.results[0].entries[1] == (TopKEntry{1, 1}) && dres.results[0].threshold == 1);
 
+    // MCIX round trip (index_io.hpp): save -> load -> same answers
+    {
+        const auto img = serialize_index(build_index(docs, 1));
+        const auto back = deserialize_index(img.data(), img.size());
+        const auto r2 = execute_batch(back, std::vector<Query>{*dq});
+        CHECK(hash_results(r2.results) == hash_results(dres.results));
+        bool bad = false;
+        try {
+            std::vector<std::uint8_t> broken(img.begin(), img.end() - 1);
+            (void)deserialize_index(broken.data(), broken.size());
+        } catch (const DataError&) {
+            bad = true;
+        }
+        CHECK(bad);
+    }
+
     std::printf(failures ? "dropin: %d failures\n" : "dropin: ok\n", failures);
     return failures ? 1 : 0;
 }

@@ -313,3 +313,23 @@ def test_many_spans_per_query(gpu, oracle, tile_bytes):
     ix = DeviceIndex.from_csr(csr, device=gpu)
     for sel in (0, 1):
         assert_same(ix.query(qb, config(selector=sel, tile_bytes=tile_bytes)), want, f"spans tile {tile_bytes} sel {sel}")
+
+
+def test_mcix_image_loads_into_the_device_index(gpu, oracle, tmp_path):
+    # load_index (index_io.hpp:148-154) straight into device memory: the same
+    # CSR back, the same answers as the oracle
+    from paper_1603_08390_b200 import engine as E
+    from paper_1603_08390_b200 import mcx
+
+    ds = synth.tweets(n=120_000, vocab=30_000, words=10, queries=48, k=100)
+    img = E.mcix_serialize(ds.csr, 4096)
+    ix = DeviceIndex.from_mcix(img, device=gpu)
+    back = ix.export()
+    assert np.array_equal(back.keys, ds.csr.keys) and np.array_equal(back.postings, ds.csr.postings)
+    want = oracle.index(ds.csr).execute(ds.queries)
+    assert_same(ix.query(ds.queries), want, "mcix")
+    path = tmp_path / "tweets.mcix"
+    mcx.save_index(mcx.InvertedIndex(ds.csr, 4096), str(path))
+    loaded = mcx.load_index(str(path))
+    assert np.array_equal(loaded.csr.key_off, ds.csr.key_off)
+    assert_same(DeviceIndex.from_mcix(str(path), device=gpu).query(ds.queries), want, "mcix file")

@@ -201,3 +201,60 @@ def test_document_match_counts_equal_set_intersections():
             assert common == 0
         else:
             assert mcx.match_count_reference(query, obj) == common
+
+
+# ----------------------------------------------------------------- MCIX files
+
+
+@needs_ref
+@pytest.mark.parametrize("seed,split", [(1, None), (2, 4096), (3, 16), (4, 1), (5, 7)])
+def test_mcix_bytes_equal_reference_serializer(seed, split):
+    # serialize_index (index_io.hpp:63-82) of build_index(objects, split): the
+    # C ABI writer produces the reference's exact bytes, and reads them back
+    ds = synth.random_instance(n=300 + 211 * seed, dims=3, tokens=4 + seed, max_kw=5, queries=2, seed=seed)
+    want = RefLib().index(ds.csr, split=split or 0).serialize()
+    got = E.mcix_serialize(ds.csr, split)
+    assert got == want
+    back = E.mcix_parse(want)
+    assert back.n == ds.csr.n and np.array_equal(back.keys, ds.csr.keys)
+    assert np.array_equal(back.key_off, ds.csr.key_off) and np.array_equal(back.postings, ds.csr.postings)
+    idx = mcx.InvertedIndex(ds.csr, split)
+    assert mcx.serialize_index(idx) == want
+    assert np.array_equal(mcx.deserialize_index(want).csr.postings, ds.csr.postings)
+
+
+@needs_ref
+def test_mcix_rejects_what_the_reference_rejects():
+    # deserialize_index's validation (index_io.hpp:84-146): same status, same message
+    ref = RefLib()
+    ds = synth.random_instance(n=200, dims=2, tokens=5, max_kw=4, queries=1, seed=11)
+    img = bytearray(E.mcix_serialize(ds.csr, 8))
+    K = ds.csr.num_keys
+
+    def entry_offset(j):  # byte offset of keyword entry j
+        pos = 16
+        for i in range(j):
+            spans = int.from_bytes(img[pos + 6:pos + 8], "little")
+            pos += 8 + 16 * spans
+        return pos
+
+    list_at = entry_offset(K)
+    cases = {
+        "magic": bytes(b"MCIY" + img[4:]),
+        "version": bytes(img[:4] + (2).to_bytes(4, "little") + img[8:]),
+        "truncated": bytes(img[:list_at - 3]),
+        "size": bytes(img[:-4]),
+        "order": bytes(img[:entry_offset(1)] + (0).to_bytes(2, "little") + (0).to_bytes(4, "little") +
+                       img[entry_offset(1) + 6:]),
+        "tiling": bytes(img[:24] + (int.from_bytes(img[24:32], "little") + 1).to_bytes(8, "little") + img[32:]),
+        "id range": bytes(img[:list_at] + (10**6).to_bytes(4, "little") + img[list_at + 4:]),
+        "ascending": bytes(img[:list_at] + img[list_at + 4:list_at + 8] + img[list_at:list_at + 4] +
+                           img[list_at + 8:]),
+        "no spans": bytes(img[:22] + (0).to_bytes(2, "little") + img[24 + 16 * int.from_bytes(img[22:24], "little"):]),
+    }
+    for name, data in cases.items():
+        rc, msg = ref.deserialize_status(data)
+        assert rc == 2, (name, rc, msg)  # DataError
+        with pytest.raises(E.DataError) as ex:
+            E.mcix_parse(data)
+        assert str(ex.value) == msg, (name, str(ex.value), msg)
