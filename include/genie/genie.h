@@ -143,6 +143,13 @@ int genie_mcix_serialize(uint32_t num_objects, uint64_t num_keys, const uint64_t
                          const uint32_t* postings, uint32_t split, uint8_t* out, uint64_t* size, char* err,
                          size_t errlen);
 
+/* build_index (index.hpp:190-250) on the device: object o owns keywords
+ * [obj_off[o], obj_off[o+1]) of dims / tokens (host arrays; ids dense 0..n-1).
+ * A keyword repeated inside one object is a ContractError (ObjectRecord,
+ * model.hpp:57-62).  The CSR is identical to the host build (tested). */
+int genie_index_build(uint32_t num_objects, const uint64_t* obj_off, const uint16_t* dims, const uint32_t* tokens,
+                      int device, genie_index** out, char* err, size_t errlen);
+
 void genie_index_destroy(genie_index* ix);
 
 /* Index facts: num_objects, keys, postings, id_offset, device. */

@@ -76,6 +76,7 @@ class LshConfig(C.Structure):
 # name -> (restype, argtypes); every symbol declared in include/genie/genie.h
 ENGINE_SYMBOLS = {
     "genie_config_default": (Config, []),
+    "genie_index_build": (C.c_int, [C.c_uint32, u64p, u16p, u32p, C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "genie_mcix_parse": (C.c_int, [vp, C.c_uint64, u32p, u64p, u64p, u64p, u64p, u32p, C.c_char_p, C.c_size_t]),
     "genie_index_load_mcix": (C.c_int, [vp, C.c_uint64, C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "genie_mcix_serialize": (C.c_int, [C.c_uint32, C.c_uint64, u64p, u64p, u32p, C.c_uint32, vp, u64p, C.c_char_p,

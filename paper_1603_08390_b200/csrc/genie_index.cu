@@ -1,6 +1,9 @@
 // Device inverted index: CSR upload, validation, id-range shards, per-dim
 // statistics, export.  Replaces the product of mcx::build_index
 // (index.hpp:190-250) and the InvertedIndex accessors (index.hpp:41-182).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+
 #include <algorithm>
 #include <cstdlib>
 #include <thread>
@@ -147,6 +150,27 @@ static void validate_csr(uint32_t n, uint64_t K, const uint64_t* keys, const uin
     (void)P;
 }
 
+// ---- device build (build_index, index.hpp:190-250): one (packed keyword,
+// object id) pair per object keyword, emitted in object order, so the stable
+// radix sort by keyword leaves each list's ids ascending.
+__global__ void k_obj_pairs(const uint64_t* obj_off, uint32_t n, const uint16_t* dims, const uint32_t* tokens,
+                            uint64_t* keys, uint32_t* ids) {
+    for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
+        for (uint64_t i = obj_off[o]; i < obj_off[o + 1]; ++i) {
+            keys[i] = (uint64_t(dims[i]) << 32) | tokens[i];
+            ids[i] = o;
+        }
+    }
+}
+
+// a keyword repeated inside one object (ObjectRecord rejects it, model.hpp:57-62):
+// the smallest such position of the sorted pairs
+__global__ void k_dup_pairs(const uint64_t* keys, const uint32_t* ids, uint64_t total, unsigned long long* first) {
+    for (uint64_t i = 1 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        if (keys[i] == keys[i - 1] && ids[i] == ids[i - 1]) atomicMin(first, static_cast<unsigned long long>(i));
+}
+
 static genie_index* upload(uint32_t n, uint64_t K, const uint64_t* keys, const uint64_t* off,
                            const uint32_t* post, const uint32_t* dim_mult, uint32_t id_offset,
                            int device) {
@@ -291,6 +315,111 @@ int genie_index_export(genie_index* ix, uint64_t* keys, uint64_t* key_off, uint3
         if (ix->P && postings)
             GENIE_CUDA(cudaMemcpy(postings, ix->postings.p, ix->P * sizeof(uint32_t),
                                   cudaMemcpyDeviceToHost));
+        return GENIE_OK;
+    });
+}
+
+int genie_index_build(uint32_t num_objects, const uint64_t* obj_off, const uint16_t* dims, const uint32_t* tokens,
+                      int device, genie_index** out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&]() -> int {
+        if (!out || !obj_off) throw Error(GENIE_ERR_CONTRACT, "genie_index_build: null argument");
+        const uint64_t total = obj_off[num_objects];
+        if (obj_off[0] != 0) throw Error(GENIE_ERR_CONTRACT, "genie_index_build: obj_off[0] must be 0");
+        for (uint32_t o = 0; o < num_objects; ++o)
+            if (obj_off[o + 1] < obj_off[o]) throw Error(GENIE_ERR_CONTRACT, "genie_index_build: obj_off not monotone");
+        if (total && (!dims || !tokens)) throw Error(GENIE_ERR_CONTRACT, "genie_index_build: null argument");
+        ensure_device(device);
+        auto* ix = new genie_index;
+        try {
+            ix->device = device;
+            ix->n = num_objects;
+            ix->sms = sm_count(device);
+            GENIE_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+            for (auto& e : ix->ev) GENIE_CUDA(cudaEventCreate(&e));
+            cudaStream_t s = ix->stream;
+            DevBuf<uint64_t> d_off, k1, k2, uk;
+            DevBuf<uint16_t> d_dims;
+            DevBuf<uint32_t> d_tok, v1, runs;
+            DevBuf<unsigned long long> first;
+            DevBuf<int64_t> nruns;
+            d_off.reserve(uint64_t(num_objects) + 1);
+            d_dims.reserve(total);
+            d_tok.reserve(total);
+            k1.reserve(total);
+            k2.reserve(total);
+            v1.reserve(total);
+            first.reserve(1);
+            nruns.reserve(1);
+            ix->postings.reserve(total + 64);
+            GENIE_CUDA(cudaMemsetAsync(ix->postings.p, 0, (total + 64) * 4, s));
+            GENIE_CUDA(cudaMemcpyAsync(d_off.p, obj_off, (uint64_t(num_objects) + 1) * 8, cudaMemcpyHostToDevice, s));
+            if (total) {
+                GENIE_CUDA(cudaMemcpyAsync(d_dims.p, dims, total * 2, cudaMemcpyHostToDevice, s));
+                GENIE_CUDA(cudaMemcpyAsync(d_tok.p, tokens, total * 4, cudaMemcpyHostToDevice, s));
+            }
+            const unsigned grid = std::max(1u, std::min<unsigned>((num_objects + 255) / 256, ix->sms * 16));
+            if (num_objects) k_obj_pairs<<<grid, 256, 0, s>>>(d_off.p, num_objects, d_dims.p, d_tok.p, k1.p, v1.p);
+            cub::DoubleBuffer<uint64_t> dk(k1.p, k2.p);
+            cub::DoubleBuffer<uint32_t> dv(v1.p, ix->postings.p);
+            std::vector<uint64_t> hkeys, hoff{0};
+            if (total) {
+                size_t tmp = 0;
+                GENIE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, static_cast<int64_t>(total), 0, 48, s));
+                DevBuf<unsigned char> t;
+                t.reserve(tmp);
+                GENIE_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, dk, dv, static_cast<int64_t>(total), 0, 48, s));
+                if (dv.Current() != ix->postings.p)
+                    GENIE_CUDA(cudaMemcpyAsync(ix->postings.p, dv.Current(), total * 4, cudaMemcpyDeviceToDevice, s));
+                GENIE_CUDA(cudaMemsetAsync(first.p, 0xff, 8, s));
+                const unsigned g2 = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, uint64_t(ix->sms) * 16));
+                k_dup_pairs<<<std::max(1u, g2), 256, 0, s>>>(dk.Current(), ix->postings.p, total, first.p);
+                unsigned long long h_first = 0;
+                GENIE_CUDA(cudaMemcpyAsync(&h_first, first.p, 8, cudaMemcpyDeviceToHost, s));
+                GENIE_CUDA(cudaStreamSynchronize(s));
+                if (h_first != ~0ull) {
+                    uint64_t key = 0;
+                    uint32_t id = 0;
+                    GENIE_CUDA(cudaMemcpy(&key, dk.Current() + h_first, 8, cudaMemcpyDeviceToHost));
+                    GENIE_CUDA(cudaMemcpy(&id, ix->postings.p + h_first, 4, cudaMemcpyDeviceToHost));
+                    throw Error(GENIE_ERR_CONTRACT, "ObjectRecord " + std::to_string(id) + ": duplicate keyword (dim=" +
+                                                        std::to_string(key >> 32) + ", token=" +
+                                                        std::to_string(key & 0xffffffffull) + ")");
+                }
+                // list boundaries: run-length encode of the sorted keywords
+                uk.reserve(total);
+                runs.reserve(total);
+                size_t tmp2 = 0;
+                GENIE_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp2, dk.Current(), uk.p, runs.p, nruns.p,
+                                                              static_cast<int64_t>(total), s));
+                DevBuf<unsigned char> t2;
+                t2.reserve(tmp2);
+                GENIE_CUDA(cub::DeviceRunLengthEncode::Encode(t2.p, tmp2, dk.Current(), uk.p, runs.p, nruns.p,
+                                                              static_cast<int64_t>(total), s));
+                int64_t K = 0;
+                GENIE_CUDA(cudaMemcpyAsync(&K, nruns.p, 8, cudaMemcpyDeviceToHost, s));
+                GENIE_CUDA(cudaStreamSynchronize(s));
+                hkeys.resize(K);
+                std::vector<uint32_t> hruns(K);
+                GENIE_CUDA(cudaMemcpy(hkeys.data(), uk.p, K * 8, cudaMemcpyDeviceToHost));
+                GENIE_CUDA(cudaMemcpy(hruns.data(), runs.p, K * 4, cudaMemcpyDeviceToHost));
+                hoff.resize(K + 1);
+                for (int64_t j = 0; j < K; ++j) hoff[j + 1] = hoff[j] + hruns[j];
+            }
+            ix->K = hkeys.size();
+            ix->P = total;
+            ix->keys.reserve(ix->K + 1);
+            ix->key_off.reserve(ix->K + 1);
+            if (ix->K) GENIE_CUDA(cudaMemcpy(ix->keys.p, hkeys.data(), ix->K * 8, cudaMemcpyHostToDevice));
+            GENIE_CUDA(cudaMemcpy(ix->key_off.p, hoff.data(), (ix->K + 1) * 8, cudaMemcpyHostToDevice));
+            ix->dim_mult.reserve(65536);
+            compute_dim_stats(ix, hkeys.data(), hoff.data());
+            build_dense_containers(ix, hoff.data());
+            GENIE_CUDA(cudaDeviceSynchronize());
+        } catch (...) {
+            genie_index_destroy(ix);
+            throw;
+        }
+        *out = ix;
         return GENIE_OK;
     });
 }

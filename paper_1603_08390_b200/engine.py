@@ -213,6 +213,23 @@ class DeviceIndex:
         return cls(h.value, lib)
 
     @classmethod
+    def build(cls, n: int, obj_off: np.ndarray, dims: np.ndarray, tokens: np.ndarray,
+              device: int = 0) -> "DeviceIndex":
+        """build_index (index.hpp:190-250) on the device: object o owns
+        keywords [obj_off[o], obj_off[o+1]) of dims/tokens."""
+        off = np.ascontiguousarray(obj_off, np.uint64)
+        d = np.ascontiguousarray(dims, np.uint16)
+        t = np.ascontiguousarray(tokens, np.uint32)
+        assert off.shape == (n + 1,) and d.shape == t.shape
+        lib = N.engine()
+        h, err = C.c_void_p(), _errbuf()
+        d1 = d if d.size else np.zeros(1, np.uint16)
+        t1 = t if t.size else np.zeros(1, np.uint32)
+        check(lib.genie_index_build(n, _ptr(off, C.c_uint64), _ptr(d1, C.c_uint16), _ptr(t1, C.c_uint32), device,
+                                    C.byref(h), err, len(err)), err)
+        return cls(h.value, lib)
+
+    @classmethod
     def from_mcix(cls, image, device: int = 0) -> "DeviceIndex":
         """load_index (index_io.hpp:148-154): an MCIX image (bytes or a path)
         validated like deserialize_index and uploaded as the device CSR."""

@@ -333,3 +333,36 @@ def test_mcix_image_loads_into_the_device_index(gpu, oracle, tmp_path):
     loaded = mcx.load_index(str(path))
     assert np.array_equal(loaded.csr.key_off, ds.csr.key_off)
     assert_same(DeviceIndex.from_mcix(str(path), device=gpu).query(ds.queries), want, "mcix file")
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_device_build_equals_host_build(gpu, oracle, seed):
+    # build_index (index.hpp:190-250) on the device: the same CSR as the host
+    # build, the same answers
+    rng = np.random.default_rng(seed)
+    n = 20_000 + 7_000 * seed
+    kw = rng.integers(0, 12, size=n)
+    off = np.concatenate([[0], np.cumsum(kw)]).astype(np.uint64)
+    dims = np.empty(int(off[-1]), np.uint16)
+    toks = np.empty(int(off[-1]), np.uint32)
+    for o in range(n):  # distinct (dim, token) per object
+        a, b = int(off[o]), int(off[o + 1])
+        code = rng.choice(4 * 300, size=b - a, replace=False)
+        dims[a:b] = code // 300
+        toks[a:b] = code % 300 + (seed * 1000)
+    host = synth.csr_from_objects(n, off, dims, toks)
+    ix = DeviceIndex.build(n, off, dims, toks, device=gpu)
+    back = ix.export()
+    assert np.array_equal(back.keys, host.keys) and np.array_equal(back.key_off, host.key_off)
+    assert np.array_equal(back.postings, host.postings)
+    ds = synth.random_instance(n=10, seed=1)  # only for a query shape
+    qb = QueryBatch(np.arange(8, dtype=np.uint32), np.full(8, 50, np.uint32), np.arange(9, dtype=np.uint64) * 2,
+                    np.array([0, 1] * 8, np.uint16), np.array([seed * 1000 + 5 * i for i in range(16)], np.uint32),
+                    np.array([seed * 1000 + 5 * i + 40 for i in range(16)], np.uint32))
+    assert_same(ix.query(qb), oracle.index(host).execute(qb), f"device build {seed}")
+    dup_dims, dup_toks = dims.copy(), toks.copy()
+    j = int(np.argmax(kw >= 2))
+    a = int(off[j])
+    dup_dims[a + 1], dup_toks[a + 1] = dup_dims[a], dup_toks[a]
+    with pytest.raises(ContractError, match="duplicate keyword"):
+        DeviceIndex.build(n, off, dup_dims, dup_toks, device=gpu)
