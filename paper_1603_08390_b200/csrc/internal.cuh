@@ -25,8 +25,11 @@ constexpr int kRecLevels = 4;                 // levels in a tile's record (gate
 constexpr uint32_t kRecWords = 8;             // record: base level + kRecLevels counts, padded to 16 B
 constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shared memory (W <= 8)
 constexpr uint32_t kMergeThreads = 512;
-constexpr uint32_t kMergeSmallThreads = 256;   // per-query merge CTAs of a batch
-constexpr uint32_t kMergeSmallCap = 4096;      // their key capacity (<= 16 x threads)
+#ifndef GENIE_MERGE_THREADS
+#define GENIE_MERGE_THREADS 128
+#endif
+constexpr uint32_t kMergeSmallThreads = GENIE_MERGE_THREADS;  // per-query merge CTAs of a batch
+constexpr uint32_t kMergeSmallCap = 16 * kMergeSmallThreads;  // their key capacity (<= 16 x threads)
 constexpr uint32_t kSortCap = 8192;           // merge entries sorted in shared memory
 constexpr uint32_t kDefaultUnit = 1024;       // postings per warp work unit (guided scheduling)
 #ifndef GENIE_DENSE_LEVELS
