@@ -2552,12 +2552,12 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     k_init_status<<<1, 32, 0, s>>>(w.status.p);
     ++launches;
     if (Q) {
-        k_resolve<<<(Q * 32 + 255) / 256, 256, 0, s>>>(p);
+        k_resolve<<<(Q * 32 + kLookupThreads - 1) / kLookupThreads, kLookupThreads, 0, s>>>(p);
         k_plan<<<1, 1024, 0, s>>>(p);
         k_worklist<<<(Q * 32 + 255) / 256, 256, 0, s>>>(p);
         launches += 3;
         const int sms = ix->sms;
-        k_cut<<<sms * 8, 256, 0, s>>>(p);
+        k_cut<<<sms * kCutCtasPerSm, kLookupThreads, 0, s>>>(p);
         ++launches;
         if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
         p.ht_slots = kHtSlots;

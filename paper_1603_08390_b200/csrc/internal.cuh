@@ -24,6 +24,14 @@ constexpr uint32_t kHtMaxSlots = 4096;        // ... and maximum (items whose co
 constexpr int kRecLevels = 4;                 // levels in a tile's record (gate_start)
 constexpr uint32_t kRecWords = 8;             // record: base level + kRecLevels counts, padded to 16 B
 constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shared memory (W <= 8)
+#ifndef GENIE_LOOKUP_THREADS
+#define GENIE_LOOKUP_THREADS 256
+#endif
+#ifndef GENIE_CUT_CTAS
+#define GENIE_CUT_CTAS 32
+#endif
+constexpr uint32_t kLookupThreads = GENIE_LOOKUP_THREADS;  // k_resolve / k_cut block size
+constexpr uint32_t kCutCtasPerSm = GENIE_CUT_CTAS;         // k_cut grid: CTAs per SM
 constexpr uint32_t kMergeThreads = 512;
 #ifndef GENIE_MERGE_THREADS
 #define GENIE_MERGE_THREADS 128
