@@ -60,7 +60,8 @@ struct BatchParams {
     const uint32_t* lo;
     const uint32_t* hi;
     // plan
-    uint32_t tile_bits;
+    uint32_t tile_bits;       // counter tile allocated per CTA (bits)
+    uint32_t tile_bits_w[3];  // tile used by width class W = 4, 8, 16 (<= tile_bits)
     uint32_t unit;
     uint32_t selector;
     // workspace
@@ -85,6 +86,10 @@ struct BatchParams {
 };
 
 __device__ __forceinline__ uint32_t wclass(uint32_t W) { return W == 4 ? 0 : (W == 8 ? 1 : 2); }
+
+__device__ __forceinline__ uint32_t tile_objs(const BatchParams& p, uint32_t W) {
+    return p.tile_bits_w[wclass(W)] / W;
+}
 
 __device__ __forceinline__ uint32_t ntiles_for(uint32_t n, uint32_t tile_bits, uint32_t W) {
     const uint32_t T = tile_bits / W;
@@ -155,7 +160,7 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
             atomicMin(&p.st[ST_BAD_BOUND], static_cast<unsigned long long>(q));
         } else {
             W = width_for(bnd);
-            nt = (P == 0 || p.n == 0) ? 0 : ntiles_for(p.n, p.tile_bits, W);
+            nt = (P == 0 || p.n == 0) ? 0 : ntiles_for(p.n, p.tile_bits_w[wclass(W)], W);
         }
     }
     p.q_bound[q] = bound;
@@ -183,7 +188,7 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
             nt = p.q_ntiles[q];
             W = p.q_W[q];
             if (nt) {
-                const uint32_t T = p.tile_bits / W;
+                const uint32_t T = tile_objs(p, W);
                 const uint32_t kq = p.k[q];
                 cap = min(kq, T);
                 // single-tile queries read each item's contiguous keyword
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(256) k_worklist(BatchParams p) {
     uint64_t cnt[3], ntc[3];
     for (int i = 0; i < 3; ++i) {
         cnt[i] = p.st[ST_CLASS0 + i];
-        ntc[i] = p.n ? ntiles_for(p.n, p.tile_bits, 4u << i) : 0;
+        ntc[i] = p.n ? ntiles_for(p.n, p.tile_bits_w[i], 4u << i) : 0;
     }
     const uint32_t rank = p.q_rank[q];
     const uint32_t tbase = p.q_tile_base[q];
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
         // batch; then this list needs no tile cuts
         if (ds >= 0 && p.q_S[q] <= kSpanBatch) continue;
         const uint32_t nt = p.q_ntiles[q];
-        const uint32_t T = p.tile_bits / p.q_W[q];
+        const uint32_t T = tile_objs(p, p.q_W[q]);
         uint32_t* cut = p.cuts + p.q_cut_base[q] + uint64_t(s) * (nt + 1);
         const uint32_t* list = p.postings + beg;
         for (uint32_t b = lane; b <= nt; b += 32) {
@@ -1854,7 +1859,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
     it.t = d.t;
     it.kq = d.kq;
     it.bound = d.bound;
-    const uint32_t T = p.tile_bits / W;
+    const uint32_t T = tile_objs(p, W);
     it.tile_lo = it.t * T;
     it.tile_n = min(T, p.n - it.tile_lo);
     it.words = ((it.tile_n + 31) >> 5) * W;  // whole 32-object blocks
@@ -1862,18 +1867,18 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
     it.slot = d.tile_slot;
     it.out_base = d.out_base;
     it.gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
-    // The table takes the shared memory after the item's counters (whole
-    // 16-word steps of dense_init), at least p.ht_slots, at most kHtMaxSlots
-    // slots -- small tiles (one-tile queries over few objects) get a large
-    // table.  The reference sizes it bit_ceil(2 k bound) (cpq.hpp:137-138,
-    // 283; that figure is kept for MemoryStats); concurrent admissions arrive
-    // in bursts of up to one per thread before AT can move, and spare
-    // capacity absorbs them without the exact-histogram fallback.  Results do
-    // not depend on the capacity.
+    // The table sits right after the item's counters (whole 16-word steps of
+    // dense_init): p.ht_slots slots, or -- for a query's first tile, whose
+    // gate starts low without lower-tile records and admits in bulk (one-tile
+    // queries, C1) -- all the room up to kHtMaxSlots.  The reference sizes it
+    // bit_ceil(2 k bound) (cpq.hpp:137-138, 283; that figure is kept for
+    // MemoryStats); concurrent admissions arrive in bursts of up to one per
+    // thread before AT can move, and spare capacity absorbs them without the
+    // exact-histogram fallback.  Results do not depend on the capacity.
     {
         const uint32_t cnt_bytes = ((it.words + 15) & ~15u) * 4;
         const uint32_t room = (p.tile_bits / 8 + p.ht_slots * 8 - cnt_bytes) / 8;
-        it.ht_cap = min(kHtMaxSlots, 1u << (31 - __clz(room)));
+        it.ht_cap = it.t == 0 ? min(kHtMaxSlots, 1u << (31 - __clz(room))) : p.ht_slots;
         sm.ht = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sm.cnt) + cnt_bytes);
     }
     const uint32_t S = d.S, nd = d.nd, G = d.G, ptot = d.ptot;
@@ -2425,6 +2430,43 @@ static uint32_t tile_bits_of(const genie_config& cfg) {
     return tb * 8;
 }
 
+// Counter tile allocation and per-width tiles.  Auto mode caps the tile so
+// that one tile's slice of the index (postings + bitmaps: bytes per object x
+// objects, at W = 8) fits ~90 % of L2 with 10 % slack: the tile-major sweep
+// then reads each slice from DRAM about once per batch, and the shared memory
+// left unallocated serves as L1 for the bitmap rows consecutive items of a
+// tile share.  The cap snaps to 64 / 48 / 32 KB (C3: 64 KB, +23 %; measured
+// non-power-of-two sizes lose up to 12 %).  W = 4 tiles hold at most as many
+// objects as the cap.  Explicit tile_bytes apply to every class unchanged.
+static uint32_t class_tile_bits(const genie_index* ix, const genie_config& cfg, uint32_t tile_bits,
+                                uint32_t (&out)[3]) {
+    for (int c = 0; c < 3; ++c) out[c] = tile_bits;
+    if (cfg.tile_bytes || ix->n == 0) return tile_bits;
+    static thread_local int dev_cached = -1;
+    static thread_local int l2_cached = 0;
+    if (dev_cached != ix->device) {
+        GENIE_CUDA(cudaDeviceGetAttribute(&l2_cached, cudaDevAttrL2CacheSize, ix->device));
+        dev_cached = ix->device;
+    }
+    const double bytes = double(ix->P) * 4.0 + double(ix->n_dense) * ix->bitmap_words * 4.0;
+    const double per_obj = bytes / double(ix->n);
+    if (per_obj <= 0 || l2_cached <= 0) return tile_bits;
+    const double objs = 0.9 * double(l2_cached) / per_obj;  // objects whose index slice fits L2
+    uint32_t alloc = tile_bits;
+    if (objs * 8.0 < 1.1 * double(tile_bits)) {  // the W = 8 tile would overflow L2
+        alloc = 32u << 13;                        // 32 KB floor
+        for (const uint32_t kb : {64u, 48u})
+            if (double(kb << 13) <= 1.1 * objs * 8.0 && (kb << 13) <= tile_bits) {
+                alloc = kb << 13;
+                break;
+            }
+    }
+    out[0] = std::min<uint32_t>(alloc, static_cast<uint32_t>(std::max(objs * 4.0, double(alloc) / 2)) & ~1023u);
+    out[1] = alloc;
+    out[2] = alloc;
+    return alloc;
+}
+
 static MergeSrc tile_merge_src(genie_index* ix, uint32_t Q, const uint32_t* d_k, uint32_t stride,
                                genie_entry* out, uint32_t* out_len, uint32_t* out_thr) {
     Workspace& w = ix->ws;
@@ -2480,9 +2522,11 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
                   uint32_t max_k, uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
                   uint32_t* d_out_thr, cudaStream_t s, bool timed) {
     (void)d_qid;
-    const uint32_t tile_bits = tile_bits_of(cfg);
+    uint32_t tile_bits_w[3];
+    const uint32_t tile_bits = class_tile_bits(ix, cfg, tile_bits_of(cfg), tile_bits_w);
     const uint32_t tile_bytes = tile_bits / 8;
-    reserve_workspace(ix, Q, total_items, max_k, out_stride, tile_bits);
+    reserve_workspace(ix, Q, total_items, max_k, out_stride,
+                      std::min({tile_bits_w[0] * 4, tile_bits_w[1] * 2, tile_bits_w[2]}));
     Workspace& w = ix->ws;
     ix->last_Q = Q;
     ix->last_cfg = cfg;
@@ -2504,6 +2548,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.lo = d_lo;
     p.hi = d_hi;
     p.tile_bits = tile_bits;
+    for (int c = 0; c < 3; ++c) p.tile_bits_w[c] = tile_bits_w[c];
     uint32_t unit = cfg.span_chunk ? cfg.span_chunk : kDefaultUnit;
     unit = std::min<uint32_t>(std::max<uint32_t>((unit + 127) & ~127u, 128), 1u << 16);
     p.unit = unit;
