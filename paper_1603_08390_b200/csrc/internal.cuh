@@ -19,7 +19,10 @@ namespace genie {
 constexpr uint32_t kScanThreads = GENIE_SCAN_THREADS;  // threads per scan CTA
 constexpr uint32_t kScanCtasPerSm = GENIE_SCAN_CTAS;   // resident scan CTAs per SM (registers, tile size)
 constexpr uint32_t kSpanBatch = 256;          // spans staged in shared memory per pass (x2 buffers)
-constexpr uint32_t kHtSlots = 1024;           // shared-memory Robin Hood table, minimum (8 KB; >= 4 x 256-bin histograms)
+#ifndef GENIE_HT_MIN
+#define GENIE_HT_MIN 1024
+#endif
+constexpr uint32_t kHtSlots = GENIE_HT_MIN;           // shared-memory Robin Hood table, minimum (8 KB; >= 4 x 256-bin histograms)
 constexpr uint32_t kHtMaxSlots = 4096;        // ... and maximum (items whose counters leave room)
 constexpr int kRecLevels = 4;                 // levels in a tile's record (gate_start)
 constexpr uint32_t kRecWords = 8;             // record: base level + kRecLevels counts, padded to 16 B
