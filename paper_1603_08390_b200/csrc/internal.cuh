@@ -24,8 +24,11 @@ constexpr uint32_t kSpanBatch = 256;          // spans staged in shared memory p
 #endif
 constexpr uint32_t kHtSlots = GENIE_HT_MIN;           // shared-memory Robin Hood table, minimum (8 KB; >= 4 x 256-bin histograms)
 constexpr uint32_t kHtMaxSlots = 4096;        // ... and maximum (items whose counters leave room)
-constexpr int kRecLevels = 4;                 // levels in a tile's record (gate_start)
-constexpr uint32_t kRecWords = 8;             // record: base level + kRecLevels counts, padded to 16 B
+#ifndef GENIE_REC_LEVELS
+#define GENIE_REC_LEVELS 3
+#endif
+constexpr int kRecLevels = GENIE_REC_LEVELS;   // levels in a tile's record (gate_start)
+constexpr uint32_t kRecWords = (1 + kRecLevels + 3) & ~3u;  // record: base level + kRecLevels counts, 16-B padded
 constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shared memory (W <= 8)
 #ifndef GENIE_LOOKUP_THREADS
 #define GENIE_LOOKUP_THREADS 256
