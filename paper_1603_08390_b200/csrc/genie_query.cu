@@ -273,47 +273,76 @@ __global__ void __launch_bounds__(256) k_worklist(BatchParams p) {
 
 // -------------------------------------------------------------------- cut
 
-// One warp per (query, span): the span's list and the positions of every
-// object-tile boundary inside it (lower_bound on the ascending ids).
+// One warp per group of G (query, span)s: lane l < G resolves span l of the
+// group (its query, keyword list and dense slot -- a chain of dependent
+// loads), then the warp's lanes run over the group's flattened (span, tile
+// boundary) pairs: the position of every object-tile boundary inside each
+// list (lower_bound on the ascending ids).  G grows with the span count so
+// batches of many short spans (C4: 128 per query) overlap their header
+// chains instead of resolving one span per warp; G = 1 when spans are few.
 __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
     if (p.st[ST_OVERFLOW]) return;
     const uint64_t total = p.st[ST_TOTAL_SPANS];
-    const int lane = threadIdx.x & 31;
+    const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    for (uint64_t g = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < total;
-         g += nwarps) {
-        // query owning global span g (last q with span_base <= g)
-        const uint32_t q = static_cast<uint32_t>(upper_bound_dev(p.q_span_base, p.Q, g) - 1);
-        const uint32_t s = static_cast<uint32_t>(g - p.q_span_base[q]);
-        const uint64_t i0 = p.item_off[q], i1 = p.item_off[q + 1];
-        const uint64_t it = i0 + upper_bound_dev(p.it_sbase + i0, i1 - i0, s) - 1;
-        const uint64_t j = p.it_kb[it] + (s - p.it_sbase[it]);
-        const uint64_t beg = p.key_off[j];
-        const uint32_t len = static_cast<uint32_t>(p.key_off[j + 1] - beg);
-        // the list's bitmap replaces its posting scan when the list is dense
-        // enough for this query's counter width (bit-sliced / lane-wise adds
-        // per 32 objects vs. an atomic per posting)
-        int32_t ds = p.n_dense ? p.key_dense[j] : -1;
-        const uint32_t inv = p.dense_inv[wclass(p.q_W[q])];
-        if (ds >= 0 && inv && uint64_t(len) * inv < p.n) ds = -1;
-        if (lane == 0) {
+    const uint64_t per = (total + nwarps - 1) / nwarps;
+    const uint32_t G = per < 1 ? 1u : (per > 32 ? 32u : static_cast<uint32_t>(per));
+    for (uint64_t g0 = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * G; g0 < total;
+         g0 += nwarps * G) {
+        const uint64_t g = g0 + lane;
+        uint32_t npair = 0, len = 0, nt = 0, T = 0;
+        uint64_t beg = 0, cbase = 0;
+        if (lane < G && g < total) {
+            // query owning global span g (last q with span_base <= g)
+            const uint32_t q = static_cast<uint32_t>(upper_bound_dev(p.q_span_base, p.Q, g) - 1);
+            const uint32_t s = static_cast<uint32_t>(g - p.q_span_base[q]);
+            const uint64_t i0 = p.item_off[q], i1 = p.item_off[q + 1];
+            const uint64_t it = i0 + upper_bound_dev(p.it_sbase + i0, i1 - i0, s) - 1;
+            const uint64_t j = p.it_kb[it] + (s - p.it_sbase[it]);
+            beg = p.key_off[j];
+            len = static_cast<uint32_t>(p.key_off[j + 1] - beg);
+            // the list's bitmap replaces its posting scan when the list is dense
+            // enough for this query's counter width (bit-sliced / lane-wise adds
+            // per 32 objects vs. an atomic per posting)
+            int32_t ds = p.n_dense ? p.key_dense[j] : -1;
+            const uint32_t inv = p.dense_inv[wclass(p.q_W[q])];
+            if (ds >= 0 && inv && uint64_t(len) * inv < p.n) ds = -1;
             p.span_beg[g] = beg;
             p.span_dense[g] = ds;
             if (ds >= 0) atomicAdd(&p.q_nd[q], 1u);  // dense spans per query
+            // k_scan uses the bitmaps when all of the query's spans fit one
+            // staging batch; then this list needs no tile cuts
+            if (!(ds >= 0 && p.q_S[q] <= kSpanBatch)) {
+                nt = p.q_ntiles[q];
+                T = tile_objs(p, p.q_W[q]);
+                cbase = p.q_cut_base[q] + uint64_t(s) * (nt + 1);
+                npair = nt + 1;
+            }
         }
-        // k_scan uses the bitmaps when all of the query's spans fit one staging
-        // batch; then this list needs no tile cuts
-        if (ds >= 0 && p.q_S[q] <= kSpanBatch) continue;
-        const uint32_t nt = p.q_ntiles[q];
-        const uint32_t T = tile_objs(p, p.q_W[q]);
-        uint32_t* cut = p.cuts + p.q_cut_base[q] + uint64_t(s) * (nt + 1);
-        const uint32_t* list = p.postings + beg;
-        for (uint32_t b = lane; b <= nt; b += 32) {
-            uint32_t v;
-            if (b == 0) v = 0;
-            else if (b == nt) v = len;
-            else v = static_cast<uint32_t>(lower_bound_dev(list, len, b * T));
-            cut[b] = v;
+        const uint32_t incl = warp_inclusive_scan(npair);
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t r = 0; r < tot; r += 32) {
+            const uint32_t idx = r + lane;
+            // owning lane: the number of lanes whose pairs all precede idx
+            uint32_t o = 0;
+#pragma unroll
+            for (uint32_t step = 16; step; step >>= 1)
+                if (__shfl_sync(0xffffffffu, incl, o + step - 1) <= idx) o += step;
+            const uint32_t o_incl = __shfl_sync(0xffffffffu, incl, o & 31);
+            const uint32_t o_np = __shfl_sync(0xffffffffu, npair, o & 31);
+            const uint32_t o_len = __shfl_sync(0xffffffffu, len, o & 31);
+            const uint32_t o_nt = __shfl_sync(0xffffffffu, nt, o & 31);
+            const uint32_t o_T = __shfl_sync(0xffffffffu, T, o & 31);
+            const uint64_t o_beg = __shfl_sync(0xffffffffu, beg, o & 31);
+            const uint64_t o_cb = __shfl_sync(0xffffffffu, cbase, o & 31);
+            if (idx < tot) {
+                const uint32_t b = idx - (o_incl - o_np);
+                uint32_t v;
+                if (b == 0) v = 0;
+                else if (b == o_nt) v = o_len;
+                else v = static_cast<uint32_t>(lower_bound_dev(p.postings + o_beg, o_len, b * o_T));
+                p.cuts[o_cb + b] = v;
+            }
         }
     }
 }
