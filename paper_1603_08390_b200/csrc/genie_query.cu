@@ -128,8 +128,12 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
             if (l > h) {
                 lohi_bad = true;
             } else {
-                const uint64_t a = lower_bound_dev(p.keys, p.K, (uint64_t(d) << 32) | l);
-                const uint64_t e = upper_bound_dev(p.keys, p.K, (uint64_t(d) << 32) | h);
+                const uint64_t kl = (uint64_t(d) << 32) | l;
+                const uint64_t a = lower_bound_dev(p.keys, p.K, kl);
+                // single-token items (the common case) need no second search:
+                // keys are unique, so the range is [a, a + (keys[a] == key))
+                const uint64_t e = l == h ? a + (a < p.K && p.keys[a] == kl)
+                                          : upper_bound_dev(p.keys, p.K, (uint64_t(d) << 32) | h);
                 kb = static_cast<uint32_t>(a);
                 nk = static_cast<uint32_t>(e - a);
                 pp = p.key_off[e] - p.key_off[a];
