@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
     const uint64_t total = p.st[ST_TOTAL_SPANS];
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-    const uint64_t per = (total + nwarps - 1) / nwarps;
+    const uint64_t per = (total * GENIE_CUT_GROUP_MUL + nwarps - 1) / nwarps;
     const uint32_t G = per < 1 ? 1u : (per > 32 ? 32u : static_cast<uint32_t>(per));
     for (uint64_t g0 = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * G; g0 < total;
          g0 += nwarps * G) {

@@ -33,6 +33,9 @@ constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shar
 #ifndef GENIE_LOOKUP_THREADS
 #define GENIE_LOOKUP_THREADS 256
 #endif
+#ifndef GENIE_CUT_GROUP_MUL  // k_cut spans per warp = clamp(mul x spans / warps, 1, 32)
+#define GENIE_CUT_GROUP_MUL 2
+#endif
 #ifndef GENIE_CUT_CTAS
 #define GENIE_CUT_CTAS 32
 #endif
