@@ -315,6 +315,27 @@ def test_many_spans_per_query(gpu, oracle, tile_bytes):
         assert_same(ix.query(qb, config(selector=sel, tile_bytes=tile_bytes)), want, f"spans tile {tile_bytes} sel {sel}")
 
 
+@pytest.mark.parametrize("tile_bytes", [4096, 16384])
+def test_many_queries_grouped_cuts(gpu, oracle, tile_bytes):
+    # ~72K (query, keyword list) spans in one batch: more spans than k_cut has
+    # warps, so each warp resolves a group of spans lane-parallel and cuts
+    # their flattened (span, tile boundary) pairs (the C4 shape: many short
+    # single-token items per query, many tiles per query).
+    rng = np.random.default_rng(5)
+    n, ndim, ntok, Q, m = 200_000, 32, 128, 3000, 24
+    off = (np.arange(n + 1, dtype=np.uint64) * ndim)
+    dims = np.tile(np.arange(ndim, dtype=np.uint16), n)
+    toks = rng.integers(0, ntok, size=n * ndim).astype(np.uint32)
+    csr = synth.csr_from_objects(n, off, dims, toks)
+    qdim = np.concatenate([rng.permutation(ndim)[:m] for _ in range(Q)]).astype(np.uint16)
+    qtok = rng.integers(0, ntok, size=Q * m).astype(np.uint32)
+    qb = QueryBatch(np.arange(Q, dtype=np.uint32), rng.integers(1, 150, size=Q).astype(np.uint32),
+                    (np.arange(Q + 1, dtype=np.uint64) * m), qdim, qtok, qtok)
+    want = oracle.index(csr).execute(qb)
+    ix = DeviceIndex.from_csr(csr, device=gpu)
+    assert_same(ix.query(qb, config(tile_bytes=tile_bytes)), want, f"grouped cuts tile {tile_bytes}")
+
+
 def test_mcix_image_loads_into_the_device_index(gpu, oracle, tmp_path):
     # load_index (index_io.hpp:148-154) straight into device memory: the same
     # CSR back, the same answers as the oracle
