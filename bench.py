@@ -81,8 +81,11 @@ def dist_env():
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    polled every ~2 ms from a thread (a C2 timed region is only ~25 ms long);
+    nvidia-smi -lms 50 when NVML is unavailable."""
 
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -91,8 +94,28 @@ class ClockSampler:
         self.gpu = gpu
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, reasons bitmask)
+        self.max_mhz = None
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            idx = self.gpu
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis and vis.split(",")[0].strip().isdigit():
+                idx = int(vis.split(",")[self.gpu].strip())
+            self.h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.nvml = nv
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                                           "-i", str(self.gpu), "-lms", "50"], stdout=subprocess.PIPE,
@@ -103,11 +126,32 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop.is_set():
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                                     int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml:
+            self.t.join(timeout=2)
+            if not self.samples:  # region shorter than one poll: take one now
+                self.stop.clear()
+                try:
+                    nv = self.nvml
+                    self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                                         int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+                except Exception:
+                    pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -118,7 +162,15 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if self.nvml:
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
+            for mhz, r in self.samples:
+                sm.append(mhz)
+                for nm, b in bits.items():
+                    if r & b:
+                        reasons.add(nm)
+            mx = self.max_mhz or 0.0
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
@@ -128,12 +180,13 @@ class ClockSampler:
                 mx = max(mx, float(parts[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[5:9]):
+            for nm, v in zip(self.NAMES, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml (2 ms poll)" if self.nvml else "nvidia-smi -lms 50"}
 
 
 # --------------------------------------------------------------- workloads
@@ -283,14 +336,17 @@ class Workload:
 # --------------------------------------------------------------- reference
 
 def reference_qps(w: Workload, sample: int, steps: int, warmup: int):
-    """The reference CPU engine on the box's cores over a bounded query sample
-    of the same index: mcx::execute_batch (Selector::cpq, parallel, all
-    threads; oracle/_ref) for C1/C2, the C port (oracle/, all threads) for
-    C3-C5.  Returns (qps per step, cores, kind, build seconds)."""
+    """The reference CPU engine on the box's cores over `sample` queries of
+    the same index per step (the whole batch for C1/C2): mcx::execute_batch
+    (Selector::cpq, ExecMode::parallel, workers = hardware threads;
+    oracle/_ref) for C1/C2, the plain-C port (oracle/, all threads) for C3-C5.
+    Returns (qps per timed step, cores, kind, build seconds, StageTimings per
+    timed step or None)."""
     from oracle.pyoracle import Oracle, RefLib, threads
 
     csr = w.cpu_csr()
     t0 = time.perf_counter()
+    stages = []
     if w.m is None:
         ref = RefLib()
         rix = ref.index(csr)
@@ -300,6 +356,7 @@ def reference_qps(w: Workload, sample: int, steps: int, warmup: int):
             rc, r = rix.execute(b, selector=0, sequential=False, workers=0)
             if rc:
                 raise RuntimeError(r)
+            return r.timings
     else:
         o = Oracle()
         oix = o.index(csr)
@@ -307,22 +364,34 @@ def reference_qps(w: Workload, sample: int, steps: int, warmup: int):
 
         def run(b):
             oix.execute(b, nthreads=cores)
+            return None
     build_s = time.perf_counter() - t0
     per_step = []
     Q = len(w.batch)
+    sample = min(sample, Q)
     for s in range(warmup + steps):
         a = (s * sample) % max(1, Q - sample + 1)
         b = w.batch.slice(a, a + sample)
         t = time.perf_counter()
-        run(b)
+        tm = run(b)
         dt = time.perf_counter() - t
         if s >= warmup:
             per_step.append(sample / dt)
-    return per_step, cores, kind, build_s
+            stages.append(tm)
+    return per_step, cores, kind, build_s, (stages if stages and stages[0] else None)
+
+
+def stage_summary(stages):
+    """Median StageTimings (engine.hpp:44-50) of the timed reference runs, ms."""
+    if not stages:
+        return None
+    return {k.replace("_ns", "_ms"): round(float(np.median([s[k] for s in stages])) / 1e6, 2)
+            for k in ("lookup_ns", "match_ns", "select_ns", "total_ns")}
 
 
 def default_sample(name: str) -> int:
-    return {"tweets": 96, "adult": 512, "sift": 16, "minhash": 512, "ocr": 16}[name]
+    # C1/C2: the whole batch (BASELINE.md 3); C3-C5: a bounded prefix
+    return {"tweets": 1024, "adult": 1024, "sift": 16, "minhash": 512, "ocr": 16}[name]
 
 
 def run_reference_arm(args):
@@ -345,24 +414,87 @@ def run_reference_arm(args):
         w.cpu_csr = lambda: ds.csr
     else:
         w = Workload(args, 0, 1, dev, local)  # tokens via the GPU encoder (inputs only)
-    sample = args.ref_sample or default_sample(args.workload)
-    qps, cores, kind, build_s = reference_qps(w, sample, args.steps, args.warmup)
-    value = float(np.mean(qps))
+    sample = min(args.ref_sample or default_sample(args.workload), len(w.batch))
+    qps, cores, kind, build_s, stages = reference_qps(w, sample, args.steps, args.warmup)
+    value = float(len(qps) * sample / np.sum([sample / v for v in qps]))  # queries / total time
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000.0 * sample / value, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded generator, SURVEY.md 8d)",
         "config": {"workload": WORKLOADS[args.workload], "queries_per_step": sample,
+                   "same_batch_as_genie_arm": sample == len(w.batch), "stage_ms_median": stage_summary(stages),
                    "engine": ("mcx::execute_batch Selector::cpq ExecMode::parallel (unmodified reference headers)"
                               if kind == "reference" else "plain-C port of mcx::execute_batch (oracle/)")},
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"{sample} queries per step of the {len(w.batch)}-query batch; "
-                                   f"CPU index build {build_s:.1f}s untimed"},
+                         "sample": (f"the whole {sample}-query batch per step" if sample == len(w.batch) else
+                                    f"{sample} queries per step of the {len(w.batch)}-query batch")
+                                   + f"; CPU index build {build_s:.1f}s untimed"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ---------------------------------------------------------------- roofline
+
+def scan_roofline(workload, world, postings, scan_ms, clocks, sms):
+    """Roofline of k_scan, the dominant kernel.
+
+    The bound is the one ncu shows (profiles/scan_counters.json, captured for
+    the CURRENT kernel sources -- an entry whose source_sha differs is stale
+    and not used): SM instruction issue.  achieved = warp instructions per
+    launch (ncu smsp__inst_executed.sum) / the live k_scan time (CUDA events
+    on the launching stream); peak = SMs x 4 schedulers x 1 warp-inst/cycle x
+    the SM clock sampled during the timed region.  HBM is reported beside it:
+    DRAM bytes per launch (ncu) / live time vs the measured copy bandwidth,
+    and the algorithmic bytes (4 B x sum_q P_q) as a diagnostic --
+    the latter exceed what the kernel moves because dense lists are read as
+    bitmaps and hot lists stay in L2 across the tile-major sweep."""
+    from tools.scan_counters import kernel_source_sha
+
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    if peaks_path.exists():
+        hbm_peak = float(json.loads(peaks_path.read_text())["hbm_gbs"])
+        hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        hbm_peak, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    alg_bytes = 4 * postings
+    entry, stale = None, None
+    cpath = ROOT / "profiles" / "scan_counters.json"
+    if cpath.exists():
+        e = json.loads(cpath.read_text()).get(workload)
+        if e and e.get("n_gpus", 1) == world:
+            if e.get("source_sha") == kernel_source_sha():
+                entry = e
+            else:
+                stale = e.get("source_sha")
+    mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    issue_peak = sms * 4 * mhz * 1e6 / 1e9  # G warp-instructions / s
+    out = {"bound": "issue", "unit": "Gwarp-inst/s", "peak": round(issue_peak, 1),
+           "peak_source": f"{sms} SMs x 4 schedulers x 1 warp-inst/cycle x {mhz:.0f} MHz (sampled)",
+           "kernel": "k_scan (fused posting scan + c-PQ gate/table + tile top-k)", "kernel_ms": round(scan_ms, 4),
+           "achieved": None, "frac": None, "traffic": None}
+    if entry:
+        ach = entry["warp_inst_per_launch"] / (scan_ms / 1e3) / 1e9
+        out.update({"achieved": round(ach, 1), "frac": round(ach / issue_peak, 4),
+                    "traffic": entry["dram_bytes_per_launch"],
+                    "warp_inst_per_launch": entry["warp_inst_per_launch"],
+                    "counters": {k: entry[k] for k in ("source_sha", "ncu_duration_ms", "issue_active_pct",
+                                                       "ipc_per_sm", "occupancy_pct", "l2_atom_sectors",
+                                                       "l2_red_sectors", "smem_atom_wavefronts", "l2_hit_pct",
+                                                       "l2_throughput_pct", "registers") if k in entry}})
+    else:
+        out["note"] = ("no ncu counters for these kernel sources" +
+                       (f" (profiles/scan_counters.json entry is stale: {stale})" if stale else ""))
+    dram_gbs = (entry["dram_bytes_per_launch"] / (scan_ms / 1e3) / 1e9) if entry else None
+    out["hbm"] = {"peak": hbm_peak, "peak_source": hbm_src, "unit": "GB/s",
+                  "dram_achieved": round(dram_gbs, 1) if dram_gbs else None,
+                  "dram_frac": round(dram_gbs / hbm_peak, 4) if dram_gbs else None,
+                  "algorithmic_bytes_per_launch": alg_bytes,
+                  "algorithmic_gbs": round(alg_bytes / (scan_ms / 1e3) / 1e9, 1),
+                  "note": "algorithmic = 4 B x sum_q P_q (SURVEY 8d); a diagnostic, not a roofline fraction"}
+    return out
 
 
 # ------------------------------------------------------------------- genie
@@ -505,36 +637,22 @@ def main_genie(args):
     e2e_value = Q / e2e_s
 
     # ---- roofline of the dominant kernel (k_scan: fused scan + c-PQ + tile select)
-    peaks_path = ROOT / "MEASURED_PEAKS.json"
-    if peaks_path.exists():
-        peak = float(json.loads(peaks_path.read_text())["hbm_gbs"])
-        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
-    else:
-        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    roof = scan_roofline(args.workload, world, int(stats["postings"]), float(np.mean(scan_ms)), clocks.summary(),
+                         torch.cuda.get_device_properties(dev).multi_processor_count)
     postings = int(stats["postings"])
-    alg_bytes = 4 * postings  # one u32 posting id per (query, posting)
-    scan_avg_ms = float(np.mean(scan_ms))
-    achieved = alg_bytes / (scan_avg_ms / 1000.0) / 1e9
-    traffic = None
-    tpath = ROOT / "profiles" / "scan_dram_bytes.json"
-    if tpath.exists():
-        try:
-            tj = json.loads(tpath.read_text())
-            entry = tj.get(args.workload) if args.workload in tj else (tj if tj.get("workload") == args.workload else None)
-            if entry and entry.get("n_gpus", 1) == world:
-                traffic = entry.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
 
-    # ---- CPU baseline (reference engine on the host cores; rank 0, N = 1)
+    # ---- CPU baseline (reference engine on the host cores; rank 0, N = 1):
+    # the whole C1/C2 batch, median of 3 runs
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            sample = args.ref_sample or default_sample(args.workload)
-            qps, cores, kind, build_ref_s = reference_qps(w, sample, steps=1, warmup=0)
-            cpu = {"value": round(float(np.mean(qps)), 3), "unit": UNIT, "cores": cores, "kind": kind,
-                   "sample": f"first {sample} of the {Q} queries on the same index ({cores} threads); "
-                             f"CPU index build {build_ref_s:.1f}s untimed"}
+            sample = min(args.ref_sample or default_sample(args.workload), Q)
+            qps, cores, kind, build_ref_s, stages = reference_qps(w, sample, steps=3, warmup=0)
+            cpu = {"value": round(float(np.median(qps)), 3), "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": (f"the whole {Q}-query batch" if sample == Q else f"first {sample} of the {Q} queries")
+                             + f", median of 3 runs on the same index ({cores} threads; CPU index build "
+                               f"{build_ref_s:.1f}s untimed)",
+                   "stage_ms_median": stage_summary(stages)}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -554,17 +672,11 @@ def main_genie(args):
                     "d2h_bytes_per_step": int(d2h_bytes),
                     "path": ("genie_lsh_encode + " if w.m else "") + "genie_query_batch (C ABI), pinned host buffers"
                             + (" + all-gather + genie_merge_topk_device" if world > 1 else "")},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "k_scan (fused posting scan + c-PQ gate/table + tile top-k)",
-                         "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": round(scan_avg_ms, 4),
-                         "peak_source": peak_src,
-                         "note": "algorithmic bytes = 4 B x sum_q P_q; hot lists shared by many queries stay "
-                                 "L2-resident across the tile-major sweep, so DRAM traffic is far below them"},
+            "roofline": roof,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clocks.summary(),
-            "stage_ms": {"step_mean": round(float(np.mean(step_ms)), 4), "scan_mean": round(scan_avg_ms, 4),
+            "stage_ms": {"step_mean": round(float(np.mean(step_ms)), 4), "scan_mean": round(float(np.mean(scan_ms)), 4),
                          "lookup_mean": round(float(np.mean(look_ms)), 4),
                          "merge_mean": round(float(np.mean(merge_ms)), 4)},
             "fallback_tiles": int(st.get("fallback_tiles", 0)), "work_items": int(st.get("work_items", 0)),

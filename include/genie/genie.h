@@ -170,7 +170,12 @@ int genie_index_dim_stats(genie_index* ix, uint32_t* dim_max_mult, char* err, si
  * out_bound (optional, Q) receives max_count_bound per query.
  * Errors: k == 0, empty query, lo > hi -> CONTRACT ("Query N: ..."), bound >
  * 0xffff -> CONTRACT "query N (setup): ...", table overflow never surfaces
- * (exact fallback), CUDA failures -> CUDA. */
+ * (exact fallback), CUDA failures -> CUDA.
+ * Counter range: the device counters are 4/8/16-bit for EVERY selector, so
+ * the bound > 0xffff ContractError (engine.hpp:230-233) also applies to
+ * GENIE_SELECT_BUCKET / GENIE_SELECT_SORT, whose reference counterparts use
+ * 32-bit counters and would answer such a query (a divergence only for
+ * queries matching one object more than 65 535 times). */
 int genie_query_batch(genie_index* ix, const genie_config* cfg, uint32_t num_queries,
                       const uint32_t* qid, const uint32_t* k, const uint64_t* item_off,
                       const uint16_t* item_dim, const uint32_t* item_lo, const uint32_t* item_hi,

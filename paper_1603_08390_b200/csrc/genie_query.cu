@@ -2070,6 +2070,9 @@ __global__ void __launch_bounds__(THREADS) k_merge(MergeSrc m, uint32_t cap) {
     __shared__ unsigned long long sums[32];
     __shared__ uint32_t s_flag, s_pos;
     __shared__ uint32_t s_scratch[256 + 8];
+    // a workspace overflow skipped k_worklist..k_scan: tile_len / tile_out
+    // hold nothing of this batch (the host grows the workspace and retries)
+    if (m.st[ST_OVERFLOW]) return;
     for (uint32_t q = blockIdx.x; q < m.Q; q += gridDim.x) {
         const uint32_t L = nlists_of(m, q);
         const uint32_t kq = m.k[q];
@@ -2162,6 +2165,8 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_big(MergeSrc m) {
     __shared__ uint32_t s_sel;
     __shared__ unsigned long long s_cum;
     __shared__ uint32_t s_pos;
+    __shared__ uint32_t s_dup;
+    if (m.st[ST_OVERFLOW]) return;  // see k_merge
     for (uint32_t q = blockIdx.x; q < m.Q; q += gridDim.x) {
         if (!m.q_big[q]) continue;
         const uint32_t L = nlists_of(m, q);
@@ -2260,10 +2265,16 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_big(MergeSrc m) {
             }
             id_cut = idp;
         }
-        // --- emit the winners into the output row
-        if (threadIdx.x == 0) s_pos = 0;
+        // --- emit the winners into the output row.  Exactly min(k, M)
+        // entries pass unless an id repeats across lists (mode 1: a
+        // ContractError, engine.hpp:165-172); writes stay inside the row.
+        if (threadIdx.x == 0) {
+            s_pos = 0;
+            s_dup = 0;
+        }
         __syncthreads();
         genie_entry* row = m.out + uint64_t(q) * m.out_stride;
+        const uint32_t lim = static_cast<uint32_t>(min(all ? M : static_cast<unsigned long long>(kq), static_cast<unsigned long long>(m.out_stride)));
         for (uint32_t l = 0; l < L; ++l) {
             const genie_entry* b;
             uint32_t len;
@@ -2272,12 +2283,26 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_big(MergeSrc m) {
                 const genie_entry x = b[e];
                 if (all || x.count > T || (x.count == T && x.id <= id_cut)) {
                     const uint32_t pos = atomicAdd(&s_pos, 1u);
-                    row[pos] = x;
+                    if (pos < lim) row[pos] = x;
+                    else s_dup = 1;
                 }
             }
         }
         __syncthreads();
-        const uint32_t outn = s_pos;
+        const uint32_t outn = min(s_pos, lim);
+        if (m.mode == 1 && outn <= kSortCap) {
+            // duplicate ids among the winners (sorted by id, adjacent pairs)
+            uint32_t N = 1;
+            while (N < outn) N <<= 1;
+            for (uint32_t i = threadIdx.x; i < N; i += blockDim.x)
+                keys[i] = i < outn ? (uint64_t(row[i].id) << 32) | row[i].count : ~0ull;
+            __syncthreads();
+            bitonic_sort_smem(keys, N);
+            for (uint32_t i = threadIdx.x + 1; i < outn; i += blockDim.x)
+                if ((keys[i] >> 32) == (keys[i - 1] >> 32)) s_dup = 1;
+            __syncthreads();
+        }
+        if (m.mode == 1 && s_dup && threadIdx.x == 0) atomicMin(&m.st[ST_MERGE_DUP], (unsigned long long)q);
         if (outn <= kSortCap) {
             uint32_t N = 1;
             while (N < outn) N <<= 1;
@@ -2345,6 +2370,18 @@ int sm_count(int device) {
 }
 
 void ensure_device(int device) { GENIE_CUDA(cudaSetDevice(device)); }
+
+// Per-device launch attributes already applied (cudaFuncSetAttribute is
+// per device context).  Guarded by the handle's single-controlling-thread
+// contract; distinct handles on one device set the same values.
+struct DeviceAttrCache {
+    size_t scan_smem = 0;
+    bool merge_set = false;
+};
+static DeviceAttrCache& attr_cache(int device) {
+    static DeviceAttrCache caches[kMaxDevices];
+    return caches[device >= 0 && device < kMaxDevices ? device : 0];
+}
 
 static void reserve_workspace(genie_index* ix, uint32_t Q, uint32_t items, uint32_t max_k,
                               uint32_t out_stride, uint32_t tile_bits) {
@@ -2640,11 +2677,13 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
         p.ht_slots = kHtSlots;
         const size_t smem = scan_smem_bytes(tile_bytes, p.ht_slots);
-        static thread_local size_t configured = 0;
-        if (configured < smem) {
+        // cudaFuncSetAttribute applies per device context: cached per device
+        // (one host thread may drive several devices, genie_group_*)
+        DeviceAttrCache& ac = attr_cache(ix->device);
+        if (ac.scan_smem < smem) {
             GENIE_CUDA(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
-            configured = smem;
+            ac.scan_smem = smem;
         }
         uint32_t per_sm = cfg.ctas_per_sm ? cfg.ctas_per_sm : 0;
         if (!per_sm) {
@@ -2657,14 +2696,13 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
         const MergeSrc m = tile_merge_src(ix, Q, d_k, out_stride, d_out, d_out_len, d_out_thr);
         const size_t msmem = kSortCap * sizeof(uint64_t);
-        static thread_local bool mconf = false;
-        if (!mconf) {
+        if (!ac.merge_set) {
             GENIE_CUDA(cudaFuncSetAttribute(k_merge<kMergeSmallThreads>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(kMergeSmallCap * sizeof(uint64_t))));
             GENIE_CUDA(cudaFuncSetAttribute(k_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(msmem)));
-            mconf = true;
+            ac.merge_set = true;
         }
         const uint32_t mgrid = std::min<uint32_t>(Q, sms * 4);
         // one small CTA per query: after the floors prune them, unions are a

@@ -74,6 +74,7 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 constexpr int kScanUnroll = GENIE_SCAN_UNROLL;               // 128-posting groups loaded per warp pass
 constexpr uint32_t kStaticGroups = 64;        // <= this many 128-posting groups per warp: static split
 constexpr uint64_t kEmptySlot = ~0ull;
+constexpr int kMaxDevices = 64;              // per-device host caches (launch attributes)
 
 // Status block words (u64) written by the device pipeline.
 enum StatusWord : int {
