@@ -62,7 +62,8 @@ typedef struct {
  * engine.hpp:186-188 (use genie_config_default()). */
 typedef struct {
     uint32_t selector;           /* genie_selector */
-    uint32_t span_chunk;         /* postings per warp work unit (rounded up to 128) */
+    uint32_t span_chunk;         /* ids per chunk (engine.hpp:40, default 4096); a scan warp claims
+                                    span_chunk / 4 postings at a time (rounded up to 128) */
     uint32_t max_spans_per_task; /* accepted for API parity; must be > 0 */
     uint32_t tile_bytes;         /* shared-memory counter bytes per object tile (0: default) */
     uint32_t ctas_per_sm;        /* persistent scan CTAs per SM (0: default) */
@@ -142,6 +143,19 @@ int genie_index_load_mcix(const uint8_t* data, uint64_t size, int device, genie_
 int genie_mcix_serialize(uint32_t num_objects, uint64_t num_keys, const uint64_t* keys, const uint64_t* key_off,
                          const uint32_t* postings, uint32_t split, uint8_t* out, uint64_t* size, char* err,
                          size_t errlen);
+
+/* The span structure of an image (InvertedIndex::entries()/spans(),
+ * index.hpp:41-73) for hosts that keep it (mcx::deserialize_index, which
+ * re-serializes byte-identically, test_index.cpp:222-236): validates like
+ * genie_mcix_parse; shape call with null arrays gives *num_spans, the fill call
+ * writes span_count[K] and span_bounds[2 * num_spans] (begin, end pairs). */
+int genie_mcix_parse_spans(const uint8_t* data, uint64_t size, uint64_t* num_spans, uint16_t* span_count,
+                           uint64_t* span_bounds, char* err, size_t errlen);
+/* serialize_index (index_io.hpp:63-82) of an index with explicit spans:
+ * keyword j owns span_count[j] consecutive (begin, end) pairs of span_bounds. */
+int genie_mcix_serialize_spans(uint32_t num_objects, uint64_t num_keys, const uint64_t* keys,
+                               const uint16_t* span_count, const uint64_t* span_bounds, uint64_t num_postings,
+                               const uint32_t* postings, uint8_t* out, uint64_t* size, char* err, size_t errlen);
 
 /* build_index (index.hpp:190-250) on the device: object o owns keywords
  * [obj_off[o], obj_off[o+1]) of dims / tokens (host arrays; ids dense 0..n-1).
@@ -226,6 +240,15 @@ int genie_merge_topk_device(genie_index* ix, uint32_t num_queries, uint32_t num_
                             const uint32_t* d_k, uint32_t out_stride, genie_entry* d_out,
                             uint32_t* d_out_len, uint32_t* d_out_threshold, void* stream,
                             char* err, size_t errlen);
+/* Same with the lists in list-major order when list_major != 0: list l of
+ * query q at d_in[(l*Q + q)*in_stride ...], length d_in_len[l*Q + q] -- the
+ * layout an all-gather of per-shard [Q][in_stride] rows produces, merged in
+ * place without a transpose. */
+int genie_merge_topk_device_layout(genie_index* ix, uint32_t num_queries, uint32_t num_lists,
+                                   const genie_entry* d_in, const uint32_t* d_in_len, uint32_t in_stride,
+                                   uint32_t list_major, const uint32_t* d_k, uint32_t out_stride,
+                                   genie_entry* d_out, uint32_t* d_out_len, uint32_t* d_out_threshold,
+                                   void* stream, char* err, size_t errlen);
 
 /* Host variant of the batched merge (runs on `device`). */
 int genie_merge_topk(int device, uint32_t num_queries, uint32_t num_lists, const genie_entry* in,

@@ -15,9 +15,11 @@
 
 #include <algorithm>
 #include <cctype>
+#include <chrono>
 #include <cstdio>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <set>
 #include <span>
@@ -59,6 +61,16 @@ inline void check(int rc, const char* msg) {
     if (rc != GENIE_OK) raise(rc, msg);
 }
 }  // namespace detail
+
+// ------------------------------------------------------------------ rng.hpp
+
+// splitmix64 finalizer (rng.hpp:25-30): the hash every seed and table home uses
+inline constexpr std::uint64_t mix64(std::uint64_t x) noexcept {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
 
 // ---------------------------------------------------------------- model.hpp
 
@@ -124,6 +136,60 @@ inline std::uint32_t match_count_reference(const Query& q, const ObjectRecord& o
     return total;
 }
 
+// Relational tables (model.hpp:119-188): one keyword per attribute (dim =
+// attribute index); query ranges are clamped into the attribute's domain.
+class RelationalSchema {
+public:
+    explicit RelationalSchema(std::vector<Token> domain_sizes) : dom_(std::move(domain_sizes)) {
+        if (dom_.empty()) throw ContractError("RelationalSchema: empty schema");
+        for (std::size_t a = 0; a < dom_.size(); ++a)
+            if (!dom_[a]) throw ContractError("RelationalSchema: attribute " + std::to_string(a) + " has empty domain");
+    }
+    std::size_t attribute_count() const noexcept { return dom_.size(); }
+    Token domain_size(std::size_t attr) const { return dom_.at(attr); }
+
+private:
+    std::vector<Token> dom_;
+};
+
+inline ObjectRecord encode_relational_tuple(const RelationalSchema& schema, std::span<const Token> values,
+                                            ObjectId id) {
+    if (values.size() != schema.attribute_count())
+        throw ContractError("tuple arity " + std::to_string(values.size()) + " != schema arity " +
+                            std::to_string(schema.attribute_count()));
+    std::vector<Keyword> kws(values.size());
+    for (std::size_t a = 0; a < values.size(); ++a) {
+        if (values[a] >= schema.domain_size(a))
+            throw DataError("attribute " + std::to_string(a) + ": token " + std::to_string(values[a]) +
+                            " outside domain [0, " + std::to_string(schema.domain_size(a)) + ")");
+        kws[a] = Keyword{DimId(a), values[a]};
+    }
+    return ObjectRecord(id, std::move(kws));
+}
+
+struct AttributeRange {
+    std::size_t attr = 0;
+    std::int64_t lo = 0;  // before clamping; may lie outside the domain
+    std::int64_t hi = 0;
+};
+
+inline Query encode_relational_query(const RelationalSchema& schema, std::span<const AttributeRange> ranges,
+                                     std::uint32_t k, std::uint32_t query_id = 0) {
+    std::vector<QueryItem> items;
+    items.reserve(ranges.size());
+    for (const auto& r : ranges) {
+        if (r.attr >= schema.attribute_count())
+            throw ContractError("range on unknown attribute " + std::to_string(r.attr));
+        const std::int64_t dom = schema.domain_size(r.attr);
+        const std::int64_t lo = std::max<std::int64_t>(r.lo, 0), hi = std::min<std::int64_t>(r.hi, dom - 1);
+        if (lo > hi)
+            throw DataError("attribute " + std::to_string(r.attr) + ": range [" + std::to_string(r.lo) + ", " +
+                            std::to_string(r.hi) + "] is empty after clamping to [0, " + std::to_string(dom) + ")");
+        items.emplace_back(DimId(r.attr), Token(lo), Token(hi));
+    }
+    return Query(query_id, std::move(items), k);
+}
+
 // ------------------------------------------------------------------ cpq.hpp
 
 struct TopKEntry {
@@ -151,109 +217,275 @@ struct PostingsSpan {
 
 inline constexpr std::uint32_t kDefaultSplitThreshold = 4096;
 
-// The host CSR (keys ascending, ids ascending per key) plus its device copy.
+// InvertedIndex (index.hpp:41-182): the reference's host view -- keyword
+// entries sorted by keyword, each owning span_count consecutive spans of one
+// list array -- kept verbatim so callers that walk entries()/spans() work
+// unchanged.  Queries run on the device copy, a CSR image of the same lists
+// uploaded on first use (device()); the spans of a keyword are contiguous, so
+// the CSR row of entry j is [spans[first_span].begin, last span's end).
 class InvertedIndex {
 public:
+    struct KeywordEntry {
+        Keyword keyword;
+        std::uint32_t first_span = 0;
+        std::uint16_t span_count = 0;
+    };
+    struct DimStats {
+        DimId dim = 0;
+        Token max_token = 0;
+        std::uint32_t max_multiplicity = 0;  // most tokens one object carries in the dim
+    };
+
     InvertedIndex() = default;
-    InvertedIndex(std::uint32_t n, std::vector<std::uint64_t> keys, std::vector<std::uint64_t> off,
-                  std::vector<ObjectId> post, std::optional<std::uint32_t> split, int device = 0)
-        : n_(n), keys_(std::move(keys)), off_(std::move(off)), post_(std::move(post)), split_(split),
-          device_(device) {}
+    InvertedIndex(std::uint32_t num_objects, std::vector<KeywordEntry> entries, std::vector<PostingsSpan> spans,
+                  std::vector<ObjectId> list_array, std::optional<std::uint32_t> split_threshold, int device = 0)
+        : n_(num_objects), entries_(std::move(entries)), spans_(std::move(spans)), list_(std::move(list_array)),
+          split_(split_threshold), device_(device), lazy_(std::make_shared<Lazy>()) {}
 
     std::uint32_t num_objects() const noexcept { return n_; }
-    std::size_t keyword_count() const noexcept { return keys_.size(); }
-    const std::vector<ObjectId>& list_array() const noexcept { return post_; }
+    std::size_t keyword_count() const noexcept { return entries_.size(); }
+    const std::vector<KeywordEntry>& entries() const noexcept { return entries_; }
+    const std::vector<PostingsSpan>& spans() const noexcept { return spans_; }
+    const std::vector<ObjectId>& list_array() const noexcept { return list_; }
     std::optional<std::uint32_t> split_threshold() const noexcept { return split_; }
-    // the CSR image: packed keywords (ascending) and their postings offsets
-    const std::vector<std::uint64_t>& packed_keys() const noexcept { return keys_; }
-    const std::vector<std::uint64_t>& key_offsets() const noexcept { return off_; }
+    int device_id() const noexcept { return device_; }
 
-    // spans of every indexed keyword inside the item's range (index.hpp:86-96)
+    std::span<const ObjectId> ids(const PostingsSpan& s) const {
+        return std::span<const ObjectId>(list_).subspan(s.begin, s.length());
+    }
+    std::span<const PostingsSpan> spans_of(const KeywordEntry& e) const {
+        return std::span<const PostingsSpan>(spans_).subspan(e.first_span, e.span_count);
+    }
+
+    // index.hpp:86-96: the spans of every indexed keyword of the item's range
+    void lookup_into(const QueryItem& item, std::vector<PostingsSpan>& out) const {
+        const auto [a, b] = keyword_range(item);
+        for (auto j = a; j < b; ++j) {
+            const auto ss = spans_of(entries_[j]);
+            out.insert(out.end(), ss.begin(), ss.end());
+        }
+    }
     std::vector<PostingsSpan> lookup(const QueryItem& item) const {
         std::vector<PostingsSpan> out;
-        auto a = std::lower_bound(keys_.begin(), keys_.end(), Keyword{item.dim, item.lo}.packed());
-        auto b = std::upper_bound(keys_.begin(), keys_.end(), Keyword{item.dim, item.hi}.packed());
-        for (auto j = std::size_t(a - keys_.begin()); j < std::size_t(b - keys_.begin()); ++j) {
-            const std::uint64_t lim = split_ ? *split_ : off_[j + 1] - off_[j];
-            for (std::uint64_t p = off_[j]; p < off_[j + 1]; p += lim) out.push_back({p, std::min(off_[j + 1], p + lim)});
-        }
+        lookup_into(item, out);
         return out;
     }
-    std::span<const ObjectId> ids(const PostingsSpan& s) const {
-        return std::span<const ObjectId>(post_).subspan(s.begin, s.length());
+
+    std::optional<Token> max_token(DimId dim) const {
+        const DimStats* s = find_dim(dim);
+        if (!s) return std::nullopt;
+        return s->max_token;
+    }
+    std::uint32_t max_multiplicity(DimId dim) const {
+        const DimStats* s = find_dim(dim);
+        return s ? s->max_multiplicity : 0;
+    }
+    // index.hpp:118-133: sum over items of min(#keywords in range, max multiplicity)
+    std::uint64_t max_count_bound(const Query& q) const {
+        std::uint64_t bound = 0;
+        for (const auto& it : q.items) {
+            const auto [a, b] = keyword_range(it);
+            bound += std::min<std::uint64_t>(b - a, max_multiplicity(it.dim));
+        }
+        return bound;
+    }
+    std::uint64_t longest_list() const {
+        std::uint64_t best = 0;
+        for (const auto& e : entries_) {
+            std::uint64_t len = 0;
+            for (const auto& s : spans_of(e)) len += s.length();
+            best = std::max(best, len);
+        }
+        return best;
     }
 
+    // CSR image of the lists (packed keywords ascending, row offsets, ids)
+    std::vector<std::uint64_t> packed_keys() const {
+        std::vector<std::uint64_t> k(entries_.size());
+        for (std::size_t j = 0; j < entries_.size(); ++j) k[j] = entries_[j].keyword.packed();
+        return k;
+    }
+
+    // the device index (uploaded once; shared by copies of this object)
     genie_index* device() const {
-        if (!dev_) {
+        std::call_once(lazy_->dev_once, [&] {
+            std::vector<std::uint64_t> off(entries_.size() + 1, 0);
+            std::vector<ObjectId> gathered;
+            const ObjectId* post = list_.data();
+            if (tiles_in_order()) {
+                for (std::size_t j = 0; j < entries_.size(); ++j)
+                    off[j] = entries_[j].span_count ? spans_[entries_[j].first_span].begin : (j ? off[j - 1] : 0);
+                off[entries_.size()] = list_.size();
+            } else {  // arbitrary span placement: gather each keyword's spans into one row
+                for (std::size_t j = 0; j < entries_.size(); ++j) {
+                    for (const auto& s : spans_of(entries_[j])) {
+                        const auto v = ids(s);
+                        gathered.insert(gathered.end(), v.begin(), v.end());
+                    }
+                    off[j + 1] = gathered.size();
+                }
+                post = gathered.data();
+            }
+            const auto keys = packed_keys();
             genie_index* h = nullptr;
             char err[512] = {};
-            const std::uint64_t zero = 0;
-            detail::check(genie_index_create(n_, keys_.size(), keys_.data(), off_.empty() ? &zero : off_.data(),
-                                             post_.data(), nullptr, 0, device_, &h, err, sizeof(err)),
+            detail::check(genie_index_create(n_, keys.size(), keys.data(), off.data(), post, nullptr, 0, device_, &h,
+                                             err, sizeof(err)),
                           err);
-            dev_ = std::shared_ptr<genie_index>(h, genie_index_destroy);
-        }
-        return dev_.get();
+            lazy_->dev = std::shared_ptr<genie_index>(h, genie_index_destroy);
+        });
+        return lazy_->dev.get();
     }
 
 private:
+    struct Lazy {
+        std::once_flag dev_once, stats_once;
+        std::shared_ptr<genie_index> dev;
+        std::vector<DimStats> stats;  // sorted by dim
+    };
+
+    std::pair<std::size_t, std::size_t> keyword_range(const QueryItem& item) const {
+        auto key_less = [](const KeywordEntry& e, const Keyword& k) { return e.keyword < k; };
+        auto less_key = [](const Keyword& k, const KeywordEntry& e) { return k < e.keyword; };
+        const auto a = std::lower_bound(entries_.begin(), entries_.end(), Keyword{item.dim, item.lo}, key_less);
+        const auto b = std::upper_bound(a, entries_.end(), Keyword{item.dim, item.hi}, less_key);
+        return {std::size_t(a - entries_.begin()), std::size_t(b - entries_.begin())};
+    }
+
+    bool tiles_in_order() const {
+        std::uint64_t at = 0;
+        for (const auto& e : entries_)
+            for (const auto& s : spans_of(e)) {
+                if (s.begin != at) return false;
+                at = s.end;
+            }
+        return at == list_.size();
+    }
+
+    // DimStats (index.hpp:153-174), computed on first use: per dim the largest
+    // token and the most keywords of that dim any one object carries
+    const DimStats* find_dim(DimId dim) const {
+        if (!lazy_) return nullptr;
+        std::call_once(lazy_->stats_once, [&] {
+            std::vector<std::uint32_t> per_obj(n_, 0);
+            std::vector<ObjectId> touched;
+            for (std::size_t j = 0; j < entries_.size();) {
+                DimStats st;
+                st.dim = entries_[j].keyword.dim;
+                for (; j < entries_.size() && entries_[j].keyword.dim == st.dim; ++j) {
+                    st.max_token = std::max(st.max_token, entries_[j].keyword.token);
+                    for (const auto& s : spans_of(entries_[j]))
+                        for (const ObjectId id : ids(s)) {
+                            if (per_obj[id]++ == 0) touched.push_back(id);
+                            st.max_multiplicity = std::max(st.max_multiplicity, per_obj[id]);
+                        }
+                }
+                for (const ObjectId id : touched) per_obj[id] = 0;
+                touched.clear();
+                lazy_->stats.push_back(st);
+            }
+        });
+        const auto& v = lazy_->stats;
+        const auto it = std::lower_bound(v.begin(), v.end(), dim, [](const DimStats& s, DimId d) { return s.dim < d; });
+        return it != v.end() && it->dim == dim ? &*it : nullptr;
+    }
+
     std::uint32_t n_ = 0;
-    std::vector<std::uint64_t> keys_, off_{0};
-    std::vector<ObjectId> post_;
+    std::vector<KeywordEntry> entries_;
+    std::vector<PostingsSpan> spans_;
+    std::vector<ObjectId> list_;
     std::optional<std::uint32_t> split_;
     int device_ = 0;
-    mutable std::shared_ptr<genie_index> dev_;
+    std::shared_ptr<Lazy> lazy_ = std::make_shared<Lazy>();
 };
 
-// build_index (index.hpp:190-250): dense ids, (keyword, id) pairs grouped by
-// keyword with ascending ids.
+namespace detail {
+// entries/spans of a CSR image cut at the split threshold (index.hpp:229-243)
+inline InvertedIndex from_csr(std::uint32_t n, const std::vector<std::uint64_t>& keys,
+                              const std::vector<std::uint64_t>& off, std::vector<ObjectId> post,
+                              std::optional<std::uint32_t> split, int device) {
+    std::vector<InvertedIndex::KeywordEntry> entries(keys.size());
+    std::vector<PostingsSpan> spans;
+    for (std::size_t j = 0; j < keys.size(); ++j) {
+        auto& e = entries[j];
+        e.keyword = Keyword{DimId(keys[j] >> 32), Token(keys[j] & 0xffffffffu)};
+        e.first_span = std::uint32_t(spans.size());
+        const std::uint64_t len = off[j + 1] - off[j];
+        const std::uint64_t lim = split ? *split : len;
+        for (std::uint64_t p = off[j]; p < off[j + 1]; p += lim) spans.push_back({p, std::min(off[j + 1], p + lim)});
+        const std::size_t made = spans.size() - e.first_span;
+        if (made > 0xffff) throw DataError("keyword has too many sub-lists (" + std::to_string(made) + ")");
+        e.span_count = std::uint16_t(made);
+    }
+    return InvertedIndex(n, std::move(entries), std::move(spans), std::move(post), split, device);
+}
+}  // namespace detail
+
+// build_index (index.hpp:190-250).  Ids are checked on the host with the
+// reference's message; the (keyword, id) sort and run-length CSR run on the
+// device (genie_index_build: CUB radix sort), and the CSR comes back to fill
+// the host view.  Same entries, spans and list array as the reference build.
 inline InvertedIndex build_index(std::span<const ObjectRecord> objects,
                                  std::optional<std::uint32_t> split_threshold = std::nullopt, int device = 0) {
     if (split_threshold && *split_threshold == 0) throw ContractError("split_threshold must be positive");
     const auto n = static_cast<std::uint32_t>(objects.size());
-    std::vector<char> seen(n, 0);
-    std::vector<std::pair<std::uint64_t, ObjectId>> pairs;
+    std::vector<const ObjectRecord*> by_id(n, nullptr);
     for (const auto& o : objects) {
-        if (o.id() >= n || seen[o.id()])
+        if (o.id() >= n || by_id[o.id()])
             throw DataError("object ids must be dense 0.." + std::to_string(n ? n - 1 : 0) + ": bad id " +
                             std::to_string(o.id()));
-        seen[o.id()] = 1;
-        for (const auto& kw : o.keywords()) pairs.emplace_back(kw.packed(), o.id());
+        by_id[o.id()] = &o;
     }
-    std::ranges::sort(pairs);
-    std::vector<std::uint64_t> keys, off{0};
-    std::vector<ObjectId> post;
-    post.reserve(pairs.size());
-    for (std::size_t i = 0; i < pairs.size(); ++i) {
-        if (i == 0 || pairs[i].first != pairs[i - 1].first) {
-            if (i) off.push_back(post.size());
-            keys.push_back(pairs[i].first);
+    std::vector<std::uint64_t> obj_off(std::size_t(n) + 1, 0);
+    for (std::uint32_t i = 0; i < n; ++i) obj_off[i + 1] = obj_off[i] + by_id[i]->keywords().size();
+    std::vector<std::uint16_t> dims(obj_off[n]);
+    std::vector<std::uint32_t> toks(obj_off[n]);
+    for (std::uint32_t i = 0; i < n; ++i) {
+        std::size_t at = obj_off[i];
+        for (const auto& kw : by_id[i]->keywords()) {
+            dims[at] = kw.dim;
+            toks[at++] = kw.token;
         }
-        post.push_back(pairs[i].second);
     }
-    if (!pairs.empty()) off.push_back(post.size());
-    return InvertedIndex(n, std::move(keys), std::move(off), std::move(post), split_threshold, device);
+    char err[512] = {};
+    genie_index* h = nullptr;
+    detail::check(genie_index_build(n, obj_off.data(), dims.data(), toks.data(), device, &h, err, sizeof(err)), err);
+    std::unique_ptr<genie_index, void (*)(genie_index*)> guard(h, genie_index_destroy);
+    std::uint32_t nn = 0, off_unused = 0;
+    std::uint64_t K = 0, P = 0;
+    int dev = 0;
+    genie_index_info(h, &nn, &K, &P, &off_unused, &dev);
+    std::vector<std::uint64_t> keys(K), off(K + 1, 0);
+    std::vector<ObjectId> post(P);
+    detail::check(genie_index_export(h, keys.data(), off.data(), post.data(), err, sizeof(err)), err);
+    return detail::from_csr(n, keys, off, std::move(post), split_threshold, device);
 }
 
 // ------------------------------------------------------------------ index_io
 // MCIX files (index_io.hpp:27-154) through the C ABI: the same bytes as the
-// reference's serialize_index for the same build, the same validation and
-// DataError messages on load.  A loaded index keeps whole-list spans (the
-// file's span cut is a build-time choice; results do not depend on it).
+// reference's serialize_index, the same validation and DataError messages on
+// load; a loaded index keeps the file's spans (so it re-serializes
+// byte-identically) and, like the reference, no split threshold.
 
 inline std::vector<std::uint8_t> serialize_index(const InvertedIndex& index) {
     char err[512] = {};
-    std::uint64_t size = 0;
-    const auto& k = index.packed_keys();
-    const auto& o = index.key_offsets();
+    const auto keys = index.packed_keys();
+    std::vector<std::uint16_t> cnt(keys.size());
+    std::vector<std::uint64_t> bounds;
+    bounds.reserve(index.spans().size() * 2);
+    for (std::size_t j = 0; j < keys.size(); ++j) {
+        const auto& e = index.entries()[j];
+        cnt[j] = e.span_count;
+        for (const auto& s : index.spans_of(e)) bounds.insert(bounds.end(), {s.begin, s.end});
+    }
     const auto& p = index.list_array();
-    const std::uint32_t split = index.split_threshold().value_or(0);
-    detail::check(genie_mcix_serialize(index.num_objects(), k.size(), k.data(), o.data(), p.data(), split, nullptr,
-                                       &size, err, sizeof(err)),
+    std::uint64_t size = 0;
+    detail::check(genie_mcix_serialize_spans(index.num_objects(), keys.size(), keys.data(), cnt.data(), bounds.data(),
+                                             p.size(), p.data(), nullptr, &size, err, sizeof(err)),
                   err);
     std::vector<std::uint8_t> out(size);
-    detail::check(genie_mcix_serialize(index.num_objects(), k.size(), k.data(), o.data(), p.data(), split, out.data(),
-                                       &size, err, sizeof(err)),
+    detail::check(genie_mcix_serialize_spans(index.num_objects(), keys.size(), keys.data(), cnt.data(), bounds.data(),
+                                             p.size(), p.data(), out.data(), &size, err, sizeof(err)),
                   err);
     return out;
 }
@@ -261,14 +493,23 @@ inline std::vector<std::uint8_t> serialize_index(const InvertedIndex& index) {
 inline InvertedIndex deserialize_index(const std::uint8_t* data, std::size_t size, int device = 0) {
     char err[512] = {};
     std::uint32_t n = 0;
-    std::uint64_t K = 0, P = 0;
+    std::uint64_t K = 0, P = 0, S = 0;
     detail::check(genie_mcix_parse(data, size, &n, &K, &P, nullptr, nullptr, nullptr, err, sizeof(err)), err);
     std::vector<std::uint64_t> keys(K), off(K + 1);
     std::vector<ObjectId> post(P);
     detail::check(genie_mcix_parse(data, size, nullptr, nullptr, nullptr, keys.data(), off.data(), post.data(), err,
                                    sizeof(err)),
                   err);
-    return InvertedIndex(n, std::move(keys), std::move(off), std::move(post), std::nullopt, device);
+    detail::check(genie_mcix_parse_spans(data, size, &S, nullptr, nullptr, err, sizeof(err)), err);
+    std::vector<std::uint16_t> cnt(K);
+    std::vector<std::uint64_t> bounds(2 * S);
+    detail::check(genie_mcix_parse_spans(data, size, &S, cnt.data(), bounds.data(), err, sizeof(err)), err);
+    std::vector<InvertedIndex::KeywordEntry> entries(K);
+    std::vector<PostingsSpan> spans(S);
+    for (std::uint64_t s = 0; s < S; ++s) spans[s] = {bounds[2 * s], bounds[2 * s + 1]};
+    for (std::uint64_t j = 0, first = 0; j < K; first += cnt[j], ++j)
+        entries[j] = {Keyword{DimId(keys[j] >> 32), Token(keys[j] & 0xffffffffu)}, std::uint32_t(first), cnt[j]};
+    return InvertedIndex(n, std::move(entries), std::move(spans), std::move(post), std::nullopt, device);
 }
 
 inline void save_index(const InvertedIndex& index, const std::string& path) {
@@ -277,17 +518,32 @@ inline void save_index(const InvertedIndex& index, const std::string& path) {
     if (!f) throw DataError("cannot open " + path + " for writing");
     const bool ok = std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size();
     std::fclose(f);
-    if (!ok) throw DataError("failed writing " + path);
+    if (!ok) throw DataError("write failed: " + path);
 }
 
-inline InvertedIndex load_index(const std::string& path, int device = 0) {
+inline std::vector<std::uint8_t> read_file_bytes(const std::string& path) {
     std::FILE* f = std::fopen(path.c_str(), "rb");
     if (!f) throw DataError("cannot open " + path);
     std::vector<std::uint8_t> bytes;
     std::uint8_t buf[1 << 16];
     for (std::size_t got; (got = std::fread(buf, 1, sizeof(buf), f)) > 0;) bytes.insert(bytes.end(), buf, buf + got);
+    const bool bad = std::ferror(f) != 0;
     std::fclose(f);
+    if (bad) throw DataError("read failed: " + path);
+    return bytes;
+}
+
+inline InvertedIndex load_index(const std::string& path, int device = 0) {
+    const auto bytes = read_file_bytes(path);
     return deserialize_index(bytes.data(), bytes.size(), device);
+}
+
+// FNV-1a over a byte image (index_io.hpp:182-189): ties encoder sidecars to
+// index files
+inline std::uint64_t fnv1a64(const std::uint8_t* data, std::size_t size) {
+    std::uint64_t h = 0xcbf29ce484222325ull;
+    for (std::size_t i = 0; i < size; ++i) h = (h ^ data[i]) * 0x100000001b3ull;
+    return h;
 }
 
 struct IndexPartition {
@@ -297,9 +553,13 @@ struct IndexPartition {
     InvertedIndex index;
 };
 
+// partition_dataset (index.hpp:263-291): consecutive parts of part_capacity
+// objects over local ids.  `devices` (optional) places part p on
+// devices[p % devices.size()], so execute_partitioned spreads over GPUs.
 inline std::vector<IndexPartition> partition_dataset(std::span<const ObjectRecord> objects,
                                                      std::uint32_t part_capacity,
-                                                     std::optional<std::uint32_t> split = std::nullopt) {
+                                                     std::optional<std::uint32_t> split = std::nullopt,
+                                                     std::span<const int> devices = {}) {
     if (part_capacity == 0) throw ContractError("part_capacity must be >= 1");
     for (std::size_t i = 0; i < objects.size(); ++i)
         if (objects[i].id() != i) throw DataError("partitioning requires objects in dense id order");
@@ -307,8 +567,10 @@ inline std::vector<IndexPartition> partition_dataset(std::span<const ObjectRecor
     for (std::size_t start = 0, pid = 0; start < objects.size(); start += part_capacity, ++pid) {
         const auto cnt = std::min<std::size_t>(part_capacity, objects.size() - start);
         std::vector<ObjectRecord> local;
+        local.reserve(cnt);
         for (std::size_t i = 0; i < cnt; ++i) local.emplace_back(ObjectId(i), objects[start + i].keywords());
-        parts.push_back({std::uint32_t(pid), ObjectId(start), std::uint32_t(cnt), build_index(local, split)});
+        const int dev = devices.empty() ? 0 : devices[pid % devices.size()];
+        parts.push_back({std::uint32_t(pid), ObjectId(start), std::uint32_t(cnt), build_index(local, split, dev)});
     }
     return parts;
 }
@@ -322,7 +584,7 @@ struct EngineConfig {
     Selector selector = Selector::cpq;
     ExecMode mode = ExecMode::parallel;  // the device path is always parallel
     std::uint32_t workers = 0;           // accepted, unused on the device
-    std::uint32_t span_chunk = 1024;     // postings per warp work unit
+    std::uint32_t span_chunk = 4096;     // ids per chunk (engine.hpp:40); the device warp unit is a quarter
     std::uint32_t max_spans_per_task = 2;
 };
 
@@ -425,6 +687,7 @@ inline BatchResult execute_partitioned(std::span<const IndexPartition> partition
             throw ContractError("partitions must be disjoint and contiguous");
         expected += p.size;
     }
+    const auto t_total = std::chrono::steady_clock::now();
     BatchResult batch;
     batch.results.resize(queries.size());
     std::vector<std::vector<TopKResult>> locals(queries.size());
@@ -441,7 +704,11 @@ inline BatchResult execute_partitioned(std::span<const IndexPartition> partition
             locals[q].push_back(std::move(local.results[q]));
         }
     }
+    const auto t_merge = std::chrono::steady_clock::now();
     for (std::size_t q = 0; q < queries.size(); ++q) batch.results[q] = merge_topk(locals[q], queries[q].k, queries[q].id);
+    const auto t_end = std::chrono::steady_clock::now();
+    batch.timings.merge_ns = std::uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(t_end - t_merge).count());
+    batch.timings.total_ns = std::uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(t_end - t_total).count());
     return batch;
 }
 
@@ -542,6 +809,13 @@ public:
     }
     const LshEncoderConfig& config() const noexcept { return cfg_; }
     std::uint32_t m() const noexcept { return cfg_.m; }
+
+    // f_function(point) (lsh.hpp:172-175)
+    Token token(std::uint32_t function, std::span<const float> point) const {
+        if (function >= cfg_.m) throw ContractError("hash function index out of range");
+        check_dims(point);
+        return encode_points(point)[function];
+    }
 
     // tokens of n points (row-major n x dims) -> n x m
     std::vector<Token> encode_points(std::span<const float> points) const {

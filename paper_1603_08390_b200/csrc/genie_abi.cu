@@ -7,55 +7,6 @@
 #include "internal.cuh"
 
 namespace genie {
-void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
-                       const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
-                       uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
-                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s);
-
-// engine.hpp:186-188 and model.hpp:80-85, 97-101: the reference raises these
-// before any work happens.
-static void validate_config(const genie_config& c) {
-    if (c.span_chunk == 0 || c.max_spans_per_task == 0)
-        throw Error(GENIE_ERR_CONTRACT, "span_chunk and max_spans_per_task must be positive");
-    if (c.selector > GENIE_SELECT_SORT) throw Error(GENIE_ERR_CONTRACT, "unknown selector");
-}
-
-static void validate_queries(uint32_t Q, const uint32_t* qid, const uint32_t* k,
-                             const uint64_t* item_off, const uint16_t* dim, const uint32_t* lo,
-                             const uint32_t* hi) {
-    if (Q >= (1u << 21)) throw Error(GENIE_ERR_CONTRACT, "batch exceeds 2^21 queries");
-    for (uint32_t q = 0; q < Q; ++q) {
-        if (item_off[q + 1] < item_off[q]) throw Error(GENIE_ERR_CONTRACT, "item_off must be non-decreasing");
-        for (uint64_t i = item_off[q]; i < item_off[q + 1]; ++i)
-            if (lo[i] > hi[i])
-                throw Error(GENIE_ERR_CONTRACT, "QueryItem: lo " + std::to_string(lo[i]) + " > hi " +
-                                                    std::to_string(hi[i]) + " on dim " +
-                                                    std::to_string(dim[i]));
-        if (item_off[q + 1] == item_off[q])
-            throw Error(GENIE_ERR_CONTRACT, "Query " + std::to_string(qid[q]) + ": no items");
-        if (k[q] == 0) throw Error(GENIE_ERR_CONTRACT, "Query " + std::to_string(qid[q]) + ": k must be >= 1");
-    }
-}
-
-template <typename T>
-static void h2d(DevBuf<T>& b, const T* src, size_t n, cudaStream_t s) {
-    b.reserve(n);
-    if (n) GENIE_CUDA(cudaMemcpyAsync(b.p, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
-}
-
-// Reference accounting of MemoryStats (engine.hpp:239-241; cpq.hpp:103-106,
-// 243, 283, 359-362), from the per-query bounds.
-static void memory_stats(uint32_t n, uint32_t Q, const uint32_t* k, const uint64_t* bounds,
-                         genie_batch_stats* st) {
-    st->counter_bytes = st->gate_bytes = st->table_bytes = 0;
-    for (uint32_t q = 0; q < Q; ++q) {
-        const uint64_t b = std::max<uint64_t>(bounds[q], 1);
-        const uint64_t w = width_for(b);
-        st->counter_bytes += (uint64_t(n) * w + 7) / 8;
-        st->gate_bytes += (b + 1) * 4 + 4;
-        st->table_bytes += 8 * bit_ceil64(std::max<uint64_t>(2ull * k[q] * b, 2));
-    }
-}
 
 }  // namespace genie
 
@@ -225,6 +176,14 @@ int genie_merge_topk_device(genie_index* ix, uint32_t Q, uint32_t L, const genie
                             const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
                             uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
                             uint32_t* d_out_threshold, void* stream, char* err, size_t errlen) {
+    return genie_merge_topk_device_layout(ix, Q, L, d_in, d_in_len, in_stride, 0, d_k, out_stride, d_out, d_out_len,
+                                          d_out_threshold, stream, err, errlen);
+}
+
+int genie_merge_topk_device_layout(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
+                                   const uint32_t* d_in_len, uint32_t in_stride, uint32_t list_major,
+                                   const uint32_t* d_k, uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
+                                   uint32_t* d_out_threshold, void* stream, char* err, size_t errlen) {
     return guarded(err, errlen, [&]() -> int {
         if (!ix) throw Error(GENIE_ERR_CONTRACT, "null index");
         ensure_device(ix->device);
@@ -232,7 +191,7 @@ int genie_merge_topk_device(genie_index* ix, uint32_t Q, uint32_t L, const genie
         // max_k is unknown on the host here; rows are bounded by L * in_stride
         const uint32_t max_rows = std::min<uint32_t>(out_stride, L * in_stride);
         launch_list_merge(ix, Q, L, d_in, d_in_len, in_stride, d_k, out_stride, d_out, d_out_len,
-                          d_out_threshold, max_rows, s);
+                          d_out_threshold, max_rows, s, list_major != 0);
         if (s != ix->stream) {
             GENIE_CUDA(cudaEventRecord(ix->ev[5], s));
             GENIE_CUDA(cudaStreamWaitEvent(ix->stream, ix->ev[5], 0));
@@ -279,7 +238,7 @@ int genie_merge_topk(int device, uint32_t Q, uint32_t L, const genie_entry* in, 
         d_olen.reserve(Q + 1);
         d_othr.reserve(Q + 1);
         launch_list_merge(&tmp, Q, L, d_in.p, d_len.p, in_stride, d_k.p, stride, d_out.p, d_olen.p,
-                          d_othr.p, max_k, tmp.stream);
+                          d_othr.p, max_k, tmp.stream, false);
         std::string msg;
         const int rc = finish_batch(&tmp, nullptr, msg, nullptr);
         if (rc != GENIE_OK) throw Error(rc, msg);

@@ -219,7 +219,7 @@ extern "C" {
 genie_config genie_config_default(void) {
     genie_config c{};
     c.selector = GENIE_SELECT_CPQ;
-    c.span_chunk = kDefaultUnit;
+    c.span_chunk = 4 * kDefaultUnit;  // 4096, engine.hpp:40
     c.max_spans_per_task = 2;
     c.tile_bytes = 0;
     c.ctas_per_sm = 0;

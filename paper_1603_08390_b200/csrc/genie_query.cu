@@ -2028,11 +2028,11 @@ struct MergeSrc {
     const uint32_t* tile_len;
     const genie_entry* tile_out;
     const uint32_t* q_floor;  // per-query floor (tile mode) or null
-    // mode 1
+    // mode 1: list l of query q at in + q * in_q + l * in_l, length in_len[q * len_q + l * len_l]
     uint32_t L;
     const genie_entry* in;
     const uint32_t* in_len;
-    uint32_t in_stride;
+    uint64_t in_q, in_l, len_q, len_l;
     // common
     const uint32_t* k;
     uint32_t Q;
@@ -2051,8 +2051,8 @@ __device__ __forceinline__ void list_of(const MergeSrc& m, uint32_t q, uint32_t 
         base = m.tile_out + m.q_out_base[q] + uint64_t(l) * m.q_cap[q];
         len = m.tile_len[m.q_tile_base[q] + l];
     } else {
-        base = m.in + (uint64_t(q) * m.L + l) * m.in_stride;
-        len = m.in_len[uint64_t(q) * m.L + l];
+        base = m.in + q * m.in_q + l * m.in_l;
+        len = m.in_len[q * m.len_q + l * m.len_l];
     }
 }
 
@@ -2376,7 +2376,8 @@ void ensure_device(int device) { GENIE_CUDA(cudaSetDevice(device)); }
 // contract; distinct handles on one device set the same values.
 struct DeviceAttrCache {
     size_t scan_smem = 0;
-    bool merge_set = false;
+    bool merge_set = false;       // k_merge (batch) and k_merge_big
+    bool list_merge_set = false;  // k_merge (list merge) and k_merge_big
 };
 static DeviceAttrCache& attr_cache(int device) {
     static DeviceAttrCache caches[kMaxDevices];
@@ -2538,7 +2539,7 @@ static uint32_t class_tile_bits(const genie_index* ix, const genie_config& cfg, 
 }
 
 static MergeSrc tile_merge_src(genie_index* ix, uint32_t Q, const uint32_t* d_k, uint32_t stride,
-                               genie_entry* out, uint32_t* out_len, uint32_t* out_thr) {
+                               genie_entry* out, uint32_t* out_len, uint32_t* out_thr, uint32_t id_offset) {
     Workspace& w = ix->ws;
     MergeSrc m{};
     m.mode = 0;
@@ -2551,7 +2552,7 @@ static MergeSrc tile_merge_src(genie_index* ix, uint32_t Q, const uint32_t* d_k,
     m.q_floor = w.q_floor.p;
     m.k = d_k;
     m.Q = Q;
-    m.id_offset = ix->id_offset;
+    m.id_offset = id_offset;
     m.q_big = w.q_big.p;
     m.st = w.status.p;
     m.out_stride = stride;
@@ -2590,8 +2591,9 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
                   const uint32_t* d_k, const uint64_t* d_item_off, const uint16_t* d_dim,
                   const uint32_t* d_lo, const uint32_t* d_hi, uint32_t total_items,
                   uint32_t max_k, uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
-                  uint32_t* d_out_thr, cudaStream_t s, bool timed) {
+                  uint32_t* d_out_thr, cudaStream_t s, bool timed, uint32_t extra_offset) {
     (void)d_qid;
+    const uint32_t id_offset = ix->id_offset + extra_offset;  // reported ids are local + id_offset
     uint32_t tile_bits_w[3];
     const uint32_t tile_bits = class_tile_bits(ix, cfg, tile_bits_of(cfg), tile_bits_w);
     const uint32_t tile_bytes = tile_bits / 8;
@@ -2610,7 +2612,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.dim_mult = ix->dim_mult.p;
     p.K = ix->K;
     p.n = ix->n;
-    p.id_offset = ix->id_offset;
+    p.id_offset = id_offset;
     p.Q = Q;
     p.k = d_k;
     p.item_off = d_item_off;
@@ -2619,7 +2621,9 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.hi = d_hi;
     p.tile_bits = tile_bits;
     for (int c = 0; c < 3; ++c) p.tile_bits_w[c] = tile_bits_w[c];
-    uint32_t unit = cfg.span_chunk ? cfg.span_chunk : kDefaultUnit;
+    // span_chunk is the reference's chunk (ids per task chunk, engine.hpp:40);
+    // a scan warp claims a quarter of one at a time (guided self-scheduling)
+    uint32_t unit = cfg.span_chunk ? cfg.span_chunk / 4 : kDefaultUnit;
     unit = std::min<uint32_t>(std::max<uint32_t>((unit + 127) & ~127u, 128), 1u << 16);
     p.unit = unit;
     p.selector = cfg.selector;
@@ -2694,7 +2698,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         k_scan<<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
         ++launches;
         if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
-        const MergeSrc m = tile_merge_src(ix, Q, d_k, out_stride, d_out, d_out_len, d_out_thr);
+        const MergeSrc m = tile_merge_src(ix, Q, d_k, out_stride, d_out, d_out_len, d_out_thr, id_offset);
         const size_t msmem = kSortCap * sizeof(uint64_t);
         if (!ac.merge_set) {
             GENIE_CUDA(cudaFuncSetAttribute(k_merge<kMergeSmallThreads>,
@@ -2712,7 +2716,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         k_merge_big<<<mgrid, kMergeThreads, msmem, s>>>(m);
         launches += 2;
         if (max_k > kSortCap) {
-            segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, ix->id_offset, s);
+            segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, id_offset, s);
             launches += 3;
         }
         if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
@@ -2773,7 +2777,7 @@ int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
 void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
                        const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
                        uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
-                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s) {
+                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s, bool list_major) {
     Workspace& w = ix->ws;
     if (!w.status.p) {
         w.status.reserve(ST_WORDS);
@@ -2788,7 +2792,12 @@ void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entr
     m.L = L;
     m.in = d_in;
     m.in_len = d_in_len;
-    m.in_stride = in_stride;
+    // query-major [Q][L][in_stride] (merge_topk callers) or list-major
+    // [L][Q][in_stride] (the order an all-gather of per-shard rows produces)
+    m.in_q = list_major ? in_stride : uint64_t(L) * in_stride;
+    m.in_l = list_major ? uint64_t(Q) * in_stride : in_stride;
+    m.len_q = list_major ? 1 : L;
+    m.len_l = list_major ? Q : 1;
     m.k = d_k;
     m.Q = Q;
     m.id_offset = 0;
@@ -2800,10 +2809,14 @@ void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entr
     m.out_thr = d_out_thr;
     k_init_status<<<1, 32, 0, s>>>(w.status.p);
     const size_t msmem = kSortCap * sizeof(uint64_t);
-    GENIE_CUDA(cudaFuncSetAttribute(k_merge<kMergeThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(msmem)));
-    GENIE_CUDA(cudaFuncSetAttribute(k_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(msmem)));
+    DeviceAttrCache& ac = attr_cache(ix->device);
+    if (!ac.list_merge_set) {
+        GENIE_CUDA(cudaFuncSetAttribute(k_merge<kMergeThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(msmem)));
+        GENIE_CUDA(cudaFuncSetAttribute(k_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(msmem)));
+        ac.list_merge_set = true;
+    }
     const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(Q, ix->sms * 4));
     if (Q) {
         k_merge<kMergeThreads><<<grid, kMergeThreads, msmem, s>>>(m, kSortCap);

@@ -1,6 +1,8 @@
 // Internal structures shared by the libgenie_b200 translation units.
 #pragma once
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace genie {
@@ -180,7 +182,14 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
                   const uint32_t* d_k, const uint64_t* d_item_off, const uint16_t* d_dim,
                   const uint32_t* d_lo, const uint32_t* d_hi, uint32_t total_items,
                   uint32_t max_k, uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
-                  uint32_t* d_out_thr, cudaStream_t stream, bool timed);
+                  uint32_t* d_out_thr, cudaStream_t stream, bool timed, uint32_t extra_offset = 0);
+
+// merge_topk over explicit candidate lists (engine.hpp:158-177), on the
+// device: query-major [Q][L][in_stride] or list-major [L][Q][in_stride].
+void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
+                       const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
+                       uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
+                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s, bool list_major);
 
 // Reads the status block (synchronises) and converts it to a status code +
 // message.  Grows the workspace and returns GENIE_RETRY on overflow.
@@ -188,5 +197,52 @@ int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
                  const uint32_t* h_qid /* optional, for messages */);
 
 void ensure_device(int device);
+
+// ---- host-side helpers shared by the C-ABI translation units
+
+// engine.hpp:186-188 and model.hpp:80-85, 97-101: the reference raises these
+// before any work happens.
+inline void validate_config(const genie_config& c) {
+    if (c.span_chunk == 0 || c.max_spans_per_task == 0)
+        throw Error(GENIE_ERR_CONTRACT, "span_chunk and max_spans_per_task must be positive");
+    if (c.selector > GENIE_SELECT_SORT) throw Error(GENIE_ERR_CONTRACT, "unknown selector");
+}
+
+inline void validate_queries(uint32_t Q, const uint32_t* qid, const uint32_t* k,
+                             const uint64_t* item_off, const uint16_t* dim, const uint32_t* lo,
+                             const uint32_t* hi) {
+    if (Q >= (1u << 21)) throw Error(GENIE_ERR_CONTRACT, "batch exceeds 2^21 queries");
+    for (uint32_t q = 0; q < Q; ++q) {
+        if (item_off[q + 1] < item_off[q]) throw Error(GENIE_ERR_CONTRACT, "item_off must be non-decreasing");
+        for (uint64_t i = item_off[q]; i < item_off[q + 1]; ++i)
+            if (lo[i] > hi[i])
+                throw Error(GENIE_ERR_CONTRACT, "QueryItem: lo " + std::to_string(lo[i]) + " > hi " +
+                                                    std::to_string(hi[i]) + " on dim " +
+                                                    std::to_string(dim[i]));
+        if (item_off[q + 1] == item_off[q])
+            throw Error(GENIE_ERR_CONTRACT, "Query " + std::to_string(qid[q]) + ": no items");
+        if (k[q] == 0) throw Error(GENIE_ERR_CONTRACT, "Query " + std::to_string(qid[q]) + ": k must be >= 1");
+    }
+}
+
+template <typename T>
+inline void h2d(DevBuf<T>& b, const T* src, size_t n, cudaStream_t s) {
+    b.reserve(n);
+    if (n) GENIE_CUDA(cudaMemcpyAsync(b.p, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+// Reference accounting of MemoryStats (engine.hpp:239-241; cpq.hpp:103-106,
+// 243, 283, 359-362), from the per-query bounds.
+inline void memory_stats(uint32_t n, uint32_t Q, const uint32_t* k, const uint64_t* bounds,
+                         genie_batch_stats* st) {
+    st->counter_bytes = st->gate_bytes = st->table_bytes = 0;
+    for (uint32_t q = 0; q < Q; ++q) {
+        const uint64_t b = std::max<uint64_t>(bounds[q], 1);
+        const uint64_t w = width_for(b);
+        st->counter_bytes += (uint64_t(n) * w + 7) / 8;
+        st->gate_bytes += (b + 1) * 4 + 4;
+        st->table_bytes += 8 * bit_ceil64(std::max<uint64_t>(2ull * k[q] * b, 2));
+    }
+}
 
 }  // namespace genie

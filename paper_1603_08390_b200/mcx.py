@@ -472,7 +472,7 @@ class EngineConfig:
     selector: Selector = Selector.cpq
     mode: ExecMode = ExecMode.parallel
     workers: int = 0
-    span_chunk: int = 1024
+    span_chunk: int = 4096
     max_spans_per_task: int = 2
     tile_bytes: int = 0
     ctas_per_sm: int = 0
