@@ -525,8 +525,6 @@ def main_genie(args):
     if world > 1:
         gath = torch.zeros((world, Q, stride, 2), dtype=torch.int32, device=dev)
         gath_len = torch.zeros((world, Q), dtype=torch.int32, device=dev)
-        m_in = torch.zeros((Q, world, stride, 2), dtype=torch.int32, device=dev)
-        m_len = torch.zeros((Q, world), dtype=torch.int32, device=dev)
         fin = torch.zeros((Q, stride, 2), dtype=torch.int32, device=dev)
         fin_len = torch.zeros(Q, dtype=torch.int32, device=dev)
         fin_thr = torch.zeros(Q, dtype=torch.int32, device=dev)
@@ -542,9 +540,9 @@ def main_genie(args):
             # all-gather the per-shard top-k (global ids), merge on the device
             dist.all_gather_into_tensor(gath, d["out"])
             dist.all_gather_into_tensor(gath_len, d["out_len"])
-            m_in.copy_(gath.permute(1, 0, 2, 3))
-            m_len.copy_(gath_len.t())
-            ix.merge_device(Q, world, m_in, m_len, stride, d["k"], stride, fin, fin_len, fin_thr, stream=sptr)
+            # rank-major rows merged in place (list-major layout, no transpose)
+            ix.merge_device(Q, world, gath, gath_len, stride, d["k"], stride, fin, fin_len, fin_thr, stream=sptr,
+                            list_major=True)
             launches_per_step += 3
 
     def run_checked():
@@ -612,9 +610,8 @@ def main_genie(args):
             lens = torch.from_numpy(hout[1].astype(np.int32)).to(dev)
             dist.all_gather_into_tensor(gath, lists.view(torch.int32))
             dist.all_gather_into_tensor(gath_len, lens)
-            m_in.copy_(gath.permute(1, 0, 2, 3))
-            m_len.copy_(gath_len.t())
-            ix.merge_device(Q, world, m_in, m_len, stride, d["k"], stride, fin, fin_len, fin_thr, stream=sptr)
+            ix.merge_device(Q, world, gath, gath_len, stride, d["k"], stride, fin, fin_len, fin_thr, stream=sptr,
+                            list_major=True)
             fin.cpu(), fin_len.cpu(), fin_thr.cpu()
         return h2d, d2h + hout[0].nbytes + hout[1].nbytes + hout[2].nbytes
 

@@ -260,6 +260,41 @@ int genie_merge_topk(int device, uint32_t num_queries, uint32_t num_lists, const
 uint64_t genie_hash_results(uint32_t num_queries, const uint32_t* qid, const uint32_t* threshold,
                             const uint32_t* len, uint32_t stride, const genie_entry* entries);
 
+/* Device groups ------------------------------------------- *
+ * Object-id-range shards of one index on several GPUs driven by ONE host
+ * thread: the concurrent form of execute_partitioned (engine.hpp:308-347).
+ * Shard p owns ids [p n / G, (p + 1) n / G) and lives on devices[p]; every
+ * shard's batch runs at once, the per-shard top-k rows (global ids) are
+ * exchanged -- an NCCL all-gather over NVLink when the shards sit on distinct
+ * devices (libnccl.so.2 loaded at run time), device-to-device / peer copies
+ * otherwise -- and merged on devices[0] with merge_topk's rule
+ * (engine.hpp:158-177).  Results equal genie_query_batch on the whole index. */
+typedef struct genie_group genie_group;
+enum genie_exchange {
+    GENIE_EXCHANGE_AUTO = 0, /* NCCL when possible, else peer copies */
+    GENIE_EXCHANGE_NCCL = 1, /* NCCL all-gather (ContractError if unavailable) */
+    GENIE_EXCHANGE_PEER = 2  /* peer / device-to-device copies into the root */
+};
+int genie_group_create(uint32_t num_objects, uint64_t num_keys, const uint64_t* keys, const uint64_t* key_off,
+                       const uint32_t* postings, uint32_t num_shards, const int* devices, int exchange,
+                       genie_group** out, char* err, size_t errlen);
+/* A group over existing indexes (borrowed, not destroyed with the group):
+ * part p reports local ids + id_offsets[p] (IndexPartition::id_offset,
+ * index.hpp:254-259); parts must be disjoint id ranges. */
+int genie_group_from_indexes(genie_index* const* indexes, const uint32_t* id_offsets, uint32_t num_shards,
+                             int exchange, genie_group** out, char* err, size_t errlen);
+void genie_group_destroy(genie_group* g);
+/* num_shards, the exchange in use (genie_exchange), total objects */
+int genie_group_info(const genie_group* g, uint32_t* num_shards, int* exchange, uint32_t* num_objects);
+/* genie_query_batch over the group (host buffers, same contract); timings:
+ * lookup / match = the slowest shard, merge = the root merge; stats: work
+ * summed, memory accounting the per-shard maximum (engine.hpp:330-333). */
+int genie_group_query_batch(genie_group* g, const genie_config* cfg, uint32_t num_queries, const uint32_t* query_id,
+                            const uint32_t* k, const uint64_t* item_off, const uint16_t* item_dim,
+                            const uint32_t* item_lo, const uint32_t* item_hi, uint32_t out_stride, genie_entry* out,
+                            uint32_t* out_len, uint32_t* out_threshold, genie_stage_ns* timings,
+                            genie_batch_stats* stats, char* err, size_t errlen);
+
 /* LSH / minHash transforms ------------------------------------------------- */
 
 /* mcx::LshFamily (lsh.hpp:130) plus minHash (new). */

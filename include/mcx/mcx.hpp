@@ -630,55 +630,84 @@ inline TopKResult merge_topk(std::span<const TopKResult> locals, std::uint32_t k
     return m;
 }
 
-inline BatchResult execute_batch(const InvertedIndex& index, std::span<const Query> queries,
-                                 const EngineConfig& config = {}) {
-    if (config.span_chunk == 0 || config.max_spans_per_task == 0)
-        throw ContractError("span_chunk and max_spans_per_task must be positive");
-    BatchResult batch;
-    const auto Q = static_cast<std::uint32_t>(queries.size());
-    if (!Q) return batch;
-    std::vector<std::uint32_t> qid(Q), k(Q), lo, hi;
-    std::vector<std::uint64_t> off(Q + 1, 0);
+namespace detail {
+// A batch flattened into the C ABI's arrays (queries in request order).
+struct FlatBatch {
+    std::vector<std::uint32_t> qid, k, lo, hi;
+    std::vector<std::uint64_t> off{0};
     std::vector<std::uint16_t> dim;
     std::uint32_t max_k = 1;
-    for (std::uint32_t q = 0; q < Q; ++q) {
-        qid[q] = queries[q].id;
-        k[q] = queries[q].k;
-        max_k = std::max(max_k, k[q]);
-        for (const auto& it : queries[q].items) {
-            dim.push_back(it.dim);
-            lo.push_back(it.lo);
-            hi.push_back(it.hi);
+    explicit FlatBatch(std::span<const Query> queries) {
+        for (const auto& q : queries) {
+            qid.push_back(q.id);
+            k.push_back(q.k);
+            max_k = std::max(max_k, q.k);
+            for (const auto& it : q.items) {
+                dim.push_back(it.dim);
+                lo.push_back(it.lo);
+                hi.push_back(it.hi);
+            }
+            off.push_back(dim.size());
         }
-        off[q + 1] = dim.size();
     }
-    const std::uint32_t stride = std::max<std::uint32_t>(1, std::min(max_k, std::max<std::uint32_t>(index.num_objects(), 1)));
-    std::vector<genie_entry> out(std::size_t(Q) * stride);
-    std::vector<std::uint32_t> len(Q), thr(Q);
+};
+
+inline genie_config to_genie(const EngineConfig& config) {
+    if (config.span_chunk == 0 || config.max_spans_per_task == 0)
+        throw ContractError("span_chunk and max_spans_per_task must be positive");
     genie_config cfg = genie_config_default();
     cfg.selector = static_cast<std::uint32_t>(config.selector);
     cfg.span_chunk = config.span_chunk;
     cfg.max_spans_per_task = config.max_spans_per_task;
-    genie_stage_ns t{};
-    genie_batch_stats st{};
-    char err[1024] = {};
-    detail::check(genie_query_batch(index.device(), &cfg, Q, qid.data(), k.data(), off.data(), dim.data(), lo.data(),
-                                    hi.data(), stride, out.data(), len.data(), thr.data(), nullptr, &t, &st, err,
-                                    sizeof(err)),
-                  err);
-    batch.results.resize(Q);
-    for (std::uint32_t q = 0; q < Q; ++q) {
+    return cfg;
+}
+
+// rows of the C ABI -> TopKResults, plus timings and memory accounting
+inline BatchResult to_batch(const FlatBatch& f, std::uint32_t stride, const std::vector<genie_entry>& out,
+                            const std::vector<std::uint32_t>& len, const std::vector<std::uint32_t>& thr,
+                            const genie_stage_ns& t, const genie_batch_stats& st) {
+    BatchResult batch;
+    batch.results.resize(f.qid.size());
+    for (std::size_t q = 0; q < f.qid.size(); ++q) {
         auto& r = batch.results[q];
-        r.query_id = qid[q];
+        r.query_id = f.qid[q];
         r.threshold = thr[q];
-        for (std::uint32_t e = 0; e < len[q]; ++e) r.entries.push_back({out[std::size_t(q) * stride + e].id,
-                                                                         out[std::size_t(q) * stride + e].count});
+        r.entries.reserve(len[q]);
+        for (std::uint32_t e = 0; e < len[q]; ++e) r.entries.push_back({out[q * stride + e].id, out[q * stride + e].count});
     }
     batch.timings = {t.lookup_ns, t.match_ns, t.select_ns, t.merge_ns, t.total_ns};
     batch.memory = {st.counter_bytes, st.gate_bytes, st.table_bytes};
     return batch;
 }
+}  // namespace detail
 
+// execute_batch (engine.hpp:184-304): lookup, counting, the Count Priority
+// Queue and top-k selection on the index's GPU; results in request order.
+inline BatchResult execute_batch(const InvertedIndex& index, std::span<const Query> queries,
+                                 const EngineConfig& config = {}) {
+    const genie_config cfg = detail::to_genie(config);
+    if (queries.empty()) return {};
+    const detail::FlatBatch f(queries);
+    const auto Q = static_cast<std::uint32_t>(queries.size());
+    const std::uint32_t stride = std::max<std::uint32_t>(1, std::min(f.max_k, std::max<std::uint32_t>(index.num_objects(), 1)));
+    std::vector<genie_entry> out(std::size_t(Q) * stride);
+    std::vector<std::uint32_t> len(Q), thr(Q);
+    genie_stage_ns t{};
+    genie_batch_stats st{};
+    char err[1024] = {};
+    detail::check(genie_query_batch(index.device(), &cfg, Q, f.qid.data(), f.k.data(), f.off.data(), f.dim.data(),
+                                    f.lo.data(), f.hi.data(), stride, out.data(), len.data(), thr.data(), nullptr, &t,
+                                    &st, err, sizeof(err)),
+                  err);
+    return detail::to_batch(f, stride, out, len, thr, t, st);
+}
+
+// execute_partitioned (engine.hpp:308-347).  The reference runs the parts one
+// after another; here all parts run at once -- each on its own device / stream
+// (partition_dataset's `devices`), one host thread -- and their top-k rows are
+// merged on the first part's device (genie_group_*: NCCL all-gather across
+// distinct GPUs, peer copies otherwise).  Same results, timings and
+// per-part-maximum memory accounting as the reference.
 inline BatchResult execute_partitioned(std::span<const IndexPartition> partitions, std::span<const Query> queries,
                                        const EngineConfig& config = {}) {
     std::uint64_t expected = 0;
@@ -687,29 +716,37 @@ inline BatchResult execute_partitioned(std::span<const IndexPartition> partition
             throw ContractError("partitions must be disjoint and contiguous");
         expected += p.size;
     }
-    const auto t_total = std::chrono::steady_clock::now();
-    BatchResult batch;
-    batch.results.resize(queries.size());
-    std::vector<std::vector<TopKResult>> locals(queries.size());
-    for (const auto& p : partitions) {
-        auto local = execute_batch(p.index, queries, config);
-        batch.timings.lookup_ns += local.timings.lookup_ns;
-        batch.timings.match_ns += local.timings.match_ns;
-        batch.timings.select_ns += local.timings.select_ns;
-        batch.memory.counter_bytes = std::max(batch.memory.counter_bytes, local.memory.counter_bytes);
-        batch.memory.gate_bytes = std::max(batch.memory.gate_bytes, local.memory.gate_bytes);
-        batch.memory.table_bytes = std::max(batch.memory.table_bytes, local.memory.table_bytes);
-        for (std::size_t q = 0; q < queries.size(); ++q) {
-            for (auto& e : local.results[q].entries) e.id += p.id_offset;
-            locals[q].push_back(std::move(local.results[q]));
-        }
+    const genie_config cfg = detail::to_genie(config);
+    if (queries.empty()) return {};
+    if (partitions.empty()) {  // nothing indexed: every merged list is empty (engine.hpp:158-177)
+        BatchResult batch;
+        for (const auto& q : queries) batch.results.push_back(TopKResult{q.id, {}, 0});
+        return batch;
     }
-    const auto t_merge = std::chrono::steady_clock::now();
-    for (std::size_t q = 0; q < queries.size(); ++q) batch.results[q] = merge_topk(locals[q], queries[q].k, queries[q].id);
-    const auto t_end = std::chrono::steady_clock::now();
-    batch.timings.merge_ns = std::uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(t_end - t_merge).count());
-    batch.timings.total_ns = std::uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(t_end - t_total).count());
-    return batch;
+    std::vector<genie_index*> handles;
+    std::vector<std::uint32_t> offsets;
+    for (const auto& p : partitions) {
+        handles.push_back(p.index.device());
+        offsets.push_back(p.id_offset);
+    }
+    char err[1024] = {};
+    genie_group* g = nullptr;
+    detail::check(genie_group_from_indexes(handles.data(), offsets.data(), std::uint32_t(handles.size()),
+                                           GENIE_EXCHANGE_AUTO, &g, err, sizeof(err)),
+                  err);
+    std::unique_ptr<genie_group, void (*)(genie_group*)> guard(g, genie_group_destroy);
+    const detail::FlatBatch f(queries);
+    const auto Q = static_cast<std::uint32_t>(queries.size());
+    const std::uint32_t stride = std::max<std::uint32_t>(1, std::min<std::uint64_t>(f.max_k, std::max<std::uint64_t>(expected, 1)));
+    std::vector<genie_entry> out(std::size_t(Q) * stride);
+    std::vector<std::uint32_t> len(Q), thr(Q);
+    genie_stage_ns t{};
+    genie_batch_stats st{};
+    detail::check(genie_group_query_batch(g, &cfg, Q, f.qid.data(), f.k.data(), f.off.data(), f.dim.data(),
+                                          f.lo.data(), f.hi.data(), stride, out.data(), len.data(), thr.data(), &t,
+                                          &st, err, sizeof(err)),
+                  err);
+    return detail::to_batch(f, stride, out, len, thr, t, st);
 }
 
 // ------------------------------------------------------------------ lsh.hpp

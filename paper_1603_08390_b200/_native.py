@@ -114,7 +114,25 @@ ENGINE_SYMBOLS = {
     "genie_index_from_tokens_device": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
                                                  C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "genie_index_export": (C.c_int, [vp, u64p, u64p, u32p, C.c_char_p, C.c_size_t]),
+    "genie_mcix_parse_spans": (C.c_int, [vp, C.c_uint64, u64p, u16p, u64p, C.c_char_p, C.c_size_t]),
+    "genie_mcix_serialize_spans": (C.c_int, [C.c_uint32, C.c_uint64, u64p, u16p, u64p, C.c_uint64, u32p, vp, u64p,
+                                             C.c_char_p, C.c_size_t]),
+    "genie_merge_topk_device_layout": (C.c_int, [vp, C.c_uint32, C.c_uint32, vp, vp, C.c_uint32, C.c_uint32, vp,
+                                                 C.c_uint32, vp, vp, vp, vp, C.c_char_p, C.c_size_t]),
+    "genie_group_create": (C.c_int, [C.c_uint32, C.c_uint64, u64p, u64p, u32p, C.c_uint32, C.POINTER(C.c_int),
+                                     C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
+    "genie_group_from_indexes": (C.c_int, [C.POINTER(vp), u32p, C.c_uint32, C.c_int, C.POINTER(vp), C.c_char_p,
+                                           C.c_size_t]),
+    "genie_group_destroy": (None, [vp]),
+    "genie_group_info": (C.c_int, [vp, u32p, C.POINTER(C.c_int), u32p]),
+    "genie_group_query_batch": (C.c_int, [vp, C.POINTER(Config), C.c_uint32, u32p, u32p, u64p, u16p, u32p, u32p,
+                                          C.c_uint32, C.POINTER(Entry), u32p, u32p, C.POINTER(StageNs),
+                                          C.POINTER(BatchStats), C.c_char_p, C.c_size_t]),
 }
+
+GENIE_EXCHANGE_AUTO = 0
+GENIE_EXCHANGE_NCCL = 1
+GENIE_EXCHANGE_PEER = 2
 
 SYNTH_SYMBOLS = {
     "genie_synth_adult": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(vp)]),

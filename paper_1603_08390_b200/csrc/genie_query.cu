@@ -39,6 +39,15 @@ namespace genie {
 
 // ------------------------------------------------------------------ params
 
+// Everything k_scan needs about a query, one 80-byte record (k_plan; nd is
+// counted by k_cut): warp 0 prefetches it with five 16-byte asynchronous
+// copies one item ahead, so preparing an item starts with it in shared memory.
+struct __align__(16) QueryPlan {
+    uint64_t cut_base, span_base, out_base, item0;
+    uint32_t S, nt, W, k, bound, tile_base, cap, nd, nitems, pad[3];
+};
+static_assert(sizeof(QueryPlan) == 80, "five 16-byte copies");
+
 struct BatchParams {
     // index
     const uint64_t* keys;
@@ -66,8 +75,9 @@ struct BatchParams {
     uint32_t selector;
     // workspace
     uint64_t *q_bound, *q_P, *q_span_base, *q_cut_base, *q_out_base;
-    uint32_t *q_S, *q_W, *q_ntiles, *q_cap, *q_tile_base, *q_rank, *q_big, *q_floor, *q_nd;
+    uint32_t *q_S, *q_W, *q_ntiles, *q_cap, *q_tile_base, *q_rank, *q_big, *q_floor;
     uint32_t* tile_rec;  // [work items][kRecWords]: what each finished tile emitted (see gate_start)
+    QueryPlan* plan;     // [Q]
     uint32_t ht_slots;
     uint32_t *it_kb, *it_nk, *it_sbase;
     uint64_t* span_beg;
@@ -171,7 +181,6 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
     p.q_S[q] = carry;
     p.q_P[q] = P;
     p.q_floor[q] = 0;
-    p.q_nd[q] = 0;
     p.q_W[q] = W;
     p.q_ntiles[q] = nt;
     if (nt) atomicAdd(&p.st[ST_TOTAL_POSTINGS], static_cast<unsigned long long>(P));
@@ -219,6 +228,23 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
             p.q_cap[q] = cap;
             const unsigned long long r = c_cls + e_cls;
             p.q_rank[q] = nt ? static_cast<uint32_t>((r >> (21 * wclass(W))) & 0x1fffffull) : 0;
+            QueryPlan pl;
+            pl.cut_base = c_cut + e_cut;
+            pl.span_base = c_span + e_span;
+            pl.out_base = c_out + e_out;
+            pl.item0 = p.item_off[q];
+            pl.S = p.q_S[q];
+            pl.nt = nt;
+            pl.W = W;
+            pl.k = p.k[q];
+            const uint64_t qb = p.q_bound[q];
+            pl.bound = qb < 1 ? 1u : (qb > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(qb));
+            pl.tile_base = static_cast<uint32_t>(c_tile + e_tile);
+            pl.cap = cap;
+            pl.nd = 0;  // k_cut counts the query's dense spans
+            pl.nitems = static_cast<uint32_t>(p.item_off[q + 1] - pl.item0);
+            pl.pad[0] = pl.pad[1] = pl.pad[2] = 0;
+            p.plan[q] = pl;
         }
         c_span += t_span;
         c_cut += t_cut;
@@ -294,7 +320,7 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
     for (uint64_t g0 = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * G; g0 < total;
          g0 += nwarps * G) {
         const uint64_t g = g0 + lane;
-        uint32_t npair = 0, len = 0, nt = 0, T = 0;
+        uint32_t npair = 0, len = 0, nt = 0, T = 0, cst = 0;
         uint64_t beg = 0, cbase = 0;
         if (lane < G && g < total) {
             // query owning global span g (last q with span_base <= g)
@@ -313,13 +339,16 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
             if (ds >= 0 && inv && uint64_t(len) * inv < p.n) ds = -1;
             p.span_beg[g] = beg;
             p.span_dense[g] = ds;
-            if (ds >= 0) atomicAdd(&p.q_nd[q], 1u);  // dense spans per query
+            if (ds >= 0) atomicAdd(&p.plan[q].nd, 1u);  // dense spans per query
             // k_scan uses the bitmaps when all of the query's spans fit one
             // staging batch; then this list needs no tile cuts
             if (!(ds >= 0 && p.q_S[q] <= kSpanBatch)) {
                 nt = p.q_ntiles[q];
                 T = tile_objs(p, p.q_W[q]);
-                cbase = p.q_cut_base[q] + uint64_t(s) * (nt + 1);
+                // boundary-major: boundary b of span s at q_cut_base + b * S + s,
+                // so an item (q, t) stages rows t and t + 1 with coalesced loads
+                cst = p.q_S[q];
+                cbase = p.q_cut_base[q] + s;
                 npair = nt + 1;
             }
         }
@@ -339,13 +368,14 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
             const uint32_t o_T = __shfl_sync(0xffffffffu, T, o & 31);
             const uint64_t o_beg = __shfl_sync(0xffffffffu, beg, o & 31);
             const uint64_t o_cb = __shfl_sync(0xffffffffu, cbase, o & 31);
+            const uint32_t o_st = __shfl_sync(0xffffffffu, cst, o & 31);
             if (idx < tot) {
                 const uint32_t b = idx - (o_incl - o_np);
                 uint32_t v;
                 if (b == 0) v = 0;
                 else if (b == o_nt) v = o_len;
                 else v = static_cast<uint32_t>(lower_bound_dev(p.postings + o_beg, o_len, b * o_T));
-                p.cuts[o_cb + b] = v;
+                p.cuts[o_cb + uint64_t(b) * o_st] = v;
             }
         }
     }
@@ -390,6 +420,7 @@ struct ScanSmem {
     unsigned long long* sums;  // block scan scratch (32)
     uint32_t* scal;            // scalars
     ItemDesc* desc;            // [2]
+    QueryPlan* plan;           // prefetched plan of the query prepare_item works on next
     uint8_t* stage;            // 2 x StageBuf
     __device__ __forceinline__ StageBuf sb(uint32_t b) const { return StageBuf{stage + b * (kSpanBatch * 20 + 16)}; }
 };
@@ -401,15 +432,15 @@ enum ScalarSlot {
     SC_UCTR = 4,        // guided-scheduling cursor
     SC_T = 7,           // hist_select scratch
     SC_FLOOR = 10,      // gate start of the item
-    SC_PF_ITEM = 13,    // next work item claimed ahead by prepare_item, its query and tile
+    SC_PF_ITEM = 13,    // the item the next prepare_item prepares (claimed and resolved), its query and tile
     SC_PF_Q = 14,
     SC_PF_T = 15,
+    SC_CLAIM = 28,      // the item after it: claimed, not yet resolved to (query, tile)
     SC_LVL = 16,        // dense-phase level counts (kLvl <= 8)
     SC_ADM_CALLS = 24,  // instrumented builds only
     SC_ADM_PASS = 25,
     SC_WMAX = 26,       // instrumented builds: slowest / fastest scan warp of the item
     SC_WMIN = 27,
-    SC_PF1 = 28,        // second set of the SC_PF_* slots (item, query, tile), by buffer parity
     SC_WORDS = 31
 };
 static_assert(SC_WORDS <= 32, "scalar area");
@@ -418,7 +449,8 @@ namespace smem_off {
 constexpr uint32_t kScal = 0;                                  // SC_WORDS u32 (<= 32)
 constexpr uint32_t kSums = 128;                                // 32 u64
 constexpr uint32_t kDesc = kSums + 256;                        // 2 x ItemDesc
-constexpr uint32_t kZa = kDesc + 2 * sizeof(ItemDesc);         // kZaMax u32
+constexpr uint32_t kPlan = kDesc + 2 * sizeof(ItemDesc);       // QueryPlan of the next item's query
+constexpr uint32_t kZa = kPlan + sizeof(QueryPlan);            // kZaMax u32
 constexpr uint32_t kStage = kZa + kZaMax * 4;                  // 2 x StageBuf
 constexpr uint32_t kStageBytes = kSpanBatch * (8 + 4 + 4 + 4) + 16;
 constexpr uint32_t kHt = kStage + 2 * kStageBytes;             // ht_slots u64, then the tile
@@ -431,6 +463,7 @@ __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t ht_slots) {
     s.scal = reinterpret_cast<uint32_t*>(base + kScal);
     s.sums = reinterpret_cast<unsigned long long*>(base + kSums);
     s.desc = reinterpret_cast<ItemDesc*>(base + kDesc);
+    s.plan = reinterpret_cast<QueryPlan*>(base + kPlan);
     s.za = reinterpret_cast<uint32_t*>(base + kZa);
     s.stage = base + kStage;
     static_assert(kStageBytes == kSpanBatch * 20 + 16, "stage buffer layout");
@@ -1477,8 +1510,9 @@ __device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanS
     const uint32_t warp = (threadIdx.x >> 5) - wfirst;
     const uint32_t nwarps = (blockDim.x >> 5) - wfirst;
     if (ptot && uint64_t(ptot) * kCompactFillInv < uint64_t(G) * 128) {  // short slices: compact mode
-        const uint32_t r0 = static_cast<uint32_t>(uint64_t(ptot) * warp / nwarps);
-        const uint32_t r1 = static_cast<uint32_t>(uint64_t(ptot) * (warp + 1) / nwarps);
+        // contiguous shares of ceil(ptot / nwarps) (32-bit arithmetic)
+        const uint32_t share = (ptot + nwarps - 1) / nwarps;
+        const uint32_t r0 = min(ptot, warp * share), r1 = min(ptot, r0 + share);
         if (it.gate) scan_compact<W, true, IL>(p.postings, it, sm, sb, nsb, r0, r1);
         else scan_compact<W, false, IL>(p.postings, it, sm, sb, nsb, r0, r1);
         return;
@@ -1488,8 +1522,8 @@ __device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanS
         // round-robin groups: every warp's share mixes hot (L2) and cold lists
         scan_group_range<W, IL>(p, it, sm, sb, nsb, G, warp, G, nwarps);
 #else
-        const uint32_t g0 = static_cast<uint32_t>(uint64_t(G) * warp / nwarps);
-        const uint32_t g1 = static_cast<uint32_t>(uint64_t(G) * (warp + 1) / nwarps);
+        // G <= kStaticGroups * nwarps: the products stay far below 2^32
+        const uint32_t g0 = G * warp / nwarps, g1 = G * (warp + 1) / nwarps;
         scan_group_range<W, IL>(p, it, sm, sb, nsb, G, g0, g1);
 #endif
         return;
@@ -1519,7 +1553,7 @@ __device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanS
 struct StageArgs {
     bool item_mode, dense;
     uint64_t i0, cb, sbq;
-    uint32_t nt;
+    uint32_t nt, S;  // tiles of the query; its spans (the length of a cut row)
 };
 
 __device__ __forceinline__ void stage_one(const BatchParams& p, const StageArgs& a, uint32_t t, uint32_t s,
@@ -1538,16 +1572,48 @@ __device__ __forceinline__ void stage_one(const BatchParams& p, const StageArgs&
                 return;
             }
         }
-        const uint32_t* c = p.cuts + a.cb + uint64_t(s) * (a.nt + 1) + t;
+        const uint32_t* c = p.cuts + a.cb + uint64_t(t) * a.S + s;
         beg = p.span_beg[a.sbq + s] + c[0];
-        len = c[1] - c[0];
+        len = c[a.S] - c[0];
     }
 }
 
-// Warp variant: spans [s0, s0 + nsb), nsb <= kSpanBatch, 32 at a time.
-__device__ __forceinline__ uint32_t stage_warp(const BatchParams& p, const StageArgs& a, const StageBuf& sb,
-                                               uint32_t t, uint32_t s0, uint32_t nsb) {
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Warp variant, first half: the raw words of spans [s0, s0 + nsb) of a
+// multi-tile item -- span start, its cut at tile t and t + 1, dense slot --
+// go straight from global memory into the stage buffer with asynchronous
+// copies (no registers held), all in flight at once; the rows of the
+// boundary-major cut table make them coalesced.  Item-mode spans (one-tile
+// queries) are read by stage_warp_finish.
+__device__ __forceinline__ void stage_warp_issue(const BatchParams& p, const StageArgs& a, const StageBuf& sb,
+                                                 uint32_t t, uint32_t s0, uint32_t nsb) {
+    if (a.item_mode) return;
+    const uint32_t* c0 = p.cuts + a.cb + uint64_t(t) * a.S + s0;
+    for (uint32_t i = threadIdx.x & 31; i < nsb; i += 32) {
+        cp_async8(sb.beg() + i, p.span_beg + a.sbq + s0 + i);
+        cp_async4(sb.ppref() + i, c0 + i);
+        cp_async4(sb.upref() + i, c0 + a.S + i);
+        if (a.dense) cp_async4(sb.dense() + i, p.span_dense + a.sbq + s0 + i);
+    }
+}
+
+// Second half: slices (start, length) from the raw words, then group ranks,
+// posting prefix and the compacted dense slots, 32 spans at a time, written
+// over the raw words in place.  Returns the number of 128-posting groups.
+__device__ __forceinline__ uint32_t stage_warp_finish(const BatchParams& p, const StageArgs& a, const StageBuf& sb,
+                                                      uint32_t t, uint32_t s0, uint32_t nsb) {
     const uint32_t lane = threadIdx.x & 31;
+    if (!a.item_mode) {
+        cp_async_wait_all();
+        __syncwarp();
+    }
     uint32_t carry = 0, dcarry = 0, pcarry = 0;
     for (uint32_t c0 = 0; c0 < nsb; c0 += 32) {
         const uint32_t i = c0 + lane;
@@ -1555,9 +1621,19 @@ __device__ __forceinline__ uint32_t stage_warp(const BatchParams& p, const Stage
         uint32_t len = 0, groups = 0;
         int32_t dslot = -1;
         if (i < nsb) {
-            stage_one(p, a, t, s0 + i, beg, len, dslot);
+            if (a.item_mode) {
+                stage_one(p, a, t, s0 + i, beg, len, dslot);
+            } else {
+                dslot = a.dense ? static_cast<int32_t>(sb.dense()[i]) : -1;
+                if (dslot < 0) {  // the list's bitmap (dslot >= 0) covers the tile: no slice
+                    const uint32_t lo = sb.ppref()[i];
+                    beg = sb.beg()[i] + lo;
+                    len = sb.upref()[i] - lo;
+                }
+            }
             groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
         }
+        __syncwarp();  // every lane has read its raw words before any result overwrites them
         const uint32_t incl = warp_inclusive_scan(groups);
         const uint32_t pincl = warp_inclusive_scan(len);
         const uint32_t dm = __ballot_sync(0xffffffffu, dslot >= 0);
@@ -1565,6 +1641,7 @@ __device__ __forceinline__ uint32_t stage_warp(const BatchParams& p, const Stage
             sb.beg()[i] = beg;
             sb.upref()[i] = carry + incl - groups;
             sb.ppref()[i] = pcarry + pincl - len;
+            // compacted slot index <= i: never a raw word still to be read
             if (dslot >= 0) sb.dense()[dcarry + __popc(dm & ((1u << lane) - 1u))] = static_cast<uint32_t>(dslot);
         }
         carry += __shfl_sync(0xffffffffu, incl, 31);
@@ -1572,6 +1649,7 @@ __device__ __forceinline__ uint32_t stage_warp(const BatchParams& p, const Stage
         dcarry += __popc(dm);
     }
     if (lane == 0) sb.ppref()[nsb] = pcarry;  // postings of the batch
+    __syncwarp();
     return carry;
 }
 
@@ -1606,25 +1684,24 @@ __device__ __forceinline__ uint32_t stage_block(const BatchParams& p, const Stag
 
 // The rest of an item once its counters hold the dense part (or zeros):
 // posting scan, then the tile's exact top-k.
-__device__ __forceinline__ StageArgs stage_args(const BatchParams& p, uint32_t q, uint32_t& S) {
+__device__ __forceinline__ StageArgs stage_args(const BatchParams& p, const QueryPlan& pl, uint32_t& S) {
     StageArgs sa;
-    sa.nt = p.q_ntiles[q];
+    sa.nt = pl.nt;
     // one tile: the slices are the items' keyword ranges, contiguous in the
     // postings array (keys of one dim are adjacent); several tiles: one slice
     // per keyword list, cut at the tile boundaries by k_cut
     sa.item_mode = sa.nt == 1;
-    sa.i0 = p.item_off[q];
-    sa.cb = p.q_cut_base[q];
-    sa.sbq = p.q_span_base[q];
-    S = sa.item_mode ? static_cast<uint32_t>(p.item_off[q + 1] - sa.i0) : p.q_S[q];
+    sa.i0 = pl.item0;
+    sa.cb = pl.cut_base;
+    sa.sbq = pl.span_base;
+    sa.S = pl.S;
+    S = sa.item_mode ? pl.nitems : sa.S;
     // dense containers apply when all spans of the query fit one staging batch
     sa.dense = p.n_dense && !sa.item_mode && S <= kSpanBatch;
     return sa;
 }
 
 __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint64_t total);
-__device__ void prepare_gate(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint32_t item, uint32_t q,
-                             uint32_t t);
 
 template <int W, bool IL>
 __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t b,
@@ -1634,15 +1711,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
     const long long t_setup = clock64();
 #endif
     // warps 1.. scan this item's postings while warp 0 prepares the next item
-#if GENIE_GATE_WARP1
-    constexpr uint32_t kScanWarp0 = 2;  // warp 0 prepares, warp 1 computes the gate start
-    if (threadIdx.x >= 32 && threadIdx.x < 64) {
-        const uint32_t pf = (b ^ 1u) ? SC_PF1 : SC_PF_ITEM;
-        prepare_gate(p, sm, b ^ 1u, sm.scal[pf], sm.scal[pf + 1], sm.scal[pf + 2]);
-    } else
-#else
     constexpr uint32_t kScanWarp0 = 1;
-#endif
 #ifdef GENIE_PHASE_TIMERS
     if (threadIdx.x < 32) {
         prepare_item(p, sm, b ^ 1u, total);
@@ -1663,7 +1732,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
     __syncthreads();
     for (uint32_t s0 = kSpanBatch; s0 < S; s0 += kSpanBatch) {  // long queries: further batches
         uint32_t S_;
-        const StageArgs sa = stage_args(p, it.q, S_);
+        const StageArgs sa = stage_args(p, p.plan[it.q], S_);
         const uint32_t nb = min(kSpanBatch, S - s0);
         const uint32_t g = stage_block(p, sa, sm, sm.sb(b), it.t, s0, nb);
         scan_groups<W, IL>(p, it, sm, sm.sb(b), nb, g, p.unit, 0);
@@ -1799,85 +1868,69 @@ __device__ __forceinline__ uint32_t fetch_item(const BatchParams& p, uint64_t to
     return i < total ? static_cast<uint32_t>(i) : 0xffffffffu;
 }
 
-// Warp 0: the CTA's next work item -- claims it, loads its parameters,
-// stages its first batch of spans into stage buffer `buf` and computes where
-// its c-PQ gate starts -- into desc[buf] (valid = 0 when the queue is empty).
-// Runs while the other warps scan the current item, so an item starts with
-// everything it needs already in shared memory.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Warp 0: prepares the CTA's next work item into desc[buf] / stage buffer
+// `buf` while the other warps scan the current one (valid = 0 when the queue
+// is empty).  A two-deep pipeline keeps this to ONE memory round trip per
+// item: on entry the item (query q, tile t) is known and q's plan already sits
+// in shared memory (copied asynchronously by the previous call), and the item
+// after it has been claimed.  This call issues at once the span words of its
+// item (asynchronous copies), the lower tiles' records (gate start), the
+// (query, tile) of the claimed item and the next claim; then it finishes the
+// staging and starts the copy of the claimed item's plan.
 __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint64_t total) {
     const uint32_t lane = threadIdx.x & 31;
     ItemDesc* d = sm.desc + buf;
-    // the item was claimed (and its query / tile read) by the previous call,
-    // into the slot set of this buffer; this call's claim goes to the other
-    const uint32_t pf = buf ? SC_PF1 : SC_PF_ITEM, pf_next = buf ? SC_PF_ITEM : SC_PF1;
-    const uint32_t item = sm.scal[pf];
+    const uint32_t item = sm.scal[SC_PF_ITEM];
     if (item == 0xffffffffu) {
         if (lane == 0) d->valid = 0;
         return;
     }
-    const uint32_t q = sm.scal[pf + 1], t = sm.scal[pf + 2];
-    // claim the one after it now (consumed at the end)
-    uint32_t nitem = 0xffffffffu;
-    if (lane == 0) nitem = fetch_item(p, total);
+    const uint32_t q = sm.scal[SC_PF_Q], t = sm.scal[SC_PF_T], claim = sm.scal[SC_CLAIM];
+    cp_async_wait_all();  // q's plan (previous call)
+    __syncwarp();
+    const QueryPlan pl = *sm.plan;
     uint32_t S;
-    const StageArgs sa = stage_args(p, q, S);
-    const uint32_t W = p.q_W[q];
-    const uint32_t kq = p.k[q];
-    const uint32_t bound = static_cast<uint32_t>(p.q_bound[q] < 1 ? 1 : p.q_bound[q]);
-    const uint32_t tbase = p.q_tile_base[q];
-    const uint32_t cap = p.q_cap[q];
-    const uint32_t ndq = p.q_nd[q];
-    const uint64_t obase = p.q_out_base[q];
-#if GENIE_GATE_WARP1
-    // warp 1 computes the gate start meanwhile (prepare_gate)
-    const uint32_t G = stage_warp(p, sa, sm.sb(buf), t, 0, min(kSpanBatch, S));
-#else
-    const bool gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
-    const uint32_t a0 = gate ? gate_start(p, q, t, kq, bound, tbase) : 0u;
-    const uint32_t G = stage_warp(p, sa, sm.sb(buf), t, 0, min(kSpanBatch, S));
-#endif
-    uint32_t nq = 0, ntile = 0;
-    if (nitem != 0xffffffffu) {
-        nq = p.work_q[nitem];
-        ntile = p.work_t[nitem];
+    const StageArgs sa = stage_args(p, pl, S);
+    const uint32_t nsb = min(kSpanBatch, S);
+    stage_warp_issue(p, sa, sm.sb(buf), t, 0, nsb);
+    uint32_t nq = 0, ntile = 0, nclaim = 0xffffffffu;
+    if (claim != 0xffffffffu) {
+        nq = p.work_q[claim];
+        ntile = p.work_t[claim];
     }
+    if (lane == 0 && claim != 0xffffffffu) nclaim = fetch_item(p, total);
+    const bool gate = (p.selector == GENIE_SELECT_CPQ) && pl.W <= 8;
+    const uint32_t a0 = gate ? gate_start(p, q, t, pl.k, pl.bound, pl.tile_base) : 0u;
+    const uint32_t G = stage_warp_finish(p, sa, sm.sb(buf), t, 0, nsb);
+    if (claim != 0xffffffffu && lane < sizeof(QueryPlan) / 16)
+        cp_async16(reinterpret_cast<uint4*>(sm.plan) + lane, reinterpret_cast<const uint4*>(p.plan + nq) + lane);
+    nclaim = __shfl_sync(0xffffffffu, nclaim, 0);
     if (lane == 0) {
         d->q = q;
         d->t = t;
-        d->kq = kq;
-        d->bound = bound;
-        d->W = W;
-        d->cap = cap;
+        d->kq = pl.k;
+        d->bound = pl.bound;
+        d->W = pl.W;
+        d->cap = pl.cap;
         d->nt = sa.nt;
         d->S = S;
-        d->nd = sa.dense ? ndq : 0u;
+        d->nd = sa.dense ? pl.nd : 0u;
         d->G = G;
-        d->ptot = sm.sb(buf).ppref()[min(kSpanBatch, S)];
-#if !GENIE_GATE_WARP1
+        d->ptot = sm.sb(buf).ppref()[nsb];
         d->a0 = a0;
-#endif
-        d->out_base = obase + uint64_t(t) * cap;
-        d->tile_slot = tbase + t;
+        d->out_base = pl.out_base + uint64_t(t) * pl.cap;
+        d->tile_slot = pl.tile_base + t;
         d->valid = 1;
-        sm.scal[pf_next] = nitem;
-        sm.scal[pf_next + 1] = nq;
-        sm.scal[pf_next + 2] = ntile;
+        sm.scal[SC_PF_ITEM] = claim;
+        sm.scal[SC_PF_Q] = nq;
+        sm.scal[SC_PF_T] = ntile;
+        sm.scal[SC_CLAIM] = nclaim;
     }
-}
-
-// Warp 1: the gate start of the item warp 0 is preparing (same claimed item,
-// read from the prefetch slots before warp 0 moves them on).
-__device__ void prepare_gate(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint32_t item, uint32_t q,
-                             uint32_t t) {
-    if (item == 0xffffffffu) return;
-    const uint32_t W = p.q_W[q];
-    const bool gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
-    uint32_t a0 = 0;
-    if (gate) {
-        const uint64_t qb = p.q_bound[q];
-        a0 = gate_start(p, q, t, p.k[q], static_cast<uint32_t>(qb < 1 ? 1 : qb), p.q_tile_base[q]);
-    }
-    if ((threadIdx.x & 31) == 0) sm.desc[buf].a0 = a0;
+    __syncwarp();
 }
 
 template <int W>
@@ -1981,26 +2034,36 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     if (p.st[ST_OVERFLOW]) return;
     const uint64_t total = p.st[ST_TOTAL_WORK];
     // item i runs from desc[i & 1]; its scan phase prepares item i + 1 into
-    // the other descriptor / stage buffer (prepare_item)
-    if (threadIdx.x == 0) {
-        const uint32_t i0 = fetch_item(p, total);
-        sm.scal[SC_PF_ITEM] = i0;
-        if (i0 != 0xffffffffu) {
-            sm.scal[SC_PF_Q] = p.work_q[i0];
-            sm.scal[SC_PF_T] = p.work_t[i0];
+    // the other descriptor / stage buffer (prepare_item).  Prime the pipeline:
+    // the first item resolved with its plan in shared memory, the second claimed.
+    if (threadIdx.x < 32) {
+        const uint32_t lane = threadIdx.x;
+        uint32_t i0 = 0xffffffffu, i1 = 0xffffffffu;
+        if (lane == 0) {
+            i0 = fetch_item(p, total);
+            if (i0 != 0xffffffffu) i1 = fetch_item(p, total);
         }
-    }
-    __syncthreads();
-#if GENIE_GATE_WARP1
-    if (threadIdx.x >= 32 && threadIdx.x < 64)
-        prepare_gate(p, sm, 0, sm.scal[SC_PF_ITEM], sm.scal[SC_PF_ITEM + 1], sm.scal[SC_PF_ITEM + 2]);
-#endif
-    if (threadIdx.x < 32) prepare_item(p, sm, 0, total);
-    if (threadIdx.x == 0) {
-        sm.scal[SC_ADM_CALLS] = 0;
-        sm.scal[SC_ADM_PASS] = 0;
-        sm.scal[SC_WMAX] = 0;
-        sm.scal[SC_WMIN] = 0xffffffffu;
+        i0 = __shfl_sync(0xffffffffu, i0, 0);
+        i1 = __shfl_sync(0xffffffffu, i1, 0);
+        uint32_t q0 = 0, t0 = 0;
+        if (i0 != 0xffffffffu) {
+            q0 = p.work_q[i0];
+            t0 = p.work_t[i0];
+            if (lane < sizeof(QueryPlan) / 16)
+                cp_async16(reinterpret_cast<uint4*>(sm.plan) + lane, reinterpret_cast<const uint4*>(p.plan + q0) + lane);
+        }
+        if (lane == 0) {
+            sm.scal[SC_PF_ITEM] = i0;
+            sm.scal[SC_PF_Q] = q0;
+            sm.scal[SC_PF_T] = t0;
+            sm.scal[SC_CLAIM] = i1;
+            sm.scal[SC_ADM_CALLS] = 0;
+            sm.scal[SC_ADM_PASS] = 0;
+            sm.scal[SC_WMAX] = 0;
+            sm.scal[SC_WMIN] = 0xffffffffu;
+        }
+        __syncwarp();
+        prepare_item(p, sm, 0, total);
     }
     __syncthreads();
     for (uint32_t iter = 0;; ++iter) {
@@ -2407,7 +2470,7 @@ static void reserve_workspace(genie_index* ix, uint32_t Q, uint32_t items, uint3
         w.q_rank.reserve(c);
         w.q_big.reserve(c);
         w.q_floor.reserve(c);
-        w.q_nd.reserve(c);
+        w.q_plan.reserve(c * (sizeof(QueryPlan) / 16));
         w.cap_q = c;
     }
     if (items > w.cap_items || !w.it_kb.p) {
@@ -2640,7 +2703,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.q_rank = w.q_rank.p;
     p.q_big = w.q_big.p;
     p.q_floor = w.q_floor.p;
-    p.q_nd = w.q_nd.p;
+    p.plan = reinterpret_cast<QueryPlan*>(w.q_plan.p);
     p.tile_rec = w.tile_rec.p;
     p.it_kb = w.it_kb.p;
     p.it_nk = w.it_nk.p;

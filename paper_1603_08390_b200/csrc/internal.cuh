@@ -64,9 +64,6 @@ constexpr uint32_t kLvl = GENIE_DENSE_LEVELS;  // dense-phase c-PQ levels counte
 // compact posting scan when the staged slices fill their 128-posting groups
 // less than 1/kCompactFillInv on average
 constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
-#ifndef GENIE_GATE_WARP1
-#define GENIE_GATE_WARP1 0
-#endif
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
 #endif
@@ -119,7 +116,8 @@ enum StatusWord : int {
 struct Workspace {
     // per query
     DevBuf<uint64_t> q_bound, q_P, q_span_base, q_cut_base, q_out_base;
-    DevBuf<uint32_t> q_S, q_W, q_ntiles, q_cap, q_tile_base, q_rank, q_big, q_floor, q_nd;
+    DevBuf<uint32_t> q_S, q_W, q_ntiles, q_cap, q_tile_base, q_rank, q_big, q_floor;
+    DevBuf<uint4> q_plan;  // QueryPlan records (80 B each, genie_query.cu)
     // per item
     DevBuf<uint32_t> it_kb, it_nk, it_sbase;
     // spans / cuts / work / tiles

@@ -120,18 +120,27 @@ class ShardedIndex:
                 self.index.query_device(d, cfg, stream=stream.cuda_stream)
                 if not self.index.status().get("retry"):
                     break
-            gath = torch.zeros((self.world, Q, S, 2), dtype=torch.int32, device=dev)
-            glen = torch.zeros((self.world, Q), dtype=torch.int32, device=dev)
-            dist.all_gather_into_tensor(gath, d["out"], group=self.group)
-            dist.all_gather_into_tensor(glen, d["out_len"], group=self.group)
-            m_in = gath.permute(1, 0, 2, 3).contiguous()
-            m_len = glen.t().contiguous()
+            st = self.index.status()
+            # [world, Q, S] rows in rank order: the list-major layout the
+            # device merge reads in place
+            if dist.get_backend(self.group) == "nccl":  # NVLink all-gather of device buffers
+                gath = torch.zeros((self.world, Q, S, 2), dtype=torch.int32, device=dev)
+                glen = torch.zeros((self.world, Q), dtype=torch.int32, device=dev)
+                dist.all_gather_into_tensor(gath, d["out"], group=self.group)
+                dist.all_gather_into_tensor(glen, d["out_len"], group=self.group)
+            else:  # CPU process groups (gloo): exchange through host memory
+                rows = [torch.zeros((Q, S, 2), dtype=torch.int32) for _ in range(self.world)]
+                lens = [torch.zeros(Q, dtype=torch.int32) for _ in range(self.world)]
+                dist.all_gather(rows, d["out"].cpu(), group=self.group)
+                dist.all_gather(lens, d["out_len"].cpu(), group=self.group)
+                gath = torch.stack(rows).to(dev)
+                glen = torch.stack(lens).to(dev)
             fin = torch.zeros((Q, S, 2), dtype=torch.int32, device=dev)
             flen = torch.zeros(Q, dtype=torch.int32, device=dev)
             fthr = torch.zeros(Q, dtype=torch.int32, device=dev)
-            self.index.merge_device(Q, self.world, m_in, m_len, S, d["k"], S, fin, flen, fthr,
-                                    stream=stream.cuda_stream)
-            st = self.index.status()
+            self.index.merge_device(Q, self.world, gath, glen, S, d["k"], S, fin, flen, fthr,
+                                    stream=stream.cuda_stream, list_major=True)
+            self.index.status()  # surfaces merge errors (duplicate ids across shards)
         stream.synchronize()
         out = fin.cpu().numpy().view(np.uint32)
         return E.Results(batch.qid.copy(), out[..., 0].copy(), out[..., 1].copy(),

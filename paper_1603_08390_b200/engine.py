@@ -66,6 +66,19 @@ def _ptr(a: np.ndarray, ctype):
 # ----------------------------------------------------------------- inputs
 
 
+def _torch_stream(stream: Optional[int]) -> C.c_void_p:
+    """The CUDA stream a device-array call is ordered on: the given handle, or
+    torch's current stream -- so work queued on torch tensors (uploads, fills)
+    is complete before the kernels read them.  torch's legacy default stream
+    has handle 0, which the C ABI reads as "the handle's own stream"; it is
+    passed as cudaStreamLegacy (0x1) instead."""
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream().cuda_stream
+    return C.c_void_p(stream if stream else 1)
+
+
 @dataclass
 class CSR:
     """Host CSR inverted index: keys (packed dim<<32|token, ascending),
@@ -343,7 +356,7 @@ class DeviceIndex:
         rc = self._lib.genie_query_batch_device(
             self._h, C.byref(cfg), int(d["qid"].numel()), ptr(d["qid"]), ptr(d["k"]), ptr(d["item_off"]),
             ptr(d["dim"]), ptr(d["lo"]), ptr(d["hi"]), int(d["max_k"]), int(d["total_items"]), int(d["stride"]),
-            ptr(d["out"]), ptr(d["out_len"]), ptr(d["out_thr"]), C.c_void_p(stream or 0), err, len(err))
+            ptr(d["out"]), ptr(d["out_len"]), ptr(d["out_thr"]), _torch_stream(stream), err, len(err))
         check(rc, err)
         return int(self._lib.genie_last_launch_count(self._h))
 
@@ -359,15 +372,83 @@ class DeviceIndex:
         return {f: getattr(stats, f) for f, _ in N.BatchStats._fields_}
 
     def merge_device(self, Q: int, L: int, d_in, d_in_len, in_stride: int, d_k, stride: int, d_out, d_out_len,
-                     d_out_thr, stream: Optional[int] = None) -> None:
+                     d_out_thr, stream: Optional[int] = None, list_major: bool = False) -> None:
         """merge_topk over per-shard lists resident on this device (the
-        multi-GPU combine step after an all-gather)."""
+        multi-GPU combine step after an all-gather): lists query-major
+        [Q, L, in_stride] or, with list_major, [L, Q, in_stride] -- the order
+        an all-gather of per-shard rows produces."""
         err = _errbuf()
         ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
-        rc = self._lib.genie_merge_topk_device(self._h, Q, L, ptr(d_in), ptr(d_in_len), in_stride, ptr(d_k), stride,
-                                               ptr(d_out), ptr(d_out_len), ptr(d_out_thr), C.c_void_p(stream or 0),
-                                               err, len(err))
+        rc = self._lib.genie_merge_topk_device_layout(self._h, Q, L, ptr(d_in), ptr(d_in_len), in_stride,
+                                                      int(list_major), ptr(d_k), stride, ptr(d_out), ptr(d_out_len),
+                                                      ptr(d_out_thr), _torch_stream(stream), err, len(err))
         check(rc, err)
+
+
+class DeviceGroup:
+    """Object-id-range shards of one index on several devices, driven by this
+    one host thread (genie_group_*): every shard's batch runs at
+    once, rows are exchanged (NCCL all-gather when the shards sit on distinct
+    devices, peer copies otherwise) and merged on the first device."""
+
+    def __init__(self, handle: int, lib, keep=()):
+        self._h = C.c_void_p(handle)
+        self._lib = lib
+        self._keep = list(keep)  # borrowed DeviceIndex objects stay alive
+        n, ex, no = C.c_uint32(), C.c_int(), C.c_uint32()
+        lib.genie_group_info(self._h, C.byref(n), C.byref(ex), C.byref(no))
+        self.num_shards, self.exchange, self.num_objects = n.value, ex.value, no.value
+
+    @classmethod
+    def from_csr(cls, csr: CSR, devices, exchange: int = N.GENIE_EXCHANGE_AUTO) -> "DeviceGroup":
+        lib = N.engine()
+        devs = (C.c_int * len(devices))(*devices)
+        h, err = C.c_void_p(), _errbuf()
+        key_off = csr.key_off if csr.key_off.size else np.zeros(1, np.uint64)
+        check(lib.genie_group_create(csr.n, csr.num_keys, _ptr(csr.keys, C.c_uint64), _ptr(key_off, C.c_uint64),
+                                     _ptr(csr.postings, C.c_uint32), len(devices), devs, exchange, C.byref(h), err,
+                                     len(err)), err)
+        return cls(h.value, lib)
+
+    @classmethod
+    def from_indexes(cls, indexes, id_offsets, exchange: int = N.GENIE_EXCHANGE_AUTO) -> "DeviceGroup":
+        lib = N.engine()
+        hs = (C.c_void_p * len(indexes))(*[ix.handle.value for ix in indexes])
+        offs = np.ascontiguousarray(id_offsets, np.uint32)
+        h, err = C.c_void_p(), _errbuf()
+        check(lib.genie_group_from_indexes(hs, _ptr(offs, C.c_uint32), len(indexes), exchange, C.byref(h), err,
+                                           len(err)), err)
+        return cls(h.value, lib, keep=indexes)
+
+    def close(self):
+        if self._h and self._h.value:
+            self._lib.genie_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def query(self, batch: QueryBatch, cfg: Optional[N.Config] = None, stride: Optional[int] = None,
+              timings: bool = False) -> Results:
+        Q = len(batch)
+        stride = int(stride if stride is not None else max(min(batch.max_k, self.num_objects), 1))
+        ent = np.zeros((Q, stride, 2), dtype=np.uint32)
+        ln = np.zeros(Q, np.uint32)
+        thr = np.zeros(Q, np.uint32)
+        st, stats, err = N.StageNs(), N.BatchStats(), _errbuf()
+        cfg = cfg if cfg is not None else config()
+        rc = self._lib.genie_group_query_batch(
+            self._h, C.byref(cfg), Q, _ptr(batch.qid, C.c_uint32), _ptr(batch.k, C.c_uint32),
+            _ptr(batch.item_off, C.c_uint64), _ptr(batch.dim, C.c_uint16), _ptr(batch.lo, C.c_uint32),
+            _ptr(batch.hi, C.c_uint32), stride, ent.ctypes.data_as(C.POINTER(N.Entry)), _ptr(ln, C.c_uint32),
+            _ptr(thr, C.c_uint32), C.byref(st) if timings else None, C.byref(stats), err, len(err))
+        check(rc, err)
+        tdict = {f: getattr(st, f) for f, _ in N.StageNs._fields_} if timings else None
+        sdict = {f: getattr(stats, f) for f, _ in N.BatchStats._fields_}
+        return Results(batch.qid.copy(), ent[:, :, 0].copy(), ent[:, :, 1].copy(), ln, thr, None, tdict, sdict)
 
 
 def merge_lists(lists_ids: np.ndarray, lists_counts: np.ndarray, lists_len: np.ndarray, k: np.ndarray,
@@ -459,7 +540,7 @@ class Encoder:
     def encode_device(self, d_points, d_tokens, stream: Optional[int] = None) -> None:
         err = _errbuf()
         check(self._lib.genie_lsh_encode_device(self._h, C.c_void_p(d_points.data_ptr()), int(d_points.shape[0]),
-                                                C.c_void_p(d_tokens.data_ptr()), C.c_void_p(stream or 0), err,
+                                                C.c_void_p(d_tokens.data_ptr()), _torch_stream(stream), err,
                                                 len(err)), err)
 
     def encode_sets(self, set_off: np.ndarray, elems: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
@@ -478,7 +559,7 @@ class Encoder:
         err = _errbuf()
         check(self._lib.genie_minhash_encode_device(self._h, C.c_void_p(d_off.data_ptr()),
                                                     C.c_void_p(d_elems.data_ptr()), int(d_off.shape[0]) - 1,
-                                                    C.c_void_p(d_tokens.data_ptr()), C.c_void_p(stream or 0), err,
+                                                    C.c_void_p(d_tokens.data_ptr()), _torch_stream(stream), err,
                                                     len(err)), err)
 
 
