@@ -4,7 +4,7 @@
  *
  * The reference (mcx, /root/reference/proj/include) has no FFI layer: its
  * hot path is inline C++ in namespace mcx.  These entry points are exactly
- * what a binding of that path needs; the C++ mirror in include/mcx/*.hpp
+ * what a binding of that path needs; the C++ mirror in the include/mcx headers
  * (same names and semantics as the reference) and the Python mirror
  * (paper_1603_08390_b200.mcx) are thin hosts over them.  Each function names
  * the reference interface it replaces.
