@@ -295,6 +295,23 @@ int genie_group_query_batch(genie_group* g, const genie_config* cfg, uint32_t nu
                             uint32_t* out_len, uint32_t* out_threshold, genie_stage_ns* timings,
                             genie_batch_stats* stats, char* err, size_t errlen);
 
+/* Sequence verification (SequenceSearcher, sa.hpp:127-162, 298-336,
+ * 419-512) ---------------------------------------------------------------- *
+ * A device-resident corpus of byte strings: sequence i is
+ * bytes[off[i], off[i+1]).  genie_seqset_distances: Levenshtein distance
+ * (unit costs) of `query` to sequences ids[0..count) -- or to sequences
+ * 0..count-1 when ids is NULL (the exhaustive scan) -- with
+ * edit_distance_bounded's contract: the exact distance when <= cap, else
+ * cap + 1 (cap = UINT32_MAX: always exact).  Bit-parallel (Myers/Hyyro) on
+ * the GPU, one thread per pair; out[count] host buffer. */
+typedef struct genie_seqset genie_seqset;
+int genie_seqset_create(const uint8_t* bytes, const uint64_t* off, uint64_t num_sequences, int device,
+                        genie_seqset** out, char* err, size_t errlen);
+void genie_seqset_destroy(genie_seqset* s);
+void genie_seqset_info(const genie_seqset* s, uint64_t* num_sequences, uint64_t* total_bytes, int* device);
+int genie_seqset_distances(genie_seqset* s, const uint8_t* query, uint64_t query_len, const uint32_t* ids,
+                           uint64_t count, uint32_t cap, uint32_t* out, char* err, size_t errlen);
+
 /* LSH / minHash transforms ------------------------------------------------- */
 
 /* mcx::LshFamily (lsh.hpp:130) plus minHash (new). */

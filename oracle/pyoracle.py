@@ -216,6 +216,12 @@ class RefLib:
                                         C.c_int64, C.c_int, C.c_double, f32p, C.c_uint64, C.c_uint32, u32p, *E]
         L.mcxref_lsh_params.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_double, C.c_double, f64p,
                                         f64p, u64p, *E]
+        L.mcxref_edit_distance_bounded.restype = C.c_uint32
+        L.mcxref_edit_distance_bounded.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, C.c_uint32,
+                                                   C.c_int]
+        L.mcxref_verify_candidates.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, u32p, u32p, C.c_uint32,
+                                               C.c_char_p, u64p, C.c_uint64, C.c_uint64, C.c_int, u32p, u32p,
+                                               C.POINTER(C.c_int), u32p, C.POINTER(C.c_int64), *E]
         L.mcxref_kernel_width.restype = C.c_double
         L.mcxref_kernel_width.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_uint64]
         L.mcxref_index_serialize.argtypes = [vp, vp, u64p, *E]
@@ -307,6 +313,78 @@ class RefLib:
     def kernel_width(self, points, max_pairs=1_000_000):
         pts = np.ascontiguousarray(points, np.float32)
         return float(self.L.mcxref_kernel_width(_p(pts, C.c_float), pts.shape[0], pts.shape[1], max_pairs))
+
+    def edit_distance(self, a: bytes, b: bytes, cap=None) -> int:
+        return int(self.L.mcxref_edit_distance_bounded(a, len(a), b, len(b), cap or 0, int(cap is not None)))
+
+    def verify_candidates(self, query: bytes, ids, counts, n, corpus, requested_k=0, early_break=True):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        counts = np.ascontiguousarray(counts, np.uint32)
+        off = np.zeros(len(corpus) + 1, np.uint64)
+        off[1:] = np.cumsum([len(c) for c in corpus])
+        blob = b"".join(corpus)
+        bi, bd, used = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        cert, theta = C.c_int(), C.c_int64()
+        err = C.create_string_buffer(512)
+        rc = self.L.mcxref_verify_candidates(query, len(query), ids.shape[0], _p(ids, C.c_uint32),
+                                             _p(counts, C.c_uint32), n, blob, _p(off, C.c_uint64), len(corpus),
+                                             requested_k, int(early_break), C.byref(bi), C.byref(bd), C.byref(cert),
+                                             C.byref(used), C.byref(theta), err, len(err))
+        self._check(rc, err)
+        return bi.value, bd.value, bool(cert.value), used.value, theta.value
+
+
+# ---- sequence search restated in plain Python (sa.hpp), small cases only
+
+def edit_distance(a: bytes, b: bytes) -> int:
+    """sa.hpp:109-123: unit-cost Levenshtein distance, two-row DP."""
+    if len(a) < len(b):
+        a, b = b, a
+    row = list(range(len(b) + 1))
+    for i in range(1, len(a) + 1):
+        diag, row[0] = row[0], i
+        for j in range(1, len(b) + 1):
+            up = row[j]
+            row[j] = min(up + 1, row[j - 1] + 1, diag + (a[i - 1] != b[j - 1]))
+            diag = up
+    return row[len(b)]
+
+
+def edit_distance_bounded(a: bytes, b: bytes, cap: int) -> int:
+    """sa.hpp:127-162: the exact distance when <= cap, else cap + 1."""
+    if abs(len(a) - len(b)) > cap:
+        return cap + 1
+    return min(edit_distance(a, b), cap + 1)
+
+
+def verify_candidates(query: bytes, hits, n: int, corpus, requested_k: int = 0, early_break: bool = True,
+                      dist=None):
+    """sa.hpp:298-336.  hits: [(id, count)] by descending count.  `dist(id, cap)`
+    supplies bounded distances (default: the DP above).  Returns (best_id,
+    best_distance, certified, candidates_used, threshold_at_stop)."""
+    if not hits:
+        raise ValueError("verify_candidates: empty candidate list")
+    dist = dist or (lambda i, cap: edit_distance(query, corpus[i]) if cap is None
+                    else edit_distance_bounded(query, corpus[i], cap))
+    requested_k = requested_k or len(hits)
+    qlen = len(query)
+    best_id = hits[0][0]
+    best = dist(best_id, None)  # cap None: the exact distance (edit_distance)
+    used = 1
+    theta = qlen - n + 1 - n * (best - 1)
+    for cid, cnt in hits[1:]:
+        if early_break and theta > cnt:
+            break
+        used += 1
+        if abs(len(corpus[cid]) - qlen) > best or best == 0:
+            continue
+        d = dist(cid, best - 1)
+        if d < best:
+            best_id, best = cid, d
+            theta = qlen - n + 1 - n * (d - 1)
+    c_k = hits[-1][1] if len(hits) >= requested_k else 0
+    certified = c_k < qlen - n + 1 - best * n
+    return best_id, best, certified, used, theta
 
 
 class RefIndex:

@@ -402,4 +402,32 @@ std::uint64_t mcxref_hash_results(std::uint32_t Q, const std::uint32_t* qid,
     return mcx::hash_results(rs);
 }
 
+// sa.hpp:127-162: the reference's edit distances (golden vectors)
+std::uint32_t mcxref_edit_distance_bounded(const char* a, std::uint64_t la, const char* b, std::uint64_t lb,
+                                           std::uint32_t cap, int bounded) {
+    const std::string_view x(a, la), y(b, lb);
+    return bounded ? mcx::edit_distance_bounded(x, y, cap) : mcx::edit_distance(x, y);
+}
+
+// sa.hpp:298-336: verify_candidates over a corpus (strings at off[i]..off[i+1])
+int mcxref_verify_candidates(const char* query, std::uint64_t qlen, std::uint32_t n_cand, const std::uint32_t* ids,
+                             const std::uint32_t* counts, std::uint32_t n, const char* corpus_bytes,
+                             const std::uint64_t* off, std::uint64_t n_corpus, std::uint64_t requested_k,
+                             int early_break, std::uint32_t* best_id, std::uint32_t* best_distance, int* certified,
+                             std::uint32_t* used, std::int64_t* theta, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::vector<std::string> corpus(n_corpus);
+        for (std::uint64_t i = 0; i < n_corpus; ++i) corpus[i].assign(corpus_bytes + off[i], off[i + 1] - off[i]);
+        std::vector<mcx::CandidateHit> hits(n_cand);
+        for (std::uint32_t i = 0; i < n_cand; ++i) hits[i] = {ids[i], counts[i]};
+        const auto o = mcx::verify_candidates(std::string_view(query, qlen), hits, n, corpus, requested_k,
+                                              early_break != 0);
+        *best_id = o.best_id;
+        *best_distance = o.best_distance;
+        *certified = o.certified;
+        *used = o.candidates_used;
+        *theta = o.threshold_at_stop;
+    });
+}
+
 }  // extern "C"

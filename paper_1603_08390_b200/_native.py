@@ -125,6 +125,11 @@ ENGINE_SYMBOLS = {
                                            C.c_size_t]),
     "genie_group_destroy": (None, [vp]),
     "genie_group_info": (C.c_int, [vp, u32p, C.POINTER(C.c_int), u32p]),
+    "genie_seqset_create": (C.c_int, [vp, u64p, C.c_uint64, C.c_int, C.POINTER(vp), C.c_char_p, C.c_size_t]),
+    "genie_seqset_destroy": (None, [vp]),
+    "genie_seqset_info": (None, [vp, u64p, u64p, C.POINTER(C.c_int)]),
+    "genie_seqset_distances": (C.c_int, [vp, vp, C.c_uint64, u32p, C.c_uint64, C.c_uint32, u32p, C.c_char_p,
+                                         C.c_size_t]),
     "genie_group_query_batch": (C.c_int, [vp, C.POINTER(Config), C.c_uint32, u32p, u32p, u64p, u16p, u32p, u32p,
                                           C.c_uint32, C.POINTER(Entry), u32p, u32p, C.POINTER(StageNs),
                                           C.POINTER(BatchStats), C.c_char_p, C.c_size_t]),

@@ -477,6 +477,50 @@ def merge_lists(lists_ids: np.ndarray, lists_counts: np.ndarray, lists_len: np.n
 PSTABLE, RBH, MINHASH = 0, 1, 2
 
 
+class SeqSet:
+    """A device-resident corpus of byte strings and the GPU edit-distance
+    kernel over it (genie_seqset_*, sa.hpp:127-162): distances of a query to
+    chosen sequences (or all of them), exact up to `cap`, cap + 1 beyond."""
+
+    UNCAPPED = 0xFFFFFFFF
+
+    def __init__(self, corpus, device: int = 0):
+        seqs = [s if isinstance(s, bytes) else str(s).encode() for s in corpus]
+        off = np.zeros(len(seqs) + 1, np.uint64)
+        off[1:] = np.cumsum([len(s) for s in seqs])
+        blob = np.frombuffer(b"".join(seqs) + b"\0", np.uint8)
+        self._lib = N.engine()
+        h, err = C.c_void_p(), _errbuf()
+        check(self._lib.genie_seqset_create(C.c_void_p(blob.ctypes.data), _ptr(off, C.c_uint64), len(seqs), device,
+                                            C.byref(h), err, len(err)), err)
+        self._h = h
+        self.lengths = np.diff(off).astype(np.int64)
+        self.num_sequences = len(seqs)
+
+    def close(self):
+        if self._h and self._h.value:
+            self._lib.genie_seqset_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def distances(self, query, ids=None, cap: int = UNCAPPED) -> np.ndarray:
+        q = query if isinstance(query, bytes) else str(query).encode()
+        qa = np.frombuffer(q + b"\0", np.uint8)
+        idv = None if ids is None else np.ascontiguousarray(ids, np.uint32)
+        count = self.num_sequences if idv is None else idv.shape[0]
+        out = np.zeros(max(count, 1), np.uint32)
+        err = _errbuf()
+        check(self._lib.genie_seqset_distances(self._h, C.c_void_p(qa.ctypes.data), len(q),
+                                               None if idv is None else _ptr(idv, C.c_uint32), count, cap,
+                                               _ptr(out, C.c_uint32), err, len(err)), err)
+        return out[:count]
+
+
 def lsh_config(family: int = RBH, m: int = 237, dims: int = 0, seed: int = 1, rehash_domain: int = 8192,
                w: float = 4.0, bucket_count: int = 67, bucket_min: int = -33, rehash_pstable: bool = False,
                sigma: float = 1.0) -> N.LshConfig:

@@ -5,6 +5,9 @@ for the reference API and, on a GPU, agrees with the oracle:
   tests/cpp/test_reference_api.cpp  the reference's test_index.cpp cases, the
                                     relational encoders, LshEncoder::token and
                                     acceptance criteria 1, 3, 10, 12 (engine half)
+  tests/cpp/test_sequence.cpp       the reference's sequence-search tests
+                                    (test_sa.cpp): SequenceSearcher with GPU
+                                    retrieval + GPU edit-distance verification
   tests/cpp/test_dataset.cpp        the reference's dataset tests (CSV + schema,
                                     discretize, vector files, encoder sidecar);
                                     CPU, plus the fig1 pipeline on the GPU
@@ -15,7 +18,7 @@ from pathlib import Path
 import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
-SOURCES = ["test_dropin", "test_reference_api", "test_dataset"]
+SOURCES = ["test_dropin", "test_reference_api", "test_dataset", "test_sequence"]
 
 
 def build(tmp_path, name="test_dropin") -> Path:
@@ -58,3 +61,10 @@ def test_dataset_pipeline_on_gpu(gpu, tmp_path):
     exe = build(tmp_path, "test_dataset")
     r = subprocess.run([str(exe), "gpu"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "dataset: ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_sequence_search_on_gpu(gpu, tmp_path):
+    exe = build(tmp_path, "test_sequence")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "sequence: ok" in r.stdout, r.stdout[-4000:] + r.stderr[-4000:]
