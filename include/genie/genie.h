@@ -329,7 +329,12 @@ typedef struct {
     int32_t rehash_pstable;
     int64_t bucket_min;
     double sigma;
+    uint32_t precision; /* GENIE_LSH_FP64 (default: bit-exact with the reference) or GENIE_LSH_FP32 (opt-in fast
+                           mode: fp32 FMA arithmetic; tokens at bucket boundaries may differ -- counted by
+                           tests/test_gpu_lsh.py and reported by bench.py) */
+    uint32_t reserved;
 } genie_lsh_config;
+enum { GENIE_LSH_FP64 = 0, GENIE_LSH_FP32 = 1 };
 
 genie_lsh_config genie_lsh_config_default(void);
 

@@ -70,6 +70,8 @@ class LshConfig(C.Structure):
         ("rehash_pstable", C.c_int32),
         ("bucket_min", C.c_int64),
         ("sigma", C.c_double),
+        ("precision", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 

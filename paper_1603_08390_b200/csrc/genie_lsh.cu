@@ -27,6 +27,7 @@ struct genie_encoder {
     int device = 0;
     genie_lsh_config cfg{};
     genie::DevBuf<double> a, b, inv;       // p-stable: a[m*dims], b[m]; RBH: pitch, shift, 1/pitch
+    genie::DevBuf<float> af, bf, invf;     // fp32 copies (GENIE_LSH_FP32)
     genie::DevBuf<unsigned long long> hash_seed, rehash_seed;
     // host-API staging, grown on demand and kept (no allocation per call)
     genie::DevBuf<float> ws_points;
@@ -92,6 +93,7 @@ static void check_cfg(const genie_lsh_config& c) {
     if (c.family == GENIE_LSH_RBH && !(c.sigma > 0.0))
         throw Error(GENIE_ERR_CONTRACT, "kernel width must be positive");
     if (c.family > GENIE_LSH_MINHASH) throw Error(GENIE_ERR_CONTRACT, "unknown LSH family");
+    if (c.precision > GENIE_LSH_FP32) throw Error(GENIE_ERR_CONTRACT, "unknown LSH precision");
 }
 
 // LshEncoder::create (lsh.hpp:151-166)
@@ -246,6 +248,115 @@ __global__ void __launch_bounds__(RB_PT * RB_FN)
     if (p < n && f < m) tokens[p * m + f] = static_cast<uint32_t>(st % domain);
 }
 
+// ------------------------------------------------- opt-in fp32 transforms
+// GENIE_LSH_FP32: the same hash functions evaluated in fp32 with FMA
+// contraction (p-stable: one FFMA per (point, function, dim); RBH: one
+// FFMA-style (p - u) * (1/g) per coordinate).  Not bit-exact: a token whose
+// fp64 bucket value lies within fp32 rounding of an integer boundary may land
+// in the neighbouring bucket.  SURVEY 8c measured 22 of 11.85M p-stable
+// tokens (1.9e-6) and 0 of 711K RBH tokens for this kind of arithmetic; the
+// tests count and bound the disagreements against the fp64 path.
+__global__ void __launch_bounds__(PS_THREADS)
+    k_pstable_f32(const float* __restrict__ pts, uint64_t n, uint32_t dims, uint32_t m, const float* __restrict__ a,
+                  const float* __restrict__ b, float w, uint32_t bucket_count, int64_t bucket_min, int rehash,
+                  const unsigned long long* __restrict__ rseed, uint32_t domain, uint32_t* __restrict__ tokens) {
+    __shared__ float sp[PS_DC][PS_PT + 1];
+    __shared__ float sa[PS_DC][PS_FN + 1];
+    const uint64_t p0 = uint64_t(blockIdx.x) * PS_PT;
+    const uint32_t f0 = blockIdx.y * PS_FN;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t f = f0 + tx + 16 * j;
+            acc[i][j] = f < m ? b[f] : 0.f;
+        }
+    for (uint32_t d0 = 0; d0 < dims; d0 += PS_DC) {
+        for (int i = threadIdx.x; i < PS_DC * PS_PT; i += PS_THREADS) {
+            const int pp = i / PS_DC, dd = i % PS_DC;
+            const uint64_t pt = p0 + pp;
+            const uint32_t d = d0 + dd;
+            sp[dd][pp] = (pt < n && d < dims) ? pts[pt * dims + d] : 0.f;
+        }
+        for (int i = threadIdx.x; i < PS_DC * PS_FN; i += PS_THREADS) {
+            const int ff = i / PS_DC, dd = i % PS_DC;
+            const uint32_t f = f0 + ff, d = d0 + dd;
+            sa[dd][ff] = (f < m && d < dims) ? a[size_t(f) * dims + d] : 0.f;
+        }
+        __syncthreads();
+        const int dn = (dims - d0) < uint32_t(PS_DC) ? int(dims - d0) : PS_DC;
+        for (int dd = 0; dd < dn; ++dd) {
+            float pv[4], av[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pv[i] = sp[dd][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) av[j] = sa[dd][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[j], pv[i], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint64_t pt = p0 + ty + 16 * i;
+        if (pt >= n) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t f = f0 + tx + 16 * j;
+            if (f >= m) continue;
+            const long long raw = static_cast<long long>(floorf(acc[i][j] / w));
+            uint32_t tok;
+            if (rehash) {
+                uint64_t st = mix64(rseed[f]);
+                st = mix64(st ^ static_cast<uint64_t>(raw));
+                tok = static_cast<uint32_t>(st % domain);
+            } else {
+                long long off = raw - bucket_min;
+                off = off < 0 ? 0 : off;
+                off = off > static_cast<long long>(bucket_count) - 1 ? static_cast<long long>(bucket_count) - 1 : off;
+                tok = static_cast<uint32_t>(off);
+            }
+            tokens[pt * m + f] = tok;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(RB_PT * RB_FN)
+    k_rbh_f32(const float* __restrict__ pts, uint64_t n, uint32_t dims, uint32_t m, const float* __restrict__ shift,
+              const float* __restrict__ inv, const unsigned long long* __restrict__ rseed, uint32_t domain,
+              uint32_t* __restrict__ tokens) {
+    __shared__ float sp[RB_PT][RB_DC + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t p = uint64_t(blockIdx.x) * RB_PT + lane;
+    const uint32_t f = blockIdx.y * RB_FN + warp;
+    uint64_t st = f < m ? mix64(rseed[f]) : 0;
+    const float* up = shift + size_t(f < m ? f : 0) * dims;
+    const float* ip = inv + size_t(f < m ? f : 0) * dims;
+    for (uint32_t d0 = 0; d0 < dims; d0 += RB_DC) {
+        for (int i = threadIdx.x; i < RB_PT * RB_DC; i += RB_PT * RB_FN) {
+            const int pp = i / RB_DC, dd = i % RB_DC;
+            const uint64_t pi = uint64_t(blockIdx.x) * RB_PT + pp;
+            const uint32_t d = d0 + dd;
+            sp[pp][dd] = (pi < n && d < dims) ? pts[pi * dims + d] : 0.f;
+        }
+        __syncthreads();
+        if (f < m) {
+            const int dn = (dims - d0) < uint32_t(RB_DC) ? int(dims - d0) : RB_DC;
+            for (int dd = 0; dd < dn; ++dd) {
+                const uint32_t d = d0 + dd;
+                const long long sig = static_cast<long long>(floorf((sp[lane][dd] - up[d]) * ip[d]));
+                st = mix64(st ^ static_cast<uint64_t>(sig));
+            }
+        }
+        __syncthreads();
+    }
+    if (p < n && f < m) tokens[p * m + f] = static_cast<uint32_t>(st % domain);
+}
+
 // ----------------------------------------------------------------- minHash
 
 // One warp per set; lanes stride over the functions.
@@ -335,6 +446,8 @@ genie_lsh_config genie_lsh_config_default(void) {
     c.rehash_pstable = 0;
     c.bucket_min = -33;
     c.sigma = 1.0;
+    c.precision = GENIE_LSH_FP64;
+    c.reserved = 0;
     return c;
 }
 
@@ -375,6 +488,15 @@ int genie_encoder_create(const genie_lsh_config* cfg, int device, genie_encoder*
             GENIE_CUDA(cudaMemcpy(enc->inv.p, inv.data(), ma * 8, cudaMemcpyHostToDevice));
             GENIE_CUDA(cudaMemcpy(enc->hash_seed.p, hs.data(), c.m * 8, cudaMemcpyHostToDevice));
             GENIE_CUDA(cudaMemcpy(enc->rehash_seed.p, rs.data(), c.m * 8, cudaMemcpyHostToDevice));
+            if (c.precision == GENIE_LSH_FP32 && c.family != GENIE_LSH_MINHASH) {
+                std::vector<float> af(a.begin(), a.end()), bf(b.begin(), b.end()), invf(inv.begin(), inv.end());
+                enc->af.reserve(ma);
+                enc->bf.reserve(mb);
+                enc->invf.reserve(ma);
+                GENIE_CUDA(cudaMemcpy(enc->af.p, af.data(), ma * 4, cudaMemcpyHostToDevice));
+                GENIE_CUDA(cudaMemcpy(enc->bf.p, bf.data(), mb * 4, cudaMemcpyHostToDevice));
+                GENIE_CUDA(cudaMemcpy(enc->invf.p, invf.data(), ma * 4, cudaMemcpyHostToDevice));
+            }
         } catch (...) {
             genie_encoder_destroy(enc);
             throw;
@@ -401,7 +523,17 @@ int genie_lsh_encode_device(genie_encoder* enc, const float* d_points, uint64_t 
         const genie_lsh_config& c = enc->cfg;
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : enc->stream;
         if (!n) return GENIE_OK;
-        if (c.family == GENIE_LSH_PSTABLE) {
+        const bool fp32 = c.precision == GENIE_LSH_FP32;
+        if (c.family == GENIE_LSH_PSTABLE && fp32) {
+            dim3 grid(static_cast<unsigned>((n + PS_PT - 1) / PS_PT), (c.m + PS_FN - 1) / PS_FN);
+            k_pstable_f32<<<grid, PS_THREADS, 0, s>>>(d_points, n, c.dims, c.m, enc->af.p, enc->bf.p, float(c.w),
+                                                      c.bucket_count, c.bucket_min, c.rehash_pstable,
+                                                      enc->rehash_seed.p, c.rehash_domain, d_tokens);
+        } else if (c.family == GENIE_LSH_RBH && fp32) {
+            dim3 grid(static_cast<unsigned>((n + RB_PT - 1) / RB_PT), (c.m + RB_FN - 1) / RB_FN);
+            k_rbh_f32<<<grid, RB_PT * RB_FN, 0, s>>>(d_points, n, c.dims, c.m, enc->bf.p, enc->invf.p,
+                                                     enc->rehash_seed.p, c.rehash_domain, d_tokens);
+        } else if (c.family == GENIE_LSH_PSTABLE) {
             dim3 grid(static_cast<unsigned>((n + PS_PT - 1) / PS_PT), (c.m + PS_FN - 1) / PS_FN);
             k_pstable<<<grid, PS_THREADS, 0, s>>>(d_points, n, c.dims, c.m, enc->a.p, enc->b.p, c.w,
                                                   c.bucket_count, c.bucket_min, c.rehash_pstable,

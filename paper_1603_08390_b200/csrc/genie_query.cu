@@ -268,10 +268,11 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
 
 // --------------------------------------------------------------- worklist
 
-// Tile-major order: all queries' tile 0, then tile 1, ...  Within a tile the
-// width classes follow each other and queries keep request order.  Items of
-// the same tile read the same slice of every hot list, so the hot slice of
-// the index stays L2-resident while the batch sweeps it.
+// Class-major, then tile-major order: the width classes follow each other
+// (one k_scan launch each); within a class all queries' tile 0, then tile 1,
+// ..., queries in request order.  Items of the same tile read the same slice
+// of every hot list, so the hot slice of the index stays L2-resident while
+// the batch sweeps it.
 __global__ void __launch_bounds__(256) k_worklist(BatchParams p) {
     // one warp per query, lanes over its tiles
     const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -287,12 +288,10 @@ __global__ void __launch_bounds__(256) k_worklist(BatchParams p) {
     }
     const uint32_t rank = p.q_rank[q];
     const uint32_t tbase = p.q_tile_base[q];
+    uint64_t cbase = 0;  // items of the lower width classes
+    for (uint32_t i = 0; i < c; ++i) cbase += cnt[i] * ntc[i];
     for (uint32_t t = lane; t < nt; t += 32) {
-        uint64_t item = rank;
-        for (int i = 0; i < 3; ++i) {
-            item += cnt[i] * (uint64_t(t) < ntc[i] ? uint64_t(t) : ntc[i]);
-            if (i < static_cast<int>(c) && ntc[i] > t) item += cnt[i];
-        }
+        const uint64_t item = cbase + uint64_t(t) * cnt[c] + rank;
         p.work_q[item] = q;
         p.work_t[item] = t;
         uint4* rec = reinterpret_cast<uint4*>(p.tile_rec + uint64_t(tbase + t) * kRecWords);
@@ -1586,6 +1585,14 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Bulk L2 prefetch (TMA unit) of the 16-byte-aligned cover of ids[0, n).
+__device__ __forceinline__ void prefetch_l2(const uint32_t* ids, uint32_t n) {
+    const uint64_t a = reinterpret_cast<uint64_t>(ids), e = a + uint64_t(n) * 4;
+    const uint64_t a16 = a & ~15ull, bytes = ((e + 15) & ~15ull) - a16;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a16), "r"(static_cast<uint32_t>(bytes))
+                 : "memory");
+}
+
 // Warp variant, first half: the raw words of spans [s0, s0 + nsb) of a
 // multi-tile item -- span start, its cut at tile t and t + 1, dense slot --
 // go straight from global memory into the stage buffer with asynchronous
@@ -1632,6 +1639,11 @@ __device__ __forceinline__ uint32_t stage_warp_finish(const BatchParams& p, cons
                 }
             }
             groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
+            // the slice streams into L2 while the current item is scanned, so
+            // this item's posting loads hit L2 instead of waiting on DRAM
+#if GENIE_SPAN_PREFETCH
+            if (len) prefetch_l2(p.postings + beg, len);
+#endif
         }
         __syncwarp();  // every lane has read its raw words before any result overwrites them
         const uint32_t incl = warp_inclusive_scan(groups);
@@ -1701,11 +1713,14 @@ __device__ __forceinline__ StageArgs stage_args(const BatchParams& p, const Quer
     return sa;
 }
 
-__device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint64_t total);
+struct WorkQueue {  // one width class's items [base, end) of the work list, claimed via st[ctr]
+    uint32_t base, end, ctr;
+};
+__device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, const WorkQueue& total);
 
 template <int W, bool IL>
 __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t b,
-                                uint32_t S, uint32_t nsb, uint32_t G, uint32_t ptot, uint64_t total) {
+                                uint32_t S, uint32_t nsb, uint32_t G, uint32_t ptot, const WorkQueue& total) {
     using L = Lay<W, IL>;
 #ifdef GENIE_PHASE_TIMERS
     const long long t_setup = clock64();
@@ -1863,9 +1878,9 @@ __device__ __forceinline__ uint32_t gate_start(const BatchParams& p, uint32_t q,
     return min(start, bound + 1);
 }
 
-__device__ __forceinline__ uint32_t fetch_item(const BatchParams& p, uint64_t total) {
-    const unsigned long long i = atomicAdd(&p.st[ST_WORK_CTR], 1ull);
-    return i < total ? static_cast<uint32_t>(i) : 0xffffffffu;
+__device__ __forceinline__ uint32_t fetch_item(const BatchParams& p, const WorkQueue& wq) {
+    const unsigned long long i = wq.base + atomicAdd(&p.st[wq.ctr], 1ull);
+    return i < wq.end ? static_cast<uint32_t>(i) : 0xffffffffu;
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -1881,7 +1896,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 // item (asynchronous copies), the lower tiles' records (gate start), the
 // (query, tile) of the claimed item and the next claim; then it finishes the
 // staging and starts the copy of the claimed item's plan.
-__device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, uint64_t total) {
+__device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, const WorkQueue& total) {
     const uint32_t lane = threadIdx.x & 31;
     ItemDesc* d = sm.desc + buf;
     const uint32_t item = sm.scal[SC_PF_ITEM];
@@ -1934,7 +1949,7 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
 }
 
 template <int W>
-__device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t b, uint64_t total) {
+__device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t b, const WorkQueue& total) {
 #ifdef GENIE_PHASE_TIMERS
     const long long t_begin = clock64();
 #endif
@@ -2026,13 +2041,25 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
     }
 }
 
+// One persistent kernel per counter width W (its own register allocation):
+// the CTAs drain the W class's slice of the work list (k_worklist orders the
+// list class-major), a launch per class.
+template <int W>
 __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     k_scan(BatchParams p, uint32_t tile_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
     (void)tile_bytes;
     const ScanSmem sm = carve(smem, p.ht_slots);
     if (p.st[ST_OVERFLOW]) return;
-    const uint64_t total = p.st[ST_TOTAL_WORK];
+    constexpr uint32_t c = W == 4 ? 0 : (W == 8 ? 1 : 2);
+    WorkQueue total{0, 0, kWorkCtr[c]};
+    for (uint32_t i = 0; i <= c; ++i) {
+        const uint32_t items = static_cast<uint32_t>(p.st[ST_CLASS0 + i]) *
+                               (p.n ? ntiles_for(p.n, p.tile_bits_w[i], 4u << i) : 0u);
+        total.base = total.end;
+        total.end += items;
+    }
+    if (total.base == total.end) return;
     // item i runs from desc[i & 1]; its scan phase prepares item i + 1 into
     // the other descriptor / stage buffer (prepare_item).  Prime the pipeline:
     // the first item resolved with its plan in shared memory, the second claimed.
@@ -2069,11 +2096,7 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     for (uint32_t iter = 0;; ++iter) {
         const uint32_t b = iter & 1u;
         if (!sm.desc[b].valid) break;
-        switch (sm.desc[b].W) {
-            case 4: process_item<4>(p, sm, b, total); break;
-            case 8: process_item<8>(p, sm, b, total); break;
-            default: process_item<16>(p, sm, b, total); break;
-        }
+        process_item<W>(p, sm, b, total);
     }
 }
 
@@ -2731,7 +2754,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.out_thr = d_out_thr;
 
     if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[0], s));
-    k_init_status<<<1, 32, 0, s>>>(w.status.p);
+    k_init_status<<<1, 64, 0, s>>>(w.status.p);
     ++launches;
     if (Q) {
         k_resolve<<<(Q * 32 + kLookupThreads - 1) / kLookupThreads, kLookupThreads, 0, s>>>(p);
@@ -2748,18 +2771,22 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         // (one host thread may drive several devices, genie_group_*)
         DeviceAttrCache& ac = attr_cache(ix->device);
         if (ac.scan_smem < smem) {
-            GENIE_CUDA(cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(smem)));
+            GENIE_CUDA(cudaFuncSetAttribute(k_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            GENIE_CUDA(cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            GENIE_CUDA(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             ac.scan_smem = smem;
         }
         uint32_t per_sm = cfg.ctas_per_sm ? cfg.ctas_per_sm : 0;
         if (!per_sm) {
             int occ = 0;
-            GENIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan, kScanThreads, smem));
+            GENIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<8>, kScanThreads, smem));
             per_sm = std::max(1, occ);
         }
-        k_scan<<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
-        ++launches;
+        // one launch per width class (an empty class's CTAs exit at once)
+        k_scan<4><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+        k_scan<8><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+        k_scan<16><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+        launches += 3;
         if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
         const MergeSrc m = tile_merge_src(ix, Q, d_k, out_stride, d_out, d_out_len, d_out_thr, id_offset);
         const size_t msmem = kSortCap * sizeof(uint64_t);
@@ -2870,7 +2897,7 @@ void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entr
     m.out = d_out;
     m.out_len = d_out_len;
     m.out_thr = d_out_thr;
-    k_init_status<<<1, 32, 0, s>>>(w.status.p);
+    k_init_status<<<1, 64, 0, s>>>(w.status.p);
     const size_t msmem = kSortCap * sizeof(uint64_t);
     DeviceAttrCache& ac = attr_cache(ix->device);
     if (!ac.list_merge_set) {

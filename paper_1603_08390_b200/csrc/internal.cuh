@@ -64,6 +64,9 @@ constexpr uint32_t kLvl = GENIE_DENSE_LEVELS;  // dense-phase c-PQ levels counte
 // compact posting scan when the staged slices fill their 128-posting groups
 // less than 1/kCompactFillInv on average
 constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
+#ifndef GENIE_SPAN_PREFETCH  // L2 bulk prefetch of the next item's posting slices (prepare_item)
+#define GENIE_SPAN_PREFETCH 1
+#endif
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
 #endif
@@ -109,8 +112,11 @@ enum StatusWord : int {
     ST_DENSE_ND = 17,   // instrumented: sum of dense lists per dense item | bit-sliced items << 40
     ST_T_WMAX = 18,     // instrumented: sum over items of the slowest / fastest scan warp (cycles)
     ST_T_WMIN = 19,
-    ST_WORDS = 32
+    ST_WORK_CTR1 = 32,  // scan queue cursors of the W = 8 / W = 16 classes (ST_WORK_CTR: W = 4)
+    ST_WORK_CTR2 = 33,
+    ST_WORDS = 40
 };
+constexpr uint32_t kWorkCtr[3] = {ST_WORK_CTR, ST_WORK_CTR1, ST_WORK_CTR2};
 
 // Per-batch device scratch, grown on demand (never shrinks).
 struct Workspace {

@@ -523,12 +523,14 @@ class SeqSet:
 
 def lsh_config(family: int = RBH, m: int = 237, dims: int = 0, seed: int = 1, rehash_domain: int = 8192,
                w: float = 4.0, bucket_count: int = 67, bucket_min: int = -33, rehash_pstable: bool = False,
-               sigma: float = 1.0) -> N.LshConfig:
-    """LshEncoderConfig (lsh.hpp:132-145) defaults."""
+               sigma: float = 1.0, fp32: bool = False) -> N.LshConfig:
+    """LshEncoderConfig (lsh.hpp:132-145) defaults; fp32=True selects the
+    opt-in fast transforms (not bit-exact, see genie.h)."""
     c = N.LshConfig()
     c.family, c.m, c.dims, c.seed = family, m, dims, seed
     c.rehash_domain, c.w, c.bucket_count, c.bucket_min = rehash_domain, w, bucket_count, bucket_min
     c.rehash_pstable, c.sigma = int(rehash_pstable), sigma
+    c.precision = 1 if fp32 else 0
     return c
 
 
