@@ -69,6 +69,7 @@ def parse():
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--span-chunk", type=int, default=None, help="postings per warp work unit (result-invariant)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the kernels one by one (no CUDA graph)")
     ap.add_argument("--ref-sample", type=int, default=0, help="queries per reference step (0: auto)")
     return ap.parse_args()
 
@@ -520,8 +521,9 @@ def main_genie(args):
 
     w = Workload(args, rank, world, dev, local)
     ix, d, Q, stride = w.ix, w.d, w.Q, w.stride
+    # the device-resident step replays the batch pipeline as one CUDA graph
     cfg = config(selector=args.selector, tile_bytes=args.tile_bytes, ctas_per_sm=args.ctas_per_sm,
-                 span_chunk=args.span_chunk, stage_events=True)
+                 span_chunk=args.span_chunk, stage_events=True, graph=not args.no_graph)
     if world > 1:
         gath = torch.zeros((world, Q, stride, 2), dtype=torch.int32, device=dev)
         gath_len = torch.zeros((world, Q), dtype=torch.int32, device=dev)

@@ -73,6 +73,11 @@ typedef struct {
 /* genie_config.flags: record CUDA events around the device stages on the
  * launching stream (read back with genie_last_stage_ns after synchronising). */
 #define GENIE_FLAG_STAGE_EVENTS 1u
+/* genie_config.flags: genie_query_batch_device replays the batch pipeline as
+ * one CUDA graph, captured on first use and re-captured whenever the batch
+ * shape, buffers, stream or workspace change (ignored for the legacy default
+ * stream and for k > 8192). */
+#define GENIE_FLAG_GRAPH 2u
 
 /* mcx::StageTimings (engine.hpp:44-50), measured with CUDA events on the
  * handle's stream (device stages) and the host clock (total). */
@@ -221,6 +226,8 @@ int genie_debug_status(genie_index* ix, uint64_t* words, uint32_t n_words, char*
 
 /* Kernels launched by the last batch (for launch accounting). */
 uint32_t genie_last_launch_count(const genie_index* ix);
+/* CUDA graphs captured for this index so far (GENIE_FLAG_GRAPH). */
+uint64_t genie_graph_captures(const genie_index* ix);
 
 /* Device stage times of the last batch launched with GENIE_FLAG_STAGE_EVENTS
  * (or through genie_query_batch with timings): lookup = resolve + plan + cut,

@@ -30,6 +30,7 @@ GENIE_ERR_CUDA = 4
 GENIE_ERR_NCCL = 5
 GENIE_RETRY = 6
 GENIE_FLAG_STAGE_EVENTS = 1
+GENIE_FLAG_GRAPH = 2
 
 
 class Entry(C.Structure):
@@ -98,6 +99,7 @@ ENGINE_SYMBOLS = {
                                            C.c_size_t]),
     "genie_query_status": (C.c_int, [vp, C.POINTER(BatchStats), C.c_char_p, C.c_size_t]),
     "genie_last_launch_count": (C.c_uint32, [vp]),
+    "genie_graph_captures": (C.c_uint64, [vp]),
     "genie_last_stage_ns": (C.c_int, [vp, C.POINTER(StageNs), C.c_char_p, C.c_size_t]),
     "genie_debug_status": (C.c_int, [vp, u64p, C.c_uint32, C.c_char_p, C.c_size_t]),
     "genie_merge_topk_device": (C.c_int, [vp, C.c_uint32, C.c_uint32, vp, vp, C.c_uint32, vp, C.c_uint32,

@@ -143,6 +143,8 @@ int genie_query_status(genie_index* ix, genie_batch_stats* stats, char* err, siz
 
 uint32_t genie_last_launch_count(const genie_index* ix) { return ix ? ix->last_launches : 0; }
 
+uint64_t genie_graph_captures(const genie_index* ix) { return ix ? graph_captures(ix) : 0; }
+
 int genie_debug_status(genie_index* ix, uint64_t* words, uint32_t n_words, char* err, size_t errlen) {
     return guarded(err, errlen, [&]() -> int {
         if (!ix || !ix->ws.h_status) throw Error(GENIE_ERR_CONTRACT, "no batch has run on this index");

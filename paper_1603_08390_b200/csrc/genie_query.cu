@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <vector>
 
 #include "block.cuh"
@@ -2447,6 +2448,37 @@ __global__ void k_keys_to_rows(genie_entry* out, const uint32_t* out_len, uint32
     }
 }
 
+// ------------------------------------------------------------ CUDA graphs
+
+// What a captured batch depends on: replayed only while all of it is equal.
+struct GraphKey {
+    BatchParams p;
+    MergeSrc m;
+    cudaStream_t s;
+    uint32_t Q, tile_bytes, per_sm;
+    size_t smem;
+    bool timed;
+};
+
+struct GraphCache {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    uint32_t launches = 0;
+    uint64_t captures = 0;
+    ~GraphCache() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
+static GraphCache& graph_cache(genie_index* ix) {
+    if (!ix->graph) ix->graph = std::shared_ptr<void>(new GraphCache(), [](void* g) { delete static_cast<GraphCache*>(g); });
+    return *static_cast<GraphCache*>(ix->graph.get());
+}
+
+uint64_t graph_captures(const genie_index* ix) {
+    return ix->graph ? static_cast<const GraphCache*>(ix->graph.get())->captures : 0;
+}
+
 // ------------------------------------------------------------ orchestration
 
 int sm_count(int device) {
@@ -2462,6 +2494,8 @@ void ensure_device(int device) { GENIE_CUDA(cudaSetDevice(device)); }
 // contract; distinct handles on one device set the same values.
 struct DeviceAttrCache {
     size_t scan_smem = 0;
+    int scan_occ = 0;             // resident k_scan CTAs per SM at scan_occ_smem bytes
+    size_t scan_occ_smem = 0;
     bool merge_set = false;       // k_merge (batch) and k_merge_big
     bool list_merge_set = false;  // k_merge (list merge) and k_merge_big
 };
@@ -2753,70 +2787,128 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.out_len = d_out_len;
     p.out_thr = d_out_thr;
 
-    if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[0], s));
-    k_init_status<<<1, 64, 0, s>>>(w.status.p);
-    ++launches;
-    if (Q) {
-        k_resolve<<<(Q * 32 + kLookupThreads - 1) / kLookupThreads, kLookupThreads, 0, s>>>(p);
-        k_plan<<<1, 1024, 0, s>>>(p);
-        k_worklist<<<(Q * 32 + 255) / 256, 256, 0, s>>>(p);
-        launches += 3;
-        const int sms = ix->sms;
-        k_cut<<<sms * kCutCtasPerSm, kLookupThreads, 0, s>>>(p);
-        ++launches;
-        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
-        p.ht_slots = kHtSlots;
-        const size_t smem = scan_smem_bytes(tile_bytes, p.ht_slots);
-        // cudaFuncSetAttribute applies per device context: cached per device
-        // (one host thread may drive several devices, genie_group_*)
-        DeviceAttrCache& ac = attr_cache(ix->device);
-        if (ac.scan_smem < smem) {
-            GENIE_CUDA(cudaFuncSetAttribute(k_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            GENIE_CUDA(cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            GENIE_CUDA(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            ac.scan_smem = smem;
-        }
-        uint32_t per_sm = cfg.ctas_per_sm ? cfg.ctas_per_sm : 0;
-        if (!per_sm) {
+    // host-side set-up first (launch attributes, occupancy): the enqueue
+    // below issues stream work only, so it can be captured into a graph
+    const int sms = ix->sms;
+    p.ht_slots = kHtSlots;
+    const size_t smem = scan_smem_bytes(tile_bytes, p.ht_slots);
+    const size_t msmem = kSortCap * sizeof(uint64_t);
+    // cudaFuncSetAttribute applies per device context: cached per device
+    // (one host thread may drive several devices, genie_group_*)
+    DeviceAttrCache& ac = attr_cache(ix->device);
+    if (ac.scan_smem < smem) {
+        GENIE_CUDA(cudaFuncSetAttribute(k_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        GENIE_CUDA(cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        GENIE_CUDA(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        ac.scan_smem = smem;
+    }
+    if (!ac.merge_set) {
+        GENIE_CUDA(cudaFuncSetAttribute(k_merge<kMergeSmallThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kMergeSmallCap * sizeof(uint64_t))));
+        GENIE_CUDA(cudaFuncSetAttribute(k_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(msmem)));
+        ac.merge_set = true;
+    }
+    uint32_t per_sm = cfg.ctas_per_sm ? cfg.ctas_per_sm : 0;
+    if (!per_sm) {
+        if (!ac.scan_occ || ac.scan_occ_smem != smem) {
             int occ = 0;
             GENIE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<8>, kScanThreads, smem));
-            per_sm = std::max(1, occ);
+            ac.scan_occ = std::max(1, occ);
+            ac.scan_occ_smem = smem;
         }
-        // one launch per width class (an empty class's CTAs exit at once)
-        k_scan<4><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
-        k_scan<8><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
-        k_scan<16><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
-        launches += 3;
-        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
-        const MergeSrc m = tile_merge_src(ix, Q, d_k, out_stride, d_out, d_out_len, d_out_thr, id_offset);
-        const size_t msmem = kSortCap * sizeof(uint64_t);
-        if (!ac.merge_set) {
-            GENIE_CUDA(cudaFuncSetAttribute(k_merge<kMergeSmallThreads>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(kMergeSmallCap * sizeof(uint64_t))));
-            GENIE_CUDA(cudaFuncSetAttribute(k_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(msmem)));
-            ac.merge_set = true;
-        }
-        const uint32_t mgrid = std::min<uint32_t>(Q, sms * 4);
-        // one small CTA per query: after the floors prune them, unions are a
-        // few k entries, so all queries merge concurrently; larger unions are
-        // left to k_merge_big
-        k_merge<kMergeSmallThreads><<<Q, kMergeSmallThreads, kMergeSmallCap * sizeof(uint64_t), s>>>(m, kMergeSmallCap);
-        k_merge_big<<<mgrid, kMergeThreads, msmem, s>>>(m);
-        launches += 2;
-        if (max_k > kSortCap) {
-            segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, id_offset, s);
-            launches += 3;
-        }
-        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
-    } else if (timed) {
-        GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
-        GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
-        GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
+        per_sm = ac.scan_occ;
     }
-    GENIE_CUDA(cudaMemcpyAsync(w.h_status, w.status.p, ST_WORDS * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, s));
+    const MergeSrc m = tile_merge_src(ix, Q, d_k, out_stride, d_out, d_out_len, d_out_thr, id_offset);
+    const bool big_rows = max_k > kSortCap;  // CUB segmented sort (allocates): never captured
+
+    auto enqueue = [&]() {
+        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[0], s));
+        k_init_status<<<1, 64, 0, s>>>(w.status.p);
+        ++launches;
+        if (Q) {
+            k_resolve<<<(Q * 32 + kLookupThreads - 1) / kLookupThreads, kLookupThreads, 0, s>>>(p);
+            k_plan<<<1, 1024, 0, s>>>(p);
+            k_worklist<<<(Q * 32 + 255) / 256, 256, 0, s>>>(p);
+            k_cut<<<sms * kCutCtasPerSm, kLookupThreads, 0, s>>>(p);
+            launches += 4;
+            if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
+            // one launch per width class (an empty class's CTAs exit at once)
+            k_scan<4><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+            k_scan<8><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+            k_scan<16><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+            launches += 3;
+            if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
+            // one small CTA per query: after the floors prune them, unions are a
+            // few k entries, so all queries merge concurrently; larger unions
+            // are left to k_merge_big
+            k_merge<kMergeSmallThreads><<<Q, kMergeSmallThreads, kMergeSmallCap * sizeof(uint64_t), s>>>(
+                m, kMergeSmallCap);
+            k_merge_big<<<std::min<uint32_t>(Q, sms * 4), kMergeThreads, msmem, s>>>(m);
+            launches += 2;
+            if (big_rows) {
+                segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, id_offset, s);
+                launches += 3;
+            }
+            if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
+        } else if (timed) {
+            GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
+            GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
+            GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
+        }
+        GENIE_CUDA(cudaMemcpyAsync(w.h_status, w.status.p, ST_WORDS * sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, s));
+    };
+
+    const bool graph = (cfg.flags & GENIE_FLAG_GRAPH) && !big_rows && s != nullptr &&
+                       s != cudaStreamLegacy && s != cudaStreamPerThread;
+    if (!graph) {
+        enqueue();
+    } else {
+        // CUDA graph per batch shape: the whole pipeline (11 launches, events,
+        // status read-back) replays with one cudaGraphLaunch while nothing it
+        // captured -- parameters, workspace, buffers, stream -- has changed
+        GraphKey key;
+        std::memset(&key, 0, sizeof(key));
+        key.p = p;
+        key.m = m;
+        key.s = s;
+        key.Q = Q;
+        key.tile_bytes = tile_bytes;
+        key.per_sm = per_sm;
+        key.smem = smem;
+        key.timed = timed;
+        GraphCache& gc = graph_cache(ix);
+        if (!gc.exec || std::memcmp(&gc.key, &key, sizeof(key)) != 0) {
+            cudaGraph_t g = nullptr;
+            GENIE_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue();
+            } catch (...) {
+                cudaStreamEndCapture(s, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            GENIE_CUDA(cudaStreamEndCapture(s, &g));
+            bool updated = false;
+            if (gc.exec) {
+                cudaGraphExecUpdateResultInfo info{};
+                updated = cudaGraphExecUpdate(gc.exec, g, &info) == cudaSuccess;
+                if (!updated) {
+                    cudaGetLastError();
+                    cudaGraphExecDestroy(gc.exec);
+                    gc.exec = nullptr;
+                }
+            }
+            if (!updated) GENIE_CUDA(cudaGraphInstantiate(&gc.exec, g, 0));
+            cudaGraphDestroy(g);
+            gc.key = key;
+            gc.launches = launches;
+            ++gc.captures;
+        }
+        launches = gc.launches;
+        GENIE_CUDA(cudaGraphLaunch(gc.exec, s));
+    }
     GENIE_CUDA(cudaGetLastError());
     ix->last_launches = launches;
 }

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <memory>
 
 #include "common.cuh"
 
@@ -176,6 +177,7 @@ struct genie_index {
     uint32_t last_launches = 0;
     bool last_timed = false;
     genie_config last_cfg{};
+    std::shared_ptr<void> graph;  // captured batch pipeline (GENIE_FLAG_GRAPH), genie_query.cu
 };
 
 namespace genie {
@@ -201,6 +203,9 @@ int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
                  const uint32_t* h_qid /* optional, for messages */);
 
 void ensure_device(int device);
+
+// CUDA-graph captures made for this index (GENIE_FLAG_GRAPH batches).
+uint64_t graph_captures(const genie_index* ix);
 
 // ---- host-side helpers shared by the C-ABI translation units
 

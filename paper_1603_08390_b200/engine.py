@@ -166,9 +166,9 @@ class Results:
 
 
 def config(selector: int = 0, span_chunk: Optional[int] = None, max_spans_per_task: int = 2,
-           tile_bytes: int = 0, ctas_per_sm: int = 0, stage_events: bool = False) -> N.Config:
+           tile_bytes: int = 0, ctas_per_sm: int = 0, stage_events: bool = False, graph: bool = False) -> N.Config:
     c = N.engine().genie_config_default()
-    c.flags = N.GENIE_FLAG_STAGE_EVENTS if stage_events else 0
+    c.flags = (N.GENIE_FLAG_STAGE_EVENTS if stage_events else 0) | (N.GENIE_FLAG_GRAPH if graph else 0)
     c.selector = selector
     if span_chunk is not None:
         c.span_chunk = span_chunk
@@ -359,6 +359,9 @@ class DeviceIndex:
             ptr(d["out"]), ptr(d["out_len"]), ptr(d["out_thr"]), _torch_stream(stream), err, len(err))
         check(rc, err)
         return int(self._lib.genie_last_launch_count(self._h))
+
+    def graph_captures(self) -> int:
+        return int(self._lib.genie_graph_captures(self._h))
 
     def status(self) -> dict:
         """Synchronise and surface the last device batch's status; raises on

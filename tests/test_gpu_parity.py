@@ -387,3 +387,64 @@ def test_device_build_equals_host_build(gpu, oracle, seed):
     dup_dims[a + 1], dup_toks[a + 1] = dup_dims[a], dup_toks[a]
     with pytest.raises(ContractError, match="duplicate keyword"):
         DeviceIndex.build(n, off, dup_dims, dup_toks, device=gpu)
+
+
+def test_cuda_graph_replay_equals_direct_launches(gpu):
+    """GENIE_FLAG_GRAPH: the batch pipeline captured once and replayed while
+    nothing it depends on changes; new buffers / a grown workspace re-capture.
+    Every replay's results equal the host API's."""
+    import torch
+
+    from paper_1603_08390_b200 import config
+
+    dev = torch.device("cuda", gpu)
+    s = torch.cuda.Stream(dev)
+
+    def dev_batch(qb):
+        with torch.cuda.stream(s):
+            return {"qid": torch.from_numpy(qb.qid.astype(np.int32)).to(dev),
+                    "k": torch.from_numpy(qb.k.astype(np.int32)).to(dev),
+                    "item_off": torch.from_numpy(qb.item_off.astype(np.int64)).to(dev),
+                    "dim": torch.from_numpy(qb.dim.astype(np.int16)).to(dev),
+                    "lo": torch.from_numpy(qb.lo.astype(np.int32)).to(dev),
+                    "hi": torch.from_numpy(qb.hi.astype(np.int32)).to(dev),
+                    "out": torch.zeros((len(qb), 100, 2), dtype=torch.int32, device=dev),
+                    "out_len": torch.zeros(len(qb), dtype=torch.int32, device=dev),
+                    "out_thr": torch.zeros(len(qb), dtype=torch.int32, device=dev),
+                    "max_k": 100, "total_items": qb.num_items, "stride": 100}
+
+    def check(d, host):
+        s.synchronize()
+        out = d["out"].cpu().numpy().view(np.uint32)
+        assert np.array_equal(d["out_len"].cpu().numpy(), host.length.astype(np.int32))
+        assert np.array_equal(d["out_thr"].cpu().numpy(), host.threshold.astype(np.int32))
+        for q in range(host.length.shape[0]):
+            n = int(host.length[q])
+            assert np.array_equal(out[q, :n, 0], host.ids[q, :n]) and np.array_equal(out[q, :n, 1], host.counts[q, :n])
+
+    ds = synth.tweets(n=400_000, vocab=40_000, words=10, queries=128, k=100)
+    ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+    host = ix.query(ds.queries)
+    cfg = config(graph=True)
+    d = dev_batch(ds.queries)
+    for _ in range(4):  # first call may grow the workspace (retry), then the graph settles
+        ix.query_device(d, cfg, stream=s.cuda_stream)
+        if not ix.status().get("retry"):
+            break
+    settled = ix.graph_captures()
+    for _ in range(5):
+        d["out"].zero_()
+        ix.query_device(d, cfg, stream=s.cuda_stream)
+        assert not ix.status().get("retry")
+        check(d, host)
+    assert ix.graph_captures() == settled  # pure replays
+    # a different batch (new buffers): re-captured, still exact
+    ds2 = synth.tweets(n=400_000, vocab=40_000, words=10, queries=96, k=100, seed=99)
+    host2 = DeviceIndex.from_csr(ds.csr, device=gpu).query(ds2.queries)
+    d2 = dev_batch(ds2.queries)
+    for _ in range(4):
+        ix.query_device(d2, cfg, stream=s.cuda_stream)
+        if not ix.status().get("retry"):
+            break
+    check(d2, host2)
+    assert ix.graph_captures() > settled
