@@ -211,6 +211,7 @@ class Workload:
         Q = args.queries or QUERIES[self.name]
         t0 = time.perf_counter()
         self.qpoints = self.qsets = None
+        self.encode_index = None
         if self.name in ("tweets", "adult"):
             ds = (synth.tweets(n=args.n or 7_000_000, vocab=1_000_000, words=10, queries=Q, k=100)
                   if self.name == "tweets" else synth.adult(n=args.n or 48842, queries=Q, k=100))
@@ -250,17 +251,24 @@ class Workload:
             lo, hi = n_all * rank // world, n_all * (rank + 1) // world
             self.n = n_all
             tok = torch.zeros((hi - lo, self.m), dtype=torch.int32, device=dev)
-            if self.name == "minhash":
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if self.name != "minhash":
+                d_pts = torch.from_numpy(ds.points[lo:hi]).to(dev)
+            else:
                 off = ds.set_off[lo:hi + 1]
                 d_off = torch.from_numpy((off - off[0]).astype(np.int64)).to(dev)
                 d_el = torch.from_numpy(ds.elems[off[0]:off[-1]].view(np.int64)).to(dev)
+            torch.cuda.synchronize(dev)
+            ev0.record()  # the index-side transform alone (inputs resident)
+            if self.name == "minhash":
                 self.lsh.encode_sets_device(d_off, d_el, tok)
                 del d_off, d_el
             else:
-                d_pts = torch.from_numpy(ds.points[lo:hi]).to(dev)
                 self.lsh.encode_device(d_pts, tok)
                 del d_pts
+            ev1.record()
             torch.cuda.synchronize(dev)
+            self.encode_index = {"points": hi - lo, "ms": round(ev0.elapsed_time(ev1), 3)}
             self.ix = DeviceIndex.from_tokens_device(tok.data_ptr(), hi - lo, self.m, domain, device=local,
                                                      id_offset=lo)
             del tok
@@ -498,6 +506,27 @@ def scan_roofline(workload, world, postings, scan_ms, clocks, sms):
     return out
 
 
+def encode_roofline(workload, w):
+    """The index-side LSH / minHash transform, timed on its own (CUDA events,
+    inputs resident): SURVEY 8d bounds it by FP64 issue (p-stable: one DMUL +
+    one DADD per (point, function, dim); RBH: DSUB + DMUL per coordinate, plus
+    an exact DDIV near bucket boundaries and a mix64 fold) against the B200
+    FP64 peak the Blackwell guide states (45 TFLOP/s).  minHash is INT64 only
+    (one mix64 per (element, function)): reported as hashes/s."""
+    e = dict(w.encode_index)
+    n, m, dims = e["points"], w.m, (w.ds.points.shape[1] if w.ds.points is not None else 0)
+    s = e["ms"] / 1e3
+    if workload in ("sift", "ocr"):
+        flops = 2.0 * n * m * dims
+        e.update({"fp64_gflop": round(flops / 1e9, 1), "fp64_tflops": round(flops / s / 1e12, 2),
+                  "fp64_peak_tflops": 45.0, "peak_source": "blackwell_cuda_programming.md (B200 FP64)",
+                  "frac": round(flops / s / 45e12, 3), "points_per_s": round(n / s, 1)})
+    else:
+        elems = int(w.ds.set_off[-1]) if w.ds.set_off is not None else 0
+        e.update({"mix64_hashes": elems * m, "ghash_per_s": round(elems * m / s / 1e9, 2), "sets_per_s": round(n / s, 1)})
+    return e
+
+
 # ------------------------------------------------------------------- genie
 
 def main_genie(args):
@@ -682,6 +711,8 @@ def main_genie(args):
         }
         if getattr(w, "sigma", None):
             line["config"]["sigma"] = round(w.sigma, 6)
+        if w.encode_index:
+            line["encode"] = encode_roofline(args.workload, w)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -876,7 +876,7 @@ __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32
 // the gate on it also counts, in registers, the objects reaching each level
 // v in [at0, at0 + kLvl) (Swar::ge + popc), for the c-PQ catch-up below.
 template <int W>
-__device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb,
+GENIE_DENSE_FN uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb,
                                uint32_t nd, uint32_t at0, uint32_t nlv, bool& csa_path, long long* t_work = nullptr) {
     using Sw = Swar<W>;
     constexpr uint32_t BPT = W == 4 ? 4 : (W == 8 ? 2 : 1);  // blocks per thread step (16 words)
@@ -1255,7 +1255,7 @@ __device__ uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const Sc
 // again); every object at or above the new AT -- fewer than k -- enters the
 // table and adds one to ZA[v] for each level v in [AT, count].
 template <int W>
-__device__ void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, uint32_t dmax, uint32_t nlv,
+GENIE_DENSE_FN void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t at0, uint32_t dmax, uint32_t nlv,
                            uint32_t reach, bool csa_path) {
     using Sw = Swar<W>;
     using L = Lay<W, true>;

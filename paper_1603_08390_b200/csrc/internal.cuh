@@ -65,8 +65,16 @@ constexpr uint32_t kLvl = GENIE_DENSE_LEVELS;  // dense-phase c-PQ levels counte
 // compact posting scan when the staged slices fill their 128-posting groups
 // less than 1/kCompactFillInv on average
 constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
+#ifndef GENIE_DENSE_NOINLINE  // dense phase as out-of-line calls (own register allocation)
+#define GENIE_DENSE_NOINLINE 0
+#endif
+#if GENIE_DENSE_NOINLINE
+#define GENIE_DENSE_FN __device__ __noinline__
+#else
+#define GENIE_DENSE_FN __device__
+#endif
 #ifndef GENIE_SPAN_PREFETCH  // L2 bulk prefetch of the next item's posting slices (prepare_item)
-#define GENIE_SPAN_PREFETCH 1
+#define GENIE_SPAN_PREFETCH 0
 #endif
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
