@@ -1906,8 +1906,14 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
         return;
     }
     const uint32_t q = sm.scal[SC_PF_Q], t = sm.scal[SC_PF_T], claim = sm.scal[SC_CLAIM];
+#ifdef GENIE_PHASE_TIMERS
+    const long long pt0 = clock64();
+#endif
     cp_async_wait_all();  // q's plan (previous call)
     __syncwarp();
+#ifdef GENIE_PHASE_TIMERS
+    const long long pt1 = clock64();
+#endif
     const QueryPlan pl = *sm.plan;
     uint32_t S;
     const StageArgs sa = stage_args(p, pl, S);
@@ -1920,8 +1926,23 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     }
     if (lane == 0 && claim != 0xffffffffu) nclaim = fetch_item(p, total);
     const bool gate = (p.selector == GENIE_SELECT_CPQ) && pl.W <= 8;
+#ifdef GENIE_PHASE_TIMERS
+    const long long pt2 = clock64();
+#endif
     const uint32_t a0 = gate ? gate_start(p, q, t, pl.k, pl.bound, pl.tile_base) : 0u;
+#ifdef GENIE_PHASE_TIMERS
+    const long long pt3 = clock64();
+#endif
     const uint32_t G = stage_warp_finish(p, sa, sm.sb(buf), t, 0, nsb);
+#ifdef GENIE_PHASE_TIMERS
+    const long long pt4 = clock64();
+    if (lane == 0) {  // prepare split: plan wait / issue / gate start / staging finish
+        atomicAdd(&p.st[ST_P_WAIT], static_cast<unsigned long long>(pt1 - pt0));
+        atomicAdd(&p.st[ST_P_ISSUE], static_cast<unsigned long long>(pt2 - pt1));
+        atomicAdd(&p.st[ST_P_GATE], static_cast<unsigned long long>(pt3 - pt2));
+        atomicAdd(&p.st[ST_P_STAGE], static_cast<unsigned long long>(pt4 - pt3));
+    }
+#endif
     if (claim != 0xffffffffu && lane < sizeof(QueryPlan) / 16)
         cp_async16(reinterpret_cast<uint4*>(sm.plan) + lane, reinterpret_cast<const uint4*>(p.plan + nq) + lane);
     nclaim = __shfl_sync(0xffffffffu, nclaim, 0);
@@ -2822,8 +2843,14 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     const MergeSrc m = tile_merge_src(ix, Q, d_k, out_stride, d_out, d_out_len, d_out_thr, id_offset);
     const bool big_rows = max_k > kSortCap;  // CUB segmented sort (allocates): never captured
 
-    auto enqueue = [&]() {
-        if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[0], s));
+    // stage events are recorded as external event nodes when captured, so a
+    // replayed graph still records them (cudaEventRecordExternal)
+    auto enqueue = [&](bool capturing) {
+        auto record = [&](int e) {
+            GENIE_CUDA(capturing ? cudaEventRecordWithFlags(ix->ev[e], s, cudaEventRecordExternal)
+                                 : cudaEventRecord(ix->ev[e], s));
+        };
+        if (timed) record(0);
         k_init_status<<<1, 64, 0, s>>>(w.status.p);
         ++launches;
         if (Q) {
@@ -2832,13 +2859,13 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
             k_worklist<<<(Q * 32 + 255) / 256, 256, 0, s>>>(p);
             k_cut<<<sms * kCutCtasPerSm, kLookupThreads, 0, s>>>(p);
             launches += 4;
-            if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
+            if (timed) record(1);
             // one launch per width class (an empty class's CTAs exit at once)
             k_scan<4><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             k_scan<8><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             k_scan<16><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             launches += 3;
-            if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
+            if (timed) record(2);
             // one small CTA per query: after the floors prune them, unions are a
             // few k entries, so all queries merge concurrently; larger unions
             // are left to k_merge_big
@@ -2850,11 +2877,11 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
                 segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, id_offset, s);
                 launches += 3;
             }
-            if (timed) GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
+            if (timed) record(3);
         } else if (timed) {
-            GENIE_CUDA(cudaEventRecord(ix->ev[1], s));
-            GENIE_CUDA(cudaEventRecord(ix->ev[2], s));
-            GENIE_CUDA(cudaEventRecord(ix->ev[3], s));
+            record(1);
+            record(2);
+            record(3);
         }
         GENIE_CUDA(cudaMemcpyAsync(w.h_status, w.status.p, ST_WORDS * sizeof(unsigned long long),
                                    cudaMemcpyDeviceToHost, s));
@@ -2863,7 +2890,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     const bool graph = (cfg.flags & GENIE_FLAG_GRAPH) && !big_rows && s != nullptr &&
                        s != cudaStreamLegacy && s != cudaStreamPerThread;
     if (!graph) {
-        enqueue();
+        enqueue(false);
     } else {
         // CUDA graph per batch shape: the whole pipeline (11 launches, events,
         // status read-back) replays with one cudaGraphLaunch while nothing it
@@ -2883,7 +2910,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
             cudaGraph_t g = nullptr;
             GENIE_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             try {
-                enqueue();
+                enqueue(true);
             } catch (...) {
                 cudaStreamEndCapture(s, &g);
                 if (g) cudaGraphDestroy(g);

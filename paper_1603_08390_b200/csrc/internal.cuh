@@ -123,6 +123,10 @@ enum StatusWord : int {
     ST_T_WMIN = 19,
     ST_WORK_CTR1 = 32,  // scan queue cursors of the W = 8 / W = 16 classes (ST_WORK_CTR: W = 4)
     ST_WORK_CTR2 = 33,
+    ST_P_WAIT = 34,     // instrumented: prepare_item split (cycles): plan wait, issue, gate start, staging
+    ST_P_ISSUE = 35,
+    ST_P_GATE = 36,
+    ST_P_STAGE = 37,
     ST_WORDS = 40
 };
 constexpr uint32_t kWorkCtr[3] = {ST_WORK_CTR, ST_WORK_CTR1, ST_WORK_CTR2};

@@ -425,7 +425,7 @@ def test_cuda_graph_replay_equals_direct_launches(gpu):
     ds = synth.tweets(n=400_000, vocab=40_000, words=10, queries=128, k=100)
     ix = DeviceIndex.from_csr(ds.csr, device=gpu)
     host = ix.query(ds.queries)
-    cfg = config(graph=True)
+    cfg = config(graph=True, stage_events=True)  # stage events replay as external event nodes
     d = dev_batch(ds.queries)
     for _ in range(4):  # first call may grow the workspace (retry), then the graph settles
         ix.query_device(d, cfg, stream=s.cuda_stream)
@@ -438,6 +438,8 @@ def test_cuda_graph_replay_equals_direct_launches(gpu):
         assert not ix.status().get("retry")
         check(d, host)
     assert ix.graph_captures() == settled  # pure replays
+    st = ix.stage_ns()
+    assert st["match_ns"] > 0 and st["lookup_ns"] > 0
     # a different batch (new buffers): re-captured, still exact
     ds2 = synth.tweets(n=400_000, vocab=40_000, words=10, queries=96, k=100, seed=99)
     host2 = DeviceIndex.from_csr(ds.csr, device=gpu).query(ds2.queries)

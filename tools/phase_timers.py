@@ -16,9 +16,9 @@ def report(ix, items: int) -> str:
 
     from paper_1603_08390_b200 import _native as N
 
-    w = np.zeros(32, np.uint64)
+    w = np.zeros(40, np.uint64)
     err = C.create_string_buffer(256)
-    N.engine().genie_debug_status(ix.handle, w.ctypes.data_as(N.u64p), 32, err, 256)
+    N.engine().genie_debug_status(ix.handle, w.ctypes.data_as(N.u64p), 40, err, 256)
     tot = max(1, int(w[20] + w[21] + w[22] + w[23]))
     items = max(1, items)
     return (f"items={items} setup={100*w[20]/tot:.1f}% dense={100*w[23]/tot:.1f}% scan={100*w[21]/tot:.1f}% "
@@ -29,7 +29,8 @@ def report(ix, items: int) -> str:
             f"scan warps max={w[18]/items:.0f} min={w[19]/items:.0f} | dense items={(int(w[17]) >> 32) & 0xffff} "
             f"lists={int(w[17]) & 0xffffffff} bit-sliced={int(w[17]) >> 48} | per dense item: thread-0 work "
             f"{w[28]/max(1, (int(w[17]) >> 32) & 0xffff):.0f} init+barrier {w[29]/max(1, (int(w[17]) >> 32) & 0xffff):.0f} "
-            f"total {w[23]/max(1, (int(w[17]) >> 32) & 0xffff):.0f}")
+            f"total {w[23]/max(1, (int(w[17]) >> 32) & 0xffff):.0f} | prepare: plan wait {w[34]/items:.0f} "
+            f"issue {w[35]/items:.0f} gate start {w[36]/items:.0f} staging {w[37]/items:.0f}")
 
 
 if __name__ == "__main__":
