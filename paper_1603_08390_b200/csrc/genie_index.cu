@@ -88,7 +88,40 @@ static double dense_density(genie_index* ix) {
     return std::atof(v);
 }
 
+// Per-dim key ranges (k_resolve): dim d's keywords are keys[first, first +
+// count); when its tokens are exactly tok0 .. tok0 + count - 1 (LSH tokens,
+// categorical domains) the count carries a flag and a point item resolves by
+// arithmetic instead of a binary search over all K keys.
+__global__ void k_dim_ranges(const uint64_t* keys, uint64_t K, DimRange* out) {
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < K; j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t d = static_cast<uint32_t>(keys[j] >> 32);
+        if (j > 0 && static_cast<uint32_t>(keys[j - 1] >> 32) == d) continue;  // first key of its dim only
+        uint64_t lo = j, hi = K;  // end of the dim: first key with a larger dim
+        while (lo < hi) {
+            const uint64_t m = (lo + hi) >> 1;
+            if (static_cast<uint32_t>(keys[m] >> 32) <= d) lo = m + 1;
+            else hi = m;
+        }
+        const uint64_t cnt = lo - j;
+        const uint32_t t0 = static_cast<uint32_t>(keys[j]), t1 = static_cast<uint32_t>(keys[lo - 1]);
+        DimRange r;
+        r.first = j;
+        r.count = static_cast<uint32_t>(cnt) | ((uint64_t(t1) - t0 + 1 == cnt) ? kDimDenseFlag : 0u);
+        r.tok0 = t0;
+        out[d] = r;
+    }
+}
+
+// Index finalization shared by every construction path: the per-dim key
+// ranges, then the dense containers.
 void build_dense_containers(genie_index* ix, const uint64_t* h_off) {
+    ix->dim_range.reserve(65536);
+    GENIE_CUDA(cudaMemsetAsync(ix->dim_range.p, 0, 65536 * sizeof(DimRange), ix->stream));
+    if (ix->K) {
+        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((ix->K + 255) / 256, uint64_t(ix->sms) * 8));
+        k_dim_ranges<<<blocks, 256, 0, ix->stream>>>(ix->keys.p, ix->K, ix->dim_range.p);
+        GENIE_CUDA(cudaGetLastError());
+    }
     const double dens = dense_density(ix);
     std::vector<int32_t> slot(ix->K, -1);
     std::vector<uint64_t> dense_keys;

@@ -56,6 +56,7 @@ struct BatchParams {
     const uint32_t* postings;
     const uint32_t* dim_mult;
     const int32_t* key_dense;  // [K] dense-container slot or -1
+    const DimRange* dim_range; // [65536] each dim's key range
     const uint32_t* bitmaps;   // [n_dense][bitmap_words]
     uint32_t bitmap_words, n_dense;
     uint32_t dense_inv[3];  // per width class W = 4, 8, 16: use a bitmap iff len * inv >= n (0: always)
@@ -140,11 +141,25 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
                 lohi_bad = true;
             } else {
                 const uint64_t kl = (uint64_t(d) << 32) | l;
-                const uint64_t a = lower_bound_dev(p.keys, p.K, kl);
-                // single-token items (the common case) need no second search:
-                // keys are unique, so the range is [a, a + (keys[a] == key))
-                const uint64_t e = l == h ? a + (a < p.K && p.keys[a] == kl)
-                                          : upper_bound_dev(p.keys, p.K, (uint64_t(d) << 32) | h);
+                // search only the dim's keys; a dim whose tokens are contiguous
+                // resolves by arithmetic (LSH dims, categorical domains)
+                const DimRange r = p.dim_range[d];
+                const uint32_t cnt = r.count & ~kDimDenseFlag;
+                uint64_t a, e;
+                if (r.count & kDimDenseFlag) {
+                    const uint64_t lo_off = l > r.tok0 ? uint64_t(l) - r.tok0 : 0;
+                    const uint64_t hi_end = h >= r.tok0 ? uint64_t(h) - r.tok0 + 1 : 0;
+                    a = r.first + (lo_off < cnt ? lo_off : cnt);
+                    e = r.first + (hi_end < cnt ? hi_end : cnt);
+                    if (e < a) e = a;
+                } else {
+                    const uint64_t* dk = p.keys + r.first;
+                    a = r.first + lower_bound_dev(dk, cnt, kl);
+                    // single-token items (the common case) need no second search:
+                    // keys are unique, so the range is [a, a + (keys[a] == key))
+                    e = l == h ? a + (a < r.first + cnt && p.keys[a] == kl)
+                               : r.first + upper_bound_dev(dk, cnt, (uint64_t(d) << 32) | h);
+                }
                 kb = static_cast<uint32_t>(a);
                 nk = static_cast<uint32_t>(e - a);
                 pp = p.key_off[e] - p.key_off[a];
@@ -352,6 +367,38 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
                 npair = nt + 1;
             }
         }
+        // Short lists: the whole warp streams the list once (coalesced) and a
+        // tile boundary is cut where consecutive postings change tile --
+        // ceil(len / 32) loads instead of nt - 1 binary searches (C4: ~244
+        // postings, 21 boundaries per list).
+        uint32_t lin = __ballot_sync(0xffffffffu, npair && len <= kCutLinearMax);
+        if (lin & (1u << lane)) npair = 0;
+        while (lin) {
+            const int o = __ffs(lin) - 1;
+            lin &= lin - 1;
+            const uint32_t o_len = __shfl_sync(0xffffffffu, len, o), o_nt = __shfl_sync(0xffffffffu, nt, o);
+            const uint32_t o_T = __shfl_sync(0xffffffffu, T, o), o_st = __shfl_sync(0xffffffffu, cst, o);
+            const uint64_t o_beg = __shfl_sync(0xffffffffu, beg, o), o_cb = __shfl_sync(0xffffffffu, cbase, o);
+            uint32_t* cut = p.cuts + o_cb;
+            if (lane == 0) {
+                cut[0] = 0;
+                cut[uint64_t(o_nt) * o_st] = o_len;
+            }
+            uint32_t carry = 0;  // tile of the posting before this chunk (0 before the first)
+            for (uint32_t b0 = 0; b0 < o_len; b0 += 32) {
+                const uint32_t i = b0 + lane;
+                const uint32_t ti = i < o_len ? p.postings[o_beg + i] / o_T : 0xffffffffu;
+                uint32_t tp = __shfl_up_sync(0xffffffffu, ti, 1);
+                if (lane == 0) tp = carry;
+                // boundaries b in (tp, ti] start at posting i (b < nt; b = nt is the end)
+                if (i < o_len)
+                    for (uint32_t b = tp + 1; b <= ti && b < o_nt; ++b) cut[uint64_t(b) * o_st] = i;
+                const uint32_t last = min(31u, o_len - 1 - b0);
+                carry = __shfl_sync(0xffffffffu, ti, last);
+            }
+            // boundaries past the last posting's tile: all postings precede them
+            for (uint32_t b = carry + 1 + lane; b < o_nt; b += 32) cut[uint64_t(b) * o_st] = o_len;
+        }
         const uint32_t incl = warp_inclusive_scan(npair);
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         for (uint32_t r = 0; r < tot; r += 32) {
@@ -453,7 +500,8 @@ constexpr uint32_t kPlan = kDesc + 2 * sizeof(ItemDesc);       // QueryPlan of t
 constexpr uint32_t kZa = kPlan + sizeof(QueryPlan);            // kZaMax u32
 constexpr uint32_t kStage = kZa + kZaMax * 4;                  // 2 x StageBuf
 constexpr uint32_t kStageBytes = kSpanBatch * (8 + 4 + 4 + 4) + 16;
-constexpr uint32_t kHt = kStage + 2 * kStageBytes;             // ht_slots u64, then the tile
+// ht_slots u64, then the counter tile (start aligned to GENIE_HT_ALIGN bytes)
+constexpr uint32_t kHt = (kStage + 2 * kStageBytes + GENIE_HT_ALIGN - 1) / GENIE_HT_ALIGN * GENIE_HT_ALIGN;
 static_assert(kHt % 16 == 0, "16-byte aligned table");
 }  // namespace smem_off
 
@@ -1919,12 +1967,15 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     const StageArgs sa = stage_args(p, pl, S);
     const uint32_t nsb = min(kSpanBatch, S);
     stage_warp_issue(p, sa, sm.sb(buf), t, 0, nsb);
-    uint32_t nq = 0, ntile = 0, nclaim = 0xffffffffu;
+    uint32_t nq = 0, ntile = 0;
     if (claim != 0xffffffffu) {
         nq = p.work_q[claim];
         ntile = p.work_t[claim];
     }
-    if (lane == 0 && claim != 0xffffffffu) nclaim = fetch_item(p, total);
+    // the next claim: the raw counter value is range-checked only at the
+    // end, so nothing waits on the atomic's round trip before then
+    unsigned long long raw_claim = ~0ull;
+    if (lane == 0 && claim != 0xffffffffu) raw_claim = atomicAdd(&p.st[total.ctr], 1ull);
     const bool gate = (p.selector == GENIE_SELECT_CPQ) && pl.W <= 8;
 #ifdef GENIE_PHASE_TIMERS
     const long long pt2 = clock64();
@@ -1945,7 +1996,10 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
 #endif
     if (claim != 0xffffffffu && lane < sizeof(QueryPlan) / 16)
         cp_async16(reinterpret_cast<uint4*>(sm.plan) + lane, reinterpret_cast<const uint4*>(p.plan + nq) + lane);
-    nclaim = __shfl_sync(0xffffffffu, nclaim, 0);
+    raw_claim = __shfl_sync(0xffffffffu, raw_claim, 0);
+    const uint32_t nclaim = raw_claim != ~0ull && total.base + raw_claim < total.end
+                                ? static_cast<uint32_t>(total.base + raw_claim)
+                                : 0xffffffffu;
     if (lane == 0) {
         d->q = q;
         d->t = t;
@@ -2789,6 +2843,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.span_beg = w.span_beg.p;
     p.span_dense = w.span_dense.p;
     p.key_dense = ix->key_dense.p;
+    p.dim_range = ix->dim_range.p;
     p.bitmaps = ix->bitmaps.p;
     p.bitmap_words = ix->bitmap_words;
     p.n_dense = ix->n_dense;

@@ -42,6 +42,10 @@ constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shar
 #ifndef GENIE_CUT_CTAS
 #define GENIE_CUT_CTAS 32
 #endif
+#ifndef GENIE_CUT_LINEAR_MAX  // k_cut: lists up to this many postings are cut by one linear pass
+#define GENIE_CUT_LINEAR_MAX 1024
+#endif
+constexpr uint32_t kCutLinearMax = GENIE_CUT_LINEAR_MAX;
 constexpr uint32_t kLookupThreads = GENIE_LOOKUP_THREADS;  // k_resolve / k_cut block size
 constexpr uint32_t kCutCtasPerSm = GENIE_CUT_CTAS;         // k_cut grid: CTAs per SM
 constexpr uint32_t kMergeThreads = 512;
@@ -65,6 +69,9 @@ constexpr uint32_t kLvl = GENIE_DENSE_LEVELS;  // dense-phase c-PQ levels counte
 // compact posting scan when the staged slices fill their 128-posting groups
 // less than 1/kCompactFillInv on average
 constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
+#ifndef GENIE_HT_ALIGN  // alignment of the table + counter-tile start in the scan CTA's shared memory
+#define GENIE_HT_ALIGN 16
+#endif
 #ifndef GENIE_DENSE_NOINLINE  // dense phase as out-of-line calls (own register allocation)
 #define GENIE_DENSE_NOINLINE 0
 #endif
@@ -164,6 +171,15 @@ struct Workspace {
     size_t cap_q = 0, cap_items = 0, cap_spans = 0, cap_cuts = 0, cap_work = 0, cap_tout = 0;
 };
 
+// Keywords of one dim (k_dim_ranges): keys[first, first + (count & ~flag));
+// kDimDenseFlag set when its tokens are tok0 .. tok0 + count - 1.
+struct __align__(16) DimRange {
+    uint64_t first;
+    uint32_t count;
+    uint32_t tok0;
+};
+constexpr uint32_t kDimDenseFlag = 0x80000000u;
+
 }  // namespace genie
 
 struct genie_index {
@@ -175,6 +191,7 @@ struct genie_index {
     genie::DevBuf<uint64_t> keys, key_off;
     genie::DevBuf<uint32_t> postings;  // padded for aligned 16-byte tail loads
     genie::DevBuf<uint32_t> dim_mult;  // 65536
+    genie::DevBuf<genie::DimRange> dim_range;  // 65536: each dim's key range (k_resolve)
     // dense containers: keys whose list covers >= dense_density of the
     // objects also carry a bitmap of n bits (Roaring-style bitmap container)
     genie::DevBuf<int32_t> key_dense;   // [K] slot in `bitmaps` or -1

@@ -46,7 +46,7 @@ def test_dropin_runs_on_gpu(gpu, tmp_path):
 @pytest.mark.gpu
 def test_reference_api_on_gpu(gpu, tmp_path):
     exe = build(tmp_path, "test_reference_api")
-    r = subprocess.run([str(exe), "300"], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([str(exe), "120"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "reference api: ok" in r.stdout, r.stdout[-4000:] + r.stderr[-4000:]
 
 

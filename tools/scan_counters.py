@@ -66,8 +66,12 @@ def capture(workloads):
     outdir.mkdir(parents=True, exist_ok=True)
     for w in workloads:
         rep = outdir / f"scan_{w}"
+        # the batch's width class: W = 4 (tweets, adult) or 8 (sift, ocr, minhash); the other
+        # classes' k_scan launches exit at once
+        wcls = 4 if w in ("tweets", "adult") else 8
         cmd = ["ncu", "--set", "full", "--metrics", ",".join(METRICS), "--clock-control", "none",
-               "--import-source", "on", "-k", "regex:k_scan", "--launch-skip", "3", "--launch-count", "1",
+               "--import-source", "on", "--kernel-name-base", "demangled", "-k", f"regex:k_scan<{wcls}>",
+               "--launch-skip", "3", "--launch-count", "1",
                "-f", "-o", str(rep), sys.executable, str(ROOT / "bench.py"), "--workload", w, "--steps", "1",
                "--warmup", "3", "--no-cpu-baseline"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -87,7 +91,7 @@ def num(d, k):
     v, u = d[k]
     x = float(v.replace(",", ""))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-             "msecond": 1e-3, "second": 1}.get(u, 1)
+             "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}.get(u, 1)
     return x * scale
 
 
