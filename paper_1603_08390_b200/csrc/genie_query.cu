@@ -57,6 +57,7 @@ struct BatchParams {
     const uint32_t* dim_mult;
     const int32_t* key_dense;  // [K] dense-container slot or -1
     const DimRange* dim_range; // [65536] each dim's key range
+    const uint32_t* keycut[3]; // per width class: precomputed tile cuts of every key (or null)
     const uint32_t* bitmaps;   // [n_dense][bitmap_words]
     uint32_t bitmap_words, n_dense;
     uint32_t dense_inv[3];  // per width class W = 4, 8, 16: use a bitmap iff len * inv >= n (0: always)
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
          g0 += nwarps * G) {
         const uint64_t g = g0 + lane;
         uint32_t npair = 0, len = 0, nt = 0, T = 0, cst = 0;
-        uint64_t beg = 0, cbase = 0;
+        uint64_t beg = 0, cbase = 0, krow = 0;  // krow: address of the key's row of the cut table (0: none)
         if (lane < G && g < total) {
             // query owning global span g (last q with span_base <= g)
             const uint32_t q = static_cast<uint32_t>(upper_bound_dev(p.q_span_base, p.Q, g) - 1);
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
                 cst = p.q_S[q];
                 cbase = p.q_cut_base[q] + s;
                 npair = nt + 1;
+                if (const uint32_t* kc = p.keycut[wclass(p.q_W[q])]) krow = reinterpret_cast<uint64_t>(kc + j * (nt + 1));
             }
         }
         // Short lists: the whole warp streams the list once (coalesced) and a
@@ -385,16 +387,27 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
                 cut[uint64_t(o_nt) * o_st] = o_len;
             }
             uint32_t carry = 0;  // tile of the posting before this chunk (0 before the first)
-            for (uint32_t b0 = 0; b0 < o_len; b0 += 32) {
-                const uint32_t i = b0 + lane;
-                const uint32_t ti = i < o_len ? p.postings[o_beg + i] / o_T : 0xffffffffu;
-                uint32_t tp = __shfl_up_sync(0xffffffffu, ti, 1);
-                if (lane == 0) tp = carry;
-                // boundaries b in (tp, ti] start at posting i (b < nt; b = nt is the end)
-                if (i < o_len)
-                    for (uint32_t b = tp + 1; b <= ti && b < o_nt; ++b) cut[uint64_t(b) * o_st] = i;
-                const uint32_t last = min(31u, o_len - 1 - b0);
-                carry = __shfl_sync(0xffffffffu, ti, last);
+            for (uint32_t c0 = 0; c0 < o_len; c0 += 32 * kCutLinearUnroll) {
+                // every load of the chunk in flight at once
+                uint32_t v[kCutLinearUnroll];
+#pragma unroll
+                for (uint32_t u = 0; u < kCutLinearUnroll; ++u) {
+                    const uint32_t i = c0 + u * 32 + lane;
+                    v[u] = i < o_len ? __ldg(p.postings + o_beg + i) : 0u;
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < kCutLinearUnroll; ++u) {
+                    const uint32_t b0 = c0 + u * 32;
+                    if (b0 >= o_len) break;  // warp-uniform
+                    const uint32_t i = b0 + lane;
+                    const uint32_t ti = i < o_len ? v[u] / o_T : 0xffffffffu;
+                    uint32_t tp = __shfl_up_sync(0xffffffffu, ti, 1);
+                    if (lane == 0) tp = carry;
+                    // boundaries b in (tp, ti] start at posting i (b < nt; b = nt is the end)
+                    if (i < o_len)
+                        for (uint32_t b = tp + 1; b <= ti && b < o_nt; ++b) cut[uint64_t(b) * o_st] = i;
+                    carry = __shfl_sync(0xffffffffu, ti, min(31u, o_len - 1 - b0));
+                }
             }
             // boundaries past the last posting's tile: all postings precede them
             for (uint32_t b = carry + 1 + lane; b < o_nt; b += 32) cut[uint64_t(b) * o_st] = o_len;
@@ -416,11 +429,13 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
             const uint64_t o_beg = __shfl_sync(0xffffffffu, beg, o & 31);
             const uint64_t o_cb = __shfl_sync(0xffffffffu, cbase, o & 31);
             const uint32_t o_st = __shfl_sync(0xffffffffu, cst, o & 31);
+            const uint64_t o_krow = __shfl_sync(0xffffffffu, krow, o & 31);
             if (idx < tot) {
                 const uint32_t b = idx - (o_incl - o_np);
                 uint32_t v;
                 if (b == 0) v = 0;
                 else if (b == o_nt) v = o_len;
+                else if (o_krow) v = reinterpret_cast<const uint32_t*>(o_krow)[b];
                 else v = static_cast<uint32_t>(lower_bound_dev(p.postings + o_beg, o_len, b * o_T));
                 p.cuts[o_cb + uint64_t(b) * o_st] = v;
             }
@@ -1765,7 +1780,7 @@ __device__ __forceinline__ StageArgs stage_args(const BatchParams& p, const Quer
 struct WorkQueue {  // one width class's items [base, end) of the work list, claimed via st[ctr]
     uint32_t base, end, ctr;
 };
-__device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, const WorkQueue& total);
+GENIE_PREP_FN void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, const WorkQueue& total);
 
 template <int W, bool IL>
 __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t b,
@@ -1945,7 +1960,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 // item (asynchronous copies), the lower tiles' records (gate start), the
 // (query, tile) of the claimed item and the next claim; then it finishes the
 // staging and starts the copy of the claimed item's plan.
-__device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, const WorkQueue& total) {
+GENIE_PREP_FN void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, const WorkQueue& total) {
     const uint32_t lane = threadIdx.x & 31;
     ItemDesc* d = sm.desc + buf;
     const uint32_t item = sm.scal[SC_PF_ITEM];
@@ -1957,12 +1972,16 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
 #ifdef GENIE_PHASE_TIMERS
     const long long pt0 = clock64();
 #endif
+#if GENIE_PLAN_ASYNC
     cp_async_wait_all();  // q's plan (previous call)
     __syncwarp();
+    const QueryPlan pl = *sm.plan;
+#else
+    const QueryPlan pl = p.plan[q];
+#endif
 #ifdef GENIE_PHASE_TIMERS
     const long long pt1 = clock64();
 #endif
-    const QueryPlan pl = *sm.plan;
     uint32_t S;
     const StageArgs sa = stage_args(p, pl, S);
     const uint32_t nsb = min(kSpanBatch, S);
@@ -1995,7 +2014,8 @@ __device__ void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t 
     }
 #endif
     if (claim != 0xffffffffu && lane < sizeof(QueryPlan) / 16)
-        cp_async16(reinterpret_cast<uint4*>(sm.plan) + lane, reinterpret_cast<const uint4*>(p.plan + nq) + lane);
+        if (GENIE_PLAN_ASYNC)
+            cp_async16(reinterpret_cast<uint4*>(sm.plan) + lane, reinterpret_cast<const uint4*>(p.plan + nq) + lane);
     raw_claim = __shfl_sync(0xffffffffu, raw_claim, 0);
     const uint32_t nclaim = raw_claim != ~0ull && total.base + raw_claim < total.end
                                 ? static_cast<uint32_t>(total.base + raw_claim)
@@ -2523,6 +2543,42 @@ __global__ void k_keys_to_rows(genie_entry* out, const uint32_t* out_len, uint32
     }
 }
 
+// ------------------------------------------------------------ key cut table
+
+// keycut[j * (nt + 1) + b] = number of key j's postings below object b * T
+// (b = 0 .. nt): the tile-aligned slices of every list, searched once per
+// index and tile size instead of once per (query, span) in every batch.
+__global__ void k_keycut(const uint64_t* key_off, const uint32_t* postings, uint64_t K, uint32_t nt, uint32_t T,
+                         uint32_t* out) {
+    const uint64_t total = K * (nt + 1);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t j = i / (nt + 1);
+        const uint32_t b = static_cast<uint32_t>(i - j * (nt + 1));
+        const uint64_t beg = key_off[j];
+        const uint32_t len = static_cast<uint32_t>(key_off[j + 1] - beg);
+        out[i] = b == 0 ? 0u : (b == nt ? len : static_cast<uint32_t>(lower_bound_dev(postings + beg, len, b * T)));
+    }
+}
+
+// Builds the table of every width class the index has been queried with
+// (class_seen, from the previous batches' status) at the batch's tile sizes.
+static void ensure_keycuts(genie_index* ix, const uint32_t (&tile_bits_w)[3], cudaStream_t s) {
+    if (!ix->K || !ix->n) return;
+    for (int c = 0; c < 3; ++c) {
+        const uint32_t T = tile_bits_w[c] / (4u << c);
+        if (!ix->class_seen[c] || ix->keycut_T[c] == T) continue;
+        const uint32_t nt = (ix->n + T - 1) / T;
+        const uint64_t total = ix->K * uint64_t(nt + 1);
+        if (total > (1ull << 31)) continue;  // bound the cache (~8 GB); such indexes keep searching
+        ix->keycut[c].reserve(total);
+        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, uint64_t(ix->sms) * 32));
+        k_keycut<<<blocks, 256, 0, s>>>(ix->key_off.p, ix->postings.p, ix->K, nt, T, ix->keycut[c].p);
+        GENIE_CUDA(cudaGetLastError());
+        ix->keycut_T[c] = T;
+    }
+}
+
 // ------------------------------------------------------------ CUDA graphs
 
 // What a captured batch depends on: replayed only while all of it is equal.
@@ -2794,6 +2850,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     const uint32_t tile_bytes = tile_bits / 8;
     reserve_workspace(ix, Q, total_items, max_k, out_stride,
                       std::min({tile_bits_w[0] * 4, tile_bits_w[1] * 2, tile_bits_w[2]}));
+    ensure_keycuts(ix, tile_bits_w, s);
     Workspace& w = ix->ws;
     ix->last_Q = Q;
     ix->last_cfg = cfg;
@@ -2844,6 +2901,8 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.span_dense = w.span_dense.p;
     p.key_dense = ix->key_dense.p;
     p.dim_range = ix->dim_range.p;
+    for (int c = 0; c < 3; ++c)
+        p.keycut[c] = ix->keycut_T[c] == tile_bits_w[c] / (4u << c) ? ix->keycut[c].p : nullptr;
     p.bitmaps = ix->bitmaps.p;
     p.bitmap_words = ix->bitmap_words;
     p.n_dense = ix->n_dense;
@@ -3000,6 +3059,8 @@ int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
     GENIE_CUDA(cudaStreamSynchronize(ix->stream));
     GENIE_CUDA(cudaGetLastError());
     const unsigned long long* h = ix->ws.h_status;
+    for (int c = 0; c < 3; ++c)
+        if (h[ST_CLASS0 + c]) ix->class_seen[c] = true;  // its cut table is built before the next batch
     if (stats) {
         stats->postings = h[ST_TOTAL_POSTINGS];
         stats->work_items = h[ST_TOTAL_WORK];

@@ -43,9 +43,10 @@ constexpr uint32_t kZaMax = 256;              // ZipperArray levels held in shar
 #define GENIE_CUT_CTAS 32
 #endif
 #ifndef GENIE_CUT_LINEAR_MAX  // k_cut: lists up to this many postings are cut by one linear pass
-#define GENIE_CUT_LINEAR_MAX 1024
+#define GENIE_CUT_LINEAR_MAX 0  // measured slower than the binary searches on C4 (0.37 vs 0.28 ms lookup)
 #endif
 constexpr uint32_t kCutLinearMax = GENIE_CUT_LINEAR_MAX;
+constexpr uint32_t kCutLinearUnroll = 8;  // posting loads per lane in flight in the linear pass
 constexpr uint32_t kLookupThreads = GENIE_LOOKUP_THREADS;  // k_resolve / k_cut block size
 constexpr uint32_t kCutCtasPerSm = GENIE_CUT_CTAS;         // k_cut grid: CTAs per SM
 constexpr uint32_t kMergeThreads = 512;
@@ -69,6 +70,9 @@ constexpr uint32_t kLvl = GENIE_DENSE_LEVELS;  // dense-phase c-PQ levels counte
 // compact posting scan when the staged slices fill their 128-posting groups
 // less than 1/kCompactFillInv on average
 constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
+#ifndef GENIE_PLAN_ASYNC  // query plans prefetched into shared memory one item ahead (1) or loaded in place (0)
+#define GENIE_PLAN_ASYNC 1
+#endif
 #ifndef GENIE_HT_ALIGN  // alignment of the table + counter-tile start in the scan CTA's shared memory
 #define GENIE_HT_ALIGN 16
 #endif
@@ -79,6 +83,14 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #define GENIE_DENSE_FN __device__ __noinline__
 #else
 #define GENIE_DENSE_FN __device__
+#endif
+#ifndef GENIE_PREP_NOINLINE  // warp 0's prepare_item as an out-of-line call
+#define GENIE_PREP_NOINLINE 0
+#endif
+#if GENIE_PREP_NOINLINE
+#define GENIE_PREP_FN __device__ __noinline__
+#else
+#define GENIE_PREP_FN __device__
 #endif
 #ifndef GENIE_SPAN_PREFETCH  // L2 bulk prefetch of the next item's posting slices (prepare_item)
 #define GENIE_SPAN_PREFETCH 0
@@ -192,6 +204,12 @@ struct genie_index {
     genie::DevBuf<uint32_t> postings;  // padded for aligned 16-byte tail loads
     genie::DevBuf<uint32_t> dim_mult;  // 65536
     genie::DevBuf<genie::DimRange> dim_range;  // 65536: each dim's key range (k_resolve)
+    // per width class: every key's position of each object-tile boundary
+    // (keycut[c][j * (nt + 1) + b], tiles of keycut_T[c] objects), built once
+    // the class has been queried; k_cut then reads cuts instead of searching
+    genie::DevBuf<uint32_t> keycut[3];
+    uint32_t keycut_T[3] = {0, 0, 0};
+    bool class_seen[3] = {false, false, false};
     // dense containers: keys whose list covers >= dense_density of the
     // objects also carry a bitmap of n bits (Roaring-style bitmap container)
     genie::DevBuf<int32_t> key_dense;   // [K] slot in `bitmaps` or -1

@@ -450,3 +450,22 @@ def test_cuda_graph_replay_equals_direct_launches(gpu):
             break
     check(d2, host2)
     assert ix.graph_captures() > settled
+
+
+@pytest.mark.parametrize("tile_bytes", [0, 16384])
+def test_key_cut_table_equals_searches(gpu, oracle, tile_bytes):
+    """The first batch of a width class cuts lists by binary search; later
+    batches read the per-key cut table built from it (k_keycut).  Both, and a
+    tile-size change (table rebuilt), give the oracle's answer."""
+    from paper_1603_08390_b200 import config
+
+    ds = synth.tweets(n=600_000, vocab=50_000, words=10, queries=96, k=100)
+    want = oracle.index(ds.csr).execute(ds.queries)
+    ix = DeviceIndex.from_csr(ds.csr, device=gpu)
+    for cfg in (config(tile_bytes=tile_bytes), config(tile_bytes=tile_bytes), config(tile_bytes=8192),
+                config(tile_bytes=tile_bytes)):
+        got = ix.query(ds.queries, cfg)
+        assert np.array_equal(got.length, want.length) and np.array_equal(got.threshold, want.threshold)
+        for q in range(len(ds.queries)):
+            assert got.row(q) == want.row(q)
+    ix.close()
