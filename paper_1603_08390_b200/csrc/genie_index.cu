@@ -104,11 +104,28 @@ __global__ void k_dim_ranges(const uint64_t* keys, uint64_t K, DimRange* out) {
         }
         const uint64_t cnt = lo - j;
         const uint32_t t0 = static_cast<uint32_t>(keys[j]), t1 = static_cast<uint32_t>(keys[lo - 1]);
-        DimRange r;
+        DimRange r{};
         r.first = j;
         r.count = static_cast<uint32_t>(cnt) | ((uint64_t(t1) - t0 + 1 == cnt) ? kDimDenseFlag : 0u);
         r.tok0 = t0;
+        r.pad = t1;  // the dim's last token (the host sizes the token maps from it)
         out[d] = r;
+    }
+}
+
+// Fills the token maps: key j (rank i in its dim, token t) owns map entries
+// (t - tok0, t_next - tok0], i.e. every token up to its successor's has
+// i + 1 keys below it.
+__global__ void k_tokmap(const uint64_t* keys, uint64_t K, const DimRange* ranges, uint32_t* map) {
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < K; j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t d = static_cast<uint32_t>(keys[j] >> 32);
+        const DimRange r = ranges[d];
+        if (!r.map_span) continue;
+        const uint32_t cnt = r.count & ~kDimDenseFlag;
+        const uint64_t i = j - r.first;
+        const uint32_t x0 = static_cast<uint32_t>(keys[j]) - r.tok0;
+        const uint32_t x1 = i + 1 < cnt ? static_cast<uint32_t>(keys[j + 1]) - r.tok0 : r.map_span;
+        for (uint32_t x = x0 + 1; x <= x1; ++x) map[r.map_off + x] = static_cast<uint32_t>(i + 1);
     }
 }
 
@@ -121,6 +138,32 @@ void build_dense_containers(genie_index* ix, const uint64_t* h_off) {
         const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((ix->K + 255) / 256, uint64_t(ix->sms) * 8));
         k_dim_ranges<<<blocks, 256, 0, ix->stream>>>(ix->keys.p, ix->K, ix->dim_range.p);
         GENIE_CUDA(cudaGetLastError());
+        // token maps for gapped dims whose token span is at most 8x their key
+        // count (C2: 1M-word vocabulary with gaps -> one 4 MB map); a point
+        // item then resolves with one map load instead of a 20-step search
+        std::vector<DimRange> h(65536);
+        GENIE_CUDA(cudaMemcpyAsync(h.data(), ix->dim_range.p, 65536 * sizeof(DimRange), cudaMemcpyDeviceToHost,
+                                   ix->stream));
+        GENIE_CUDA(cudaStreamSynchronize(ix->stream));
+        uint64_t total = 0;
+        for (auto& r : h) {
+            const uint32_t cnt = r.count & ~kDimDenseFlag;
+            if (!cnt || (r.count & kDimDenseFlag)) continue;
+            const uint64_t span = uint64_t(r.pad) - r.tok0 + 1;
+            if (span <= 8ull * cnt && total + span + 1 <= (1ull << 28)) {
+                r.map_off = total;
+                r.map_span = static_cast<uint32_t>(span);
+                total += span + 1;
+            }
+        }
+        if (total) {
+            ix->tokmap.reserve(total);
+            GENIE_CUDA(cudaMemsetAsync(ix->tokmap.p, 0, total * 4, ix->stream));
+            GENIE_CUDA(cudaMemcpyAsync(ix->dim_range.p, h.data(), 65536 * sizeof(DimRange), cudaMemcpyHostToDevice,
+                                       ix->stream));
+            k_tokmap<<<blocks, 256, 0, ix->stream>>>(ix->keys.p, ix->K, ix->dim_range.p, ix->tokmap.p);
+            GENIE_CUDA(cudaGetLastError());
+        }
     }
     const double dens = dense_density(ix);
     std::vector<int32_t> slot(ix->K, -1);

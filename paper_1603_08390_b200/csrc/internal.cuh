@@ -189,6 +189,11 @@ struct __align__(16) DimRange {
     uint64_t first;
     uint32_t count;
     uint32_t tok0;
+    // token map of a dim whose tokens have gaps (map_span > 0): the dim's
+    // tokmap[map_off + x] = #keys with token < tok0 + x, x in [0, map_span]
+    uint64_t map_off;
+    uint32_t map_span;
+    uint32_t pad;
 };
 constexpr uint32_t kDimDenseFlag = 0x80000000u;
 
@@ -204,6 +209,7 @@ struct genie_index {
     genie::DevBuf<uint32_t> postings;  // padded for aligned 16-byte tail loads
     genie::DevBuf<uint32_t> dim_mult;  // 65536
     genie::DevBuf<genie::DimRange> dim_range;  // 65536: each dim's key range (k_resolve)
+    genie::DevBuf<uint32_t> tokmap;            // token -> key-rank maps of gapped dims (DimRange::map_*)
     // per width class: every key's position of each object-tile boundary
     // (keycut[c][j * (nt + 1) + b], tiles of keycut_T[c] objects), built once
     // the class has been queried; k_cut then reads cuts instead of searching
