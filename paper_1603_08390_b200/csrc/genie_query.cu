@@ -1785,9 +1785,15 @@ __device__ __forceinline__ StageArgs stage_args(const BatchParams& p, const Quer
     return sa;
 }
 
+// warps that prepare the next item in the W kernel (GENIE_PREP_WARPS_W8 for W >= 8)
+template <int W>
+__device__ __host__ constexpr uint32_t prep_warps() {
+    return W >= 8 ? GENIE_PREP_WARPS_W8 : 1u;
+}
 struct WorkQueue {  // one width class's items [base, end) of the work list, claimed via st[ctr]
     uint32_t base, end, ctr;
 };
+template <int PW>
 GENIE_PREP_FN void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, const WorkQueue& total);
 
 template <int W, bool IL>
@@ -1797,11 +1803,11 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
 #ifdef GENIE_PHASE_TIMERS
     const long long t_setup = clock64();
 #endif
-    // warps 1.. scan this item's postings while warp 0 prepares the next item
-    constexpr uint32_t kScanWarp0 = 1;
+    // warps PW.. scan this item's postings while warps 0..PW-1 prepare the next item
+    constexpr uint32_t kScanWarp0 = prep_warps<W>();
 #ifdef GENIE_PHASE_TIMERS
-    if (threadIdx.x < 32) {
-        prepare_item(p, sm, b ^ 1u, total);
+    if (threadIdx.x < 32 * kScanWarp0) {
+        prepare_item<kScanWarp0>(p, sm, b ^ 1u, total);
         if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_PREP], static_cast<unsigned long long>(clock64() - t_setup));
     } else {
         scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, kScanWarp0, ptot);
@@ -1813,7 +1819,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
         }
     }
 #else
-    if (threadIdx.x < 32) prepare_item(p, sm, b ^ 1u, total);
+    if (threadIdx.x < 32 * kScanWarp0) prepare_item<kScanWarp0>(p, sm, b ^ 1u, total);
     else scan_groups<W, IL>(p, it, sm, sm.sb(b), nsb, G, p.unit, kScanWarp0, ptot);
 #endif
     __syncthreads();
@@ -1968,21 +1974,33 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 // item (asynchronous copies), the lower tiles' records (gate start), the
 // (query, tile) of the claimed item and the next claim; then it finishes the
 // staging and starts the copy of the claimed item's plan.
+__device__ __forceinline__ void named_barrier(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// PW = 1: warp 0 does everything below.  PW = 2 (the W >= 8 kernels: C3-C5,
+// whose items stage up to 237 short slices): warp 1 stages the slices while
+// warp 0 claims, reads the records for the gate start and writes the
+// descriptor -- the two halves of the round trip run side by side (two
+// named barriers: the plan is in shared memory / warp 1 is done with it).
+template <int PW>
 GENIE_PREP_FN void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32_t buf, const WorkQueue& total) {
-    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t lane = threadIdx.x & 31, pw = threadIdx.x >> 5;  // pw < PW
     ItemDesc* d = sm.desc + buf;
     const uint32_t item = sm.scal[SC_PF_ITEM];
     if (item == 0xffffffffu) {
-        if (lane == 0) d->valid = 0;
+        if (threadIdx.x == 0) d->valid = 0;
         return;
     }
     const uint32_t q = sm.scal[SC_PF_Q], t = sm.scal[SC_PF_T], claim = sm.scal[SC_CLAIM];
+    constexpr uint32_t kStager = PW - 1;  // the warp that stages the slices
 #ifdef GENIE_PHASE_TIMERS
     const long long pt0 = clock64();
 #endif
 #if GENIE_PLAN_ASYNC
-    cp_async_wait_all();  // q's plan (previous call)
-    __syncwarp();
+    if (pw == 0) cp_async_wait_all();  // q's plan (issued by warp 0 in the previous call)
+    if constexpr (PW > 1) named_barrier(1, 32 * PW);
+    else __syncwarp();
     const QueryPlan pl = *sm.plan;
 #else
     const QueryPlan pl = p.plan[q];
@@ -1993,34 +2011,48 @@ GENIE_PREP_FN void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32
     uint32_t S;
     const StageArgs sa = stage_args(p, pl, S);
     const uint32_t nsb = min(kSpanBatch, S);
-    stage_warp_issue(p, sa, sm.sb(buf), t, 0, nsb);
-    uint32_t nq = 0, ntile = 0;
-    if (claim != 0xffffffffu) {
-        nq = p.work_q[claim];
-        ntile = p.work_t[claim];
-    }
-    // the next claim: the raw counter value is range-checked only at the
-    // end, so nothing waits on the atomic's round trip before then
+    if (pw == kStager) stage_warp_issue(p, sa, sm.sb(buf), t, 0, nsb);
+    uint32_t nq = 0, ntile = 0, a0 = 0;
     unsigned long long raw_claim = ~0ull;
-    if (lane == 0 && claim != 0xffffffffu) raw_claim = atomicAdd(&p.st[total.ctr], 1ull);
     const bool gate = (p.selector == GENIE_SELECT_CPQ) && pl.W <= 8;
 #ifdef GENIE_PHASE_TIMERS
-    const long long pt2 = clock64();
+    long long pt2 = 0, pt3 = 0;
 #endif
-    const uint32_t a0 = gate ? gate_start(p, q, t, pl.k, pl.bound, pl.tile_base) : 0u;
+    if (pw == 0) {
+        if (claim != 0xffffffffu) {
+            nq = p.work_q[claim];
+            ntile = p.work_t[claim];
+        }
+        // the next claim: the raw counter value is range-checked only at the
+        // end, so nothing waits on the atomic's round trip before then
+        if (lane == 0 && claim != 0xffffffffu) raw_claim = atomicAdd(&p.st[total.ctr], 1ull);
 #ifdef GENIE_PHASE_TIMERS
-    const long long pt3 = clock64();
+        pt2 = clock64();
 #endif
-    const uint32_t G = stage_warp_finish(p, sa, sm.sb(buf), t, 0, nsb);
+        a0 = gate ? gate_start(p, q, t, pl.k, pl.bound, pl.tile_base) : 0u;
+#ifdef GENIE_PHASE_TIMERS
+        pt3 = clock64();
+#endif
+    }
+    uint32_t G = 0;
+    if (pw == kStager) {
+        G = stage_warp_finish(p, sa, sm.sb(buf), t, 0, nsb);
+        if (lane == 0) {
+            d->G = G;
+            d->ptot = sm.sb(buf).ppref()[nsb];
+        }
+    }
+    if constexpr (PW > 1) named_barrier(2, 32 * PW);  // staging done, warp 1 no longer reads sm.plan
 #ifdef GENIE_PHASE_TIMERS
     const long long pt4 = clock64();
-    if (lane == 0) {  // prepare split: plan wait / issue / gate start / staging finish
+    if (threadIdx.x == 0) {  // prepare split: plan wait / issue / gate start / staging finish
         atomicAdd(&p.st[ST_P_WAIT], static_cast<unsigned long long>(pt1 - pt0));
         atomicAdd(&p.st[ST_P_ISSUE], static_cast<unsigned long long>(pt2 - pt1));
         atomicAdd(&p.st[ST_P_GATE], static_cast<unsigned long long>(pt3 - pt2));
         atomicAdd(&p.st[ST_P_STAGE], static_cast<unsigned long long>(pt4 - pt3));
     }
 #endif
+    if (pw != 0) return;
     if (claim != 0xffffffffu && lane < sizeof(QueryPlan) / 16)
         if (GENIE_PLAN_ASYNC)
             cp_async16(reinterpret_cast<uint4*>(sm.plan) + lane, reinterpret_cast<const uint4*>(p.plan + nq) + lane);
@@ -2038,8 +2070,6 @@ GENIE_PREP_FN void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32
         d->nt = sa.nt;
         d->S = S;
         d->nd = sa.dense ? pl.nd : 0u;
-        d->G = G;
-        d->ptot = sm.sb(buf).ppref()[nsb];
         d->a0 = a0;
         d->out_base = pl.out_base + uint64_t(t) * pl.cap;
         d->tile_slot = pl.tile_base + t;
@@ -2203,9 +2233,9 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
             sm.scal[SC_WMAX] = 0;
             sm.scal[SC_WMIN] = 0xffffffffu;
         }
-        __syncwarp();
-        prepare_item(p, sm, 0, total);
     }
+    __syncthreads();
+    if (threadIdx.x < 32 * prep_warps<W>()) prepare_item<prep_warps<W>()>(p, sm, 0, total);
     __syncthreads();
     for (uint32_t iter = 0;; ++iter) {
         const uint32_t b = iter & 1u;

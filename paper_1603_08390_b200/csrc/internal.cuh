@@ -84,6 +84,9 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #else
 #define GENIE_DENSE_FN __device__
 #endif
+#ifndef GENIE_PREP_WARPS_W8  // warps preparing the next item in the W >= 8 kernels (1 or 2)
+#define GENIE_PREP_WARPS_W8 2
+#endif
 #ifndef GENIE_PREP_NOINLINE  // warp 0's prepare_item as an out-of-line call
 #define GENIE_PREP_NOINLINE 0
 #endif
