@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--span-chunk", type=int, default=None, help="postings per warp work unit (result-invariant)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the kernels one by one (no CUDA graph)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 exchange: NCCL over NVLink (default) or gloo through host memory (plumbing tests)")
     ap.add_argument("--ref-sample", type=int, default=0, help="queries per reference step (0: auto)")
     return ap.parse_args()
 
@@ -514,6 +516,25 @@ def scan_roofline(workload, world, postings, scan_ms, clocks, sms):
     return out
 
 
+GOLDEN_NAME = {"adult": "c1", "tweets": "c2", "sift": "c3", "minhash": "c4", "ocr": "c5"}
+
+
+def result_parity(args, w, Q, stride, out, out_len, out_thr):
+    """hash_results (engine.hpp:141-153) of the last timed batch against the
+    reference-pinned digest of the same config (tests/golden/full_configs.json),
+    when the workload runs at its BASELINE size."""
+    from paper_1603_08390_b200.engine import hash_results
+
+    g = json.loads((ROOT / "tests" / "golden" / "full_configs.json").read_text()).get(GOLDEN_NAME[args.workload])
+    if not g or args.n or args.queries:
+        return {"checked": False, "why": "no golden digest for this size"}
+    ent = out.cpu().numpy().view(np.uint32).reshape(Q, stride, 2)
+    h = hash_results(w.batch.qid, out_thr.cpu().numpy().astype(np.uint32), out_len.cpu().numpy().astype(np.uint32),
+                     ent[:, :, 0], ent[:, :, 1])
+    return {"checked": True, "hash": f"{h:#018x}", "golden": g["hash"], "equal": f"{h:#018x}" == g["hash"],
+            "golden_source": g["source"]}
+
+
 def encode_roofline(workload, w):
     """The index-side LSH / minHash transform, timed on its own (CUDA events,
     inputs resident): SURVEY 8d bounds it by FP64 issue (p-stable: one DMUL +
@@ -546,10 +567,30 @@ def main_genie(args):
 
     rank, local, world = dist_env()
     assert world == args.gpus or world == 1, "launch N>1 under torch.distributed.run"
+    # ranks beyond the box's GPUs share devices (gloo plumbing tests on a 1-GPU box)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    gloo = args.dist_backend == "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def all_gather(dst, src):
+        """[world, ...] <- every rank's src: NCCL over NVLink, or through host memory for gloo."""
+        if not gloo:
+            dist.all_gather_into_tensor(dst, src)
+            return
+        parts = [torch.zeros_like(src, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, src.cpu())
+        dst.copy_(torch.stack(parts))
+
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], device="cpu" if gloo else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     # a dedicated stream: torch's default stream has handle 0, which the C ABI
     # reads as "the index's own stream"
     stream = torch.cuda.Stream(dev)
@@ -571,24 +612,37 @@ def main_genie(args):
 
     launches_per_step = 0
 
-    def step():
+    def step(check=False):
+        """One batch; with check, the shard batch's status (workspace growth,
+        errors) is read before the merge reuses the status block."""
         nonlocal launches_per_step
         launches_per_step = w.encode(sptr)
         launches_per_step += ix.query_device(d, cfg, stream=sptr)
+        st = None
+        if check:
+            torch.cuda.synchronize(dev)
+            st = ix.status()
+            retry = float(bool(st.get("retry")))
+            if world > 1:
+                retry = max_over_ranks(retry)
+            if retry:
+                return {"retry": True}
         if world > 1:
             # all-gather the per-shard top-k (global ids), merge on the device
-            dist.all_gather_into_tensor(gath, d["out"])
-            dist.all_gather_into_tensor(gath_len, d["out_len"])
+            all_gather(gath, d["out"])
+            all_gather(gath_len, d["out_len"])
             # rank-major rows merged in place (list-major layout, no transpose)
             ix.merge_device(Q, world, gath, gath_len, stride, d["k"], stride, fin, fin_len, fin_thr, stream=sptr,
                             list_major=True)
             launches_per_step += 3
+            if check:
+                torch.cuda.synchronize(dev)
+                ix.status()  # merge errors (duplicate ids) surface here
+        return st
 
     def run_checked():
         for _ in range(3):
-            step()
-            torch.cuda.synchronize(dev)
-            st = ix.status()
+            st = step(check=True)
             if not st.get("retry"):
                 return st
         raise RuntimeError("workspace did not converge")
@@ -623,9 +677,9 @@ def main_genie(args):
         print(report(ix, int(stats["work_items"])), file=sys.stderr)
     total_ms = float(np.sum(step_ms))
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms)
+    parity = result_parity(args, w, Q, stride, *((fin, fin_len, fin_thr) if world > 1 else
+                                                 (d["out"], d["out_len"], d["out_thr"])))
     ms_per_step = total_ms / args.steps
     value = Q * args.steps / (total_ms / 1000.0)
 
@@ -647,8 +701,8 @@ def main_genie(args):
         if world > 1:
             lists = torch.from_numpy(hout[0]).to(dev)
             lens = torch.from_numpy(hout[1].astype(np.int32)).to(dev)
-            dist.all_gather_into_tensor(gath, lists.view(torch.int32))
-            dist.all_gather_into_tensor(gath_len, lens)
+            all_gather(gath, lists.view(torch.int32))
+            all_gather(gath_len, lens)
             ix.merge_device(Q, world, gath, gath_len, stride, d["k"], stride, fin, fin_len, fin_thr, stream=sptr,
                             list_major=True)
             fin.cpu(), fin_len.cpu(), fin_thr.cpu()
@@ -667,9 +721,7 @@ def main_genie(args):
         e2e_times.append(time.perf_counter() - t)
     e2e_s = float(np.mean(e2e_times))
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s)
     e2e_value = Q / e2e_s
 
     # ---- roofline of the dominant kernel (k_scan: fused scan + c-PQ + tile select)
@@ -715,7 +767,8 @@ def main_genie(args):
             "stage_ms": {"step_mean": round(float(np.mean(step_ms)), 4), "scan_mean": round(float(np.mean(scan_ms)), 4),
                          "lookup_mean": round(float(np.mean(look_ms)), 4),
                          "merge_mean": round(float(np.mean(merge_ms)), 4)},
-            "fallback_tiles": int(st.get("fallback_tiles", 0)), "work_items": int(st.get("work_items", 0)),
+            "fallback_tiles": int(stats.get("fallback_tiles", 0)), "work_items": int(stats.get("work_items", 0)),
+            "parity": parity,
         }
         if getattr(w, "sigma", None):
             line["config"]["sigma"] = round(w.sigma, 6)

@@ -519,8 +519,12 @@ namespace smem_off {
 constexpr uint32_t kScal = 0;                                  // SC_WORDS u32 (<= 32)
 constexpr uint32_t kSums = 128;                                // 32 u64
 constexpr uint32_t kDesc = kSums + 256;                        // 2 x ItemDesc
+#if GENIE_PLAN_AT_END  // the QueryPlan slot after the tile (carve); the fixed area keeps round 1's offsets
+constexpr uint32_t kZa = kDesc + 2 * sizeof(ItemDesc);         // kZaMax u32
+#else
 constexpr uint32_t kPlan = kDesc + 2 * sizeof(ItemDesc);       // QueryPlan of the next item's query
 constexpr uint32_t kZa = kPlan + sizeof(QueryPlan);            // kZaMax u32
+#endif
 constexpr uint32_t kStage = kZa + kZaMax * 4;                  // 2 x StageBuf
 constexpr uint32_t kStageBytes = kSpanBatch * (8 + 4 + 4 + 4) + 16;
 // ht_slots u64, then the counter tile (start aligned to GENIE_HT_ALIGN bytes)
@@ -528,13 +532,18 @@ constexpr uint32_t kHt = (kStage + 2 * kStageBytes + GENIE_HT_ALIGN - 1) / GENIE
 static_assert(kHt % 16 == 0, "16-byte aligned table");
 }  // namespace smem_off
 
-__device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t ht_slots) {
+__device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t ht_slots, uint32_t tile_bytes) {
     using namespace smem_off;
     ScanSmem s;
     s.scal = reinterpret_cast<uint32_t*>(base + kScal);
     s.sums = reinterpret_cast<unsigned long long*>(base + kSums);
     s.desc = reinterpret_cast<ItemDesc*>(base + kDesc);
+#if GENIE_PLAN_AT_END
+    s.plan = reinterpret_cast<QueryPlan*>(base + kHt + size_t(ht_slots) * 8 + tile_bytes);
+#else
     s.plan = reinterpret_cast<QueryPlan*>(base + kPlan);
+    (void)tile_bytes;
+#endif
     s.za = reinterpret_cast<uint32_t*>(base + kZa);
     s.stage = base + kStage;
     static_assert(kStageBytes == kSpanBatch * 20 + 16, "stage buffer layout");
@@ -545,7 +554,7 @@ __device__ __forceinline__ ScanSmem carve(uint8_t* base, uint32_t ht_slots) {
 }
 
 inline size_t scan_smem_bytes(uint32_t tile_bytes, uint32_t ht_slots) {
-    return smem_off::kHt + size_t(ht_slots) * 8 + tile_bytes;
+    return smem_off::kHt + size_t(ht_slots) * 8 + tile_bytes + (GENIE_PLAN_AT_END ? sizeof(QueryPlan) : 0);
 }
 
 __device__ __forceinline__ uint32_t ht_home(uint32_t id, uint32_t mask) {
@@ -2192,8 +2201,7 @@ template <int W>
 __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     k_scan(BatchParams p, uint32_t tile_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
-    (void)tile_bytes;
-    const ScanSmem sm = carve(smem, p.ht_slots);
+    const ScanSmem sm = carve(smem, p.ht_slots, tile_bytes);
     if (p.st[ST_OVERFLOW]) return;
     constexpr uint32_t c = W == 4 ? 0 : (W == 8 ? 1 : 2);
     WorkQueue total{0, 0, kWorkCtr[c]};
@@ -2786,7 +2794,8 @@ static uint32_t auto_tile_bytes() {
         int smem_sm = 0, reserved = 0;
         GENIE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
         GENIE_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev));
-        const int per_cta = smem_sm / static_cast<int>(kScanCtasPerSm) - reserved - static_cast<int>(smem_off::kHt) - static_cast<int>(kHtSlots * 8);
+        const int per_cta = smem_sm / static_cast<int>(kScanCtasPerSm) - reserved - static_cast<int>(smem_off::kHt) -
+                            static_cast<int>(kHtSlots * 8) - (GENIE_PLAN_AT_END ? int(sizeof(QueryPlan)) : 0);
         tb_cached = per_cta > 4096 ? static_cast<uint32_t>(per_cta) : 4096u;
         dev_cached = dev;
     }

@@ -73,6 +73,9 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #ifndef GENIE_PLAN_ASYNC  // query plans prefetched into shared memory one item ahead (1) or loaded in place (0)
 #define GENIE_PLAN_ASYNC 1
 #endif
+#ifndef GENIE_PLAN_AT_END  // the prefetched QueryPlan after the counter tile instead of in the fixed area
+#define GENIE_PLAN_AT_END 0
+#endif
 #ifndef GENIE_HT_ALIGN  // alignment of the table + counter-tile start in the scan CTA's shared memory
 #define GENIE_HT_ALIGN 16
 #endif
