@@ -9,6 +9,7 @@
 #include <thread>
 #include <vector>
 
+#include "block.cuh"
 #include "internal.cuh"
 
 namespace genie {
@@ -35,19 +36,33 @@ __global__ void k_dim_max(const uint32_t* post, uint64_t b, uint64_t e, uint32_t
     if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
 }
 
+__global__ void k_max_into(const uint32_t* src, uint32_t* dst, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[i] = max(dst[i], src[i]);
+}
+
+// max_multiplicity per dim (index.hpp:110-113, 153-174): per dim with more
+// than one keyword, count each object's postings of that dim and take the
+// max (two passes over only the dim's postings); a one-keyword dim has
+// multiplicity 1 (ObjectRecord rejects duplicate keywords) -- gram-coded
+// corpora have tens of thousands of such dims.
 static void compute_dim_stats(genie_index* ix, const uint64_t* h_keys, const uint64_t* h_off) {
     GENIE_CUDA(cudaMemsetAsync(ix->dim_mult.p, 0, 65536 * sizeof(uint32_t), ix->stream));
     if (!ix->K || !ix->n) return;
     DevBuf<uint32_t> scratch;
     scratch.reserve(ix->n);
     GENIE_CUDA(cudaMemsetAsync(scratch.p, 0, size_t(ix->n) * sizeof(uint32_t), ix->stream));
+    std::vector<uint32_t> single(65536, 0);  // dims with one keyword: every object carries it at most once
+    bool any_single = false;
     uint64_t j = 0;
     while (j < ix->K) {
         const uint32_t d = static_cast<uint32_t>(h_keys[j] >> 32);
         uint64_t e = j;
         while (e < ix->K && static_cast<uint32_t>(h_keys[e] >> 32) == d) ++e;
         const uint64_t pb = h_off[j], pe = h_off[e];
-        if (pe > pb) {
+        if (e - j == 1) {
+            if (pe > pb) single[d] = 1, any_single = true;
+        } else if (pe > pb) {
             const uint64_t blocks = std::min<uint64_t>((pe - pb + 255) / 256, uint64_t(ix->sms) * 16);
             k_dim_count<<<static_cast<unsigned>(blocks), 256, 0, ix->stream>>>(ix->postings.p, pb, pe,
                                                                               scratch.p);
@@ -55,6 +70,14 @@ static void compute_dim_stats(genie_index* ix, const uint64_t* h_keys, const uin
                                                                             scratch.p, ix->dim_mult.p + d);
         }
         j = e;
+    }
+    if (any_single) {  // the multi-keyword dims' maxima were atomicMax'ed into zeros: merge by max
+        DevBuf<uint32_t> ones;
+        ones.reserve(65536);
+        GENIE_CUDA(cudaMemcpyAsync(ones.p, single.data(), 65536 * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                   ix->stream));
+        k_max_into<<<256, 256, 0, ix->stream>>>(ones.p, ix->dim_mult.p, 65536);
+        GENIE_CUDA(cudaStreamSynchronize(ix->stream));
     }
     GENIE_CUDA(cudaStreamSynchronize(ix->stream));
     GENIE_CUDA(cudaGetLastError());
@@ -113,6 +136,37 @@ __global__ void k_dim_ranges(const uint64_t* keys, uint64_t K, DimRange* out) {
     }
 }
 
+// Which gapped dims get a token map (span <= 8 x keys, total <= 2^28 entries)
+// and where: one CTA, 64 dims per thread, a block scan of the map sizes.
+__global__ void __launch_bounds__(1024) k_tokmap_plan(DimRange* ranges, unsigned long long* total_out) {
+    __shared__ unsigned long long sums[32];
+    constexpr uint32_t kPer = 65536 / 1024;
+    unsigned long long mine = 0;
+    for (uint32_t i = 0; i < kPer; ++i) {
+        const DimRange& r = ranges[threadIdx.x * kPer + i];
+        const uint32_t cnt = r.count & ~kDimDenseFlag;
+        if (!cnt || (r.count & kDimDenseFlag)) continue;
+        const uint64_t span = uint64_t(r.pad) - r.tok0 + 1;
+        if (span <= 8ull * cnt) mine += span + 1;
+    }
+    unsigned long long total = 0;
+    unsigned long long at = block_exclusive_scan<unsigned long long>(mine, sums, total);
+    const bool fits = total <= (1ull << 28);  // all or nothing: the maps are an accelerator
+    for (uint32_t i = 0; i < kPer; ++i) {
+        DimRange& r = ranges[threadIdx.x * kPer + i];
+        const uint32_t cnt = r.count & ~kDimDenseFlag;
+        r.map_span = 0;
+        if (!fits || !cnt || (r.count & kDimDenseFlag)) continue;
+        const uint64_t span = uint64_t(r.pad) - r.tok0 + 1;
+        if (span <= 8ull * cnt) {
+            r.map_off = at;
+            r.map_span = static_cast<uint32_t>(span);
+            at += span + 1;
+        }
+    }
+    if (threadIdx.x == 0) *total_out = fits ? total : 0;
+}
+
 // Fills the token maps: key j (rank i in its dim, token t) owns map entries
 // (t - tok0, t_next - tok0], i.e. every token up to its successor's has
 // i + 1 keys below it.
@@ -140,27 +194,18 @@ void build_dense_containers(genie_index* ix, const uint64_t* h_off) {
         GENIE_CUDA(cudaGetLastError());
         // token maps for gapped dims whose token span is at most 8x their key
         // count (C2: 1M-word vocabulary with gaps -> one 4 MB map); a point
-        // item then resolves with one map load instead of a 20-step search
-        std::vector<DimRange> h(65536);
-        GENIE_CUDA(cudaMemcpyAsync(h.data(), ix->dim_range.p, 65536 * sizeof(DimRange), cudaMemcpyDeviceToHost,
-                                   ix->stream));
+        // item then resolves with one map load instead of a 20-step search.
+        // Planned on the device (one CTA scans the 65536 dims); only the
+        // total comes back to size the map.
+        DevBuf<unsigned long long> total_d;
+        total_d.reserve(1);
+        k_tokmap_plan<<<1, 1024, 0, ix->stream>>>(ix->dim_range.p, total_d.p);
+        unsigned long long total = 0;
+        GENIE_CUDA(cudaMemcpyAsync(&total, total_d.p, 8, cudaMemcpyDeviceToHost, ix->stream));
         GENIE_CUDA(cudaStreamSynchronize(ix->stream));
-        uint64_t total = 0;
-        for (auto& r : h) {
-            const uint32_t cnt = r.count & ~kDimDenseFlag;
-            if (!cnt || (r.count & kDimDenseFlag)) continue;
-            const uint64_t span = uint64_t(r.pad) - r.tok0 + 1;
-            if (span <= 8ull * cnt && total + span + 1 <= (1ull << 28)) {
-                r.map_off = total;
-                r.map_span = static_cast<uint32_t>(span);
-                total += span + 1;
-            }
-        }
         if (total) {
             ix->tokmap.reserve(total);
             GENIE_CUDA(cudaMemsetAsync(ix->tokmap.p, 0, total * 4, ix->stream));
-            GENIE_CUDA(cudaMemcpyAsync(ix->dim_range.p, h.data(), 65536 * sizeof(DimRange), cudaMemcpyHostToDevice,
-                                       ix->stream));
             k_tokmap<<<blocks, 256, 0, ix->stream>>>(ix->keys.p, ix->K, ix->dim_range.p, ix->tokmap.p);
             GENIE_CUDA(cudaGetLastError());
         }
