@@ -306,6 +306,12 @@ public:
         return k;
     }
 
+    // adopt an existing device copy of exactly these lists (build_index's
+    // device build), so the first query does not upload them again
+    void adopt_device(std::shared_ptr<genie_index> h) const {
+        std::call_once(lazy_->dev_once, [&] { lazy_->dev = std::move(h); });
+    }
+
     // the device index (uploaded once; shared by copies of this object)
     genie_index* device() const {
         std::call_once(lazy_->dev_once, [&] {
@@ -450,7 +456,7 @@ inline InvertedIndex build_index(std::span<const ObjectRecord> objects,
     char err[512] = {};
     genie_index* h = nullptr;
     detail::check(genie_index_build(n, obj_off.data(), dims.data(), toks.data(), device, &h, err, sizeof(err)), err);
-    std::unique_ptr<genie_index, void (*)(genie_index*)> guard(h, genie_index_destroy);
+    std::shared_ptr<genie_index> dev_ix(h, genie_index_destroy);
     std::uint32_t nn = 0, off_unused = 0;
     std::uint64_t K = 0, P = 0;
     int dev = 0;
@@ -458,7 +464,9 @@ inline InvertedIndex build_index(std::span<const ObjectRecord> objects,
     std::vector<std::uint64_t> keys(K), off(K + 1, 0);
     std::vector<ObjectId> post(P);
     detail::check(genie_index_export(h, keys.data(), off.data(), post.data(), err, sizeof(err)), err);
-    return detail::from_csr(n, keys, off, std::move(post), split_threshold, device);
+    InvertedIndex index = detail::from_csr(n, keys, off, std::move(post), split_threshold, device);
+    index.adopt_device(std::move(dev_ix));  // the built device CSR serves the queries
+    return index;
 }
 
 // ------------------------------------------------------------------ index_io

@@ -1722,8 +1722,17 @@ __device__ __forceinline__ uint32_t stage_warp_finish(const BatchParams& p, cons
             groups = len ? static_cast<uint32_t>(((beg + len - 1) >> 7) - (beg >> 7) + 1) : 0u;
             // the slice streams into L2 while the current item is scanned, so
             // this item's posting loads hit L2 instead of waiting on DRAM
-#if GENIE_SPAN_PREFETCH
+#if GENIE_SPAN_PREFETCH == 1
             if (len) prefetch_l2(p.postings + beg, len);
+#elif GENIE_SPAN_PREFETCH == 2
+            // the slice's first two 128-byte lines into L2 (per-lane prefetch;
+            // minHash slices are ~12 postings)
+            if (len) {
+                const uint32_t* a = p.postings + beg;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                if (((reinterpret_cast<uint64_t>(a) & 127) + uint64_t(len) * 4) > 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a + 32));
+            }
 #endif
         }
         __syncwarp();  // every lane has read its raw words before any result overwrites them

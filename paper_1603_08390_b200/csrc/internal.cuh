@@ -98,8 +98,8 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #else
 #define GENIE_PREP_FN __device__
 #endif
-#ifndef GENIE_SPAN_PREFETCH  // L2 bulk prefetch of the next item's posting slices (prepare_item)
-#define GENIE_SPAN_PREFETCH 0
+#ifndef GENIE_SPAN_PREFETCH  // L2 prefetch of the next item's posting slices: 0 off, 1 bulk (UBLKPF), 2 per-lane lines
+#define GENIE_SPAN_PREFETCH 2
 #endif
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
