@@ -1696,8 +1696,14 @@ __device__ __forceinline__ void stage_warp_issue(const BatchParams& p, const Sta
 // posting prefix and the compacted dense slots, 32 spans at a time, written
 // over the raw words in place.  Returns the number of 128-posting groups.
 __device__ __forceinline__ uint32_t stage_warp_finish(const BatchParams& p, const StageArgs& a, const StageBuf& sb,
-                                                      uint32_t t, uint32_t s0, uint32_t nsb) {
+                                                      uint32_t t, uint32_t s0, uint32_t nsb, uint32_t W = 0) {
     const uint32_t lane = threadIdx.x & 31;
+#if GENIE_BITMAP_PREFETCH
+    // the item's object tile, for the bitmap-row prefetch
+    const uint32_t T = W ? tile_objs(p, W) : 0u, tile_lo = t * T;
+    const uint32_t tile_n = T ? min(T, p.n - min(p.n, tile_lo)) : 0u;
+    const uint32_t tile_word0 = tile_lo >> 5, tile_bytes = (tile_n + 7) / 8;
+#endif
     if (!a.item_mode) {
         cp_async_wait_all();
         __syncwarp();
@@ -1728,10 +1734,12 @@ __device__ __forceinline__ uint32_t stage_warp_finish(const BatchParams& p, cons
             // the slice's first two 128-byte lines into L2 (per-lane prefetch;
             // minHash slices are ~12 postings)
             if (len) {
-                const uint32_t* a = p.postings + beg;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-                if (((reinterpret_cast<uint64_t>(a) & 127) + uint64_t(len) * 4) > 128)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a + 32));
+                // up to GENIE_PREFETCH_LINES 128-byte lines of the slice
+                const char* a = reinterpret_cast<const char*>(p.postings + beg);
+                const char* line = reinterpret_cast<const char*>(reinterpret_cast<uint64_t>(a) & ~127ull);
+                const char* end = a + uint64_t(len) * 4;
+                for (uint32_t l = 0; l < GENIE_PREFETCH_LINES && line < end; ++l, line += 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(line));
             }
 #endif
         }
@@ -1739,6 +1747,20 @@ __device__ __forceinline__ uint32_t stage_warp_finish(const BatchParams& p, cons
         const uint32_t incl = warp_inclusive_scan(groups);
         const uint32_t pincl = warp_inclusive_scan(len);
         const uint32_t dm = __ballot_sync(0xffffffffu, dslot >= 0);
+#if GENIE_BITMAP_PREFETCH
+        // the tile's slice of every dense list's bitmap row into L2, its 128-byte
+        // lines spread over the warp (C3: 64 lines per list, C2: 184)
+        if (dm && tile_bytes) {
+            for (uint32_t m = dm; m;) {
+                const int o = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t slot = __shfl_sync(0xffffffffu, static_cast<uint32_t>(dslot), o);
+                const char* row = reinterpret_cast<const char*>(p.bitmaps + size_t(slot) * p.bitmap_words + tile_word0);
+                for (uint32_t off = lane * 128; off < tile_bytes; off += 32 * 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
+            }
+        }
+#endif
         if (i < nsb) {
             sb.beg()[i] = beg;
             sb.upref()[i] = carry + incl - groups;
@@ -2054,7 +2076,7 @@ GENIE_PREP_FN void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32
     }
     uint32_t G = 0;
     if (pw == kStager) {
-        G = stage_warp_finish(p, sa, sm.sb(buf), t, 0, nsb);
+        G = stage_warp_finish(p, sa, sm.sb(buf), t, 0, nsb, pl.W);
         if (lane == 0) {
             d->G = G;
             d->ptot = sm.sb(buf).ppref()[nsb];

@@ -98,6 +98,12 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #else
 #define GENIE_PREP_FN __device__
 #endif
+#ifndef GENIE_BITMAP_PREFETCH  // also prefetch the next item's bitmap-row slices into L2
+#define GENIE_BITMAP_PREFETCH 0
+#endif
+#ifndef GENIE_PREFETCH_LINES  // 128-byte lines prefetched per posting slice (GENIE_SPAN_PREFETCH = 2)
+#define GENIE_PREFETCH_LINES 2
+#endif
 #ifndef GENIE_SPAN_PREFETCH  // L2 prefetch of the next item's posting slices: 0 off, 1 bulk (UBLKPF), 2 per-lane lines
 #define GENIE_SPAN_PREFETCH 2
 #endif
