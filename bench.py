@@ -200,7 +200,6 @@ class Workload:
     points into the batch's items (C3-C5) and is part of every step."""
 
     lsh = None  # engine.Encoder for C3-C5
-    _pinned = None  # e2e host buffers (host_encode)
 
     def __init__(self, args, rank, world, dev, local):
         import torch
@@ -314,29 +313,6 @@ class Workload:
         self.d["lo"].copy_(flat)
         self.d["hi"].copy_(flat)
         return 1
-
-    def host_encode(self):
-        """e2e: host query points/sets (pinned) -> tokens (pinned) through the
-        public API; the batch's lo/hi views the token buffer."""
-        if self._pinned is None:
-            import torch
-
-            from paper_1603_08390_b200 import engine as E
-
-            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-            Q = len(self.batch)
-            tok = pin(np.zeros((Q, self.m), np.uint32))
-            sk = E.point_queries(tok, self.k)
-            flat = tok.reshape(-1)
-            src = ((pin(self.ds.query_set_off.astype(np.uint64)), pin(self.ds.query_elems.astype(np.uint64)))
-                   if self.name == "minhash" else (pin(self.ds.query_points),))
-            self._pinned = (tok, src, E.QueryBatch(pin(sk.qid), pin(sk.k), pin(sk.item_off), pin(sk.dim), flat, flat))
-        tok, src, batch = self._pinned
-        if self.name == "minhash":
-            self.lsh.encode_sets(src[0], src[1], out=tok)
-        else:
-            self.lsh.encode(src[0], out=tok)
-        return batch, sum(a.nbytes for a in src), tok.nbytes
 
     def cpu_csr(self):
         if self.m is None:
@@ -691,13 +667,19 @@ def main_genie(args):
     qb = w.batch
     hb = QueryBatch(pin(qb.qid), pin(qb.k), pin(qb.item_off), pin(qb.dim), pin(qb.lo), pin(qb.hi))
 
+    if w.m:  # host query points / sets, pinned
+        e2e_src = (dict(set_off=pin(w.ds.query_set_off.astype(np.uint64)), elems=pin(w.ds.query_elems.astype(np.uint64)))
+                   if w.name == "minhash" else dict(points=pin(w.ds.query_points)))
+
     def e2e_step():
-        h2d, d2h = hb.nbytes(), 0
-        b = hb
         if w.m:
-            b, h2d_p, d2h_t = w.host_encode()
-            h2d, d2h = h2d_p + b.nbytes(), d2h_t
-        ix.query(b, e2e_cfg, stride=stride, out=hout, copy=False)
+            # LshEncoder::encode_query_point + execute_batch fused on the GPU
+            # (genie_lsh_query_batch): the tokens never leave the device
+            w.lsh.query(ix, w.k, cfg=e2e_cfg, stride=stride, out=hout, copy=False, **e2e_src)
+            h2d, d2h = sum(a.nbytes for a in e2e_src.values()), 0
+        else:
+            h2d, d2h = hb.nbytes(), 0
+            ix.query(hb, e2e_cfg, stride=stride, out=hout, copy=False)
         if world > 1:
             lists = torch.from_numpy(hout[0]).to(dev)
             lens = torch.from_numpy(hout[1].astype(np.int32)).to(dev)
@@ -758,7 +740,8 @@ def main_genie(args):
                        "generate_s": round(w.gen_s, 2), "index_build_s": round(w.build_s, 2)},
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes),
                     "d2h_bytes_per_step": int(d2h_bytes),
-                    "path": ("genie_lsh_encode + " if w.m else "") + "genie_query_batch (C ABI), pinned host buffers"
+                    "path": ("genie_lsh_query_batch (C ABI: host points/sets -> device encode -> batch)" if w.m else
+                     "genie_query_batch (C ABI)") + ", pinned host buffers"
                             + (" + all-gather + genie_merge_topk_device" if world > 1 else "")},
             "roofline": roof,
             "cpu_baseline": cpu,

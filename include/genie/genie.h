@@ -374,6 +374,18 @@ int genie_minhash_encode_device(genie_encoder* enc, const uint64_t* d_set_off,
                                 const uint64_t* d_elems, uint64_t n_sets, uint32_t* d_tokens,
                                 void* stream, char* err, size_t errlen);
 
+/* LshEncoder::encode_query_point + execute_batch in one call on the GPU (the
+ * query path of a vector / set index): host points (n x dims f32) or sets
+ * (minHash encoders: set_off[n+1], elems) are uploaded, encoded on the device
+ * into one point item per hash function (Keyword{i, f_i(p)}, lsh.hpp:186-195),
+ * queried with k results each (query_id = first_id + row) and the results read
+ * back -- the tokens never leave the device.  Same output contract as
+ * genie_query_batch. */
+int genie_lsh_query_batch(genie_encoder* enc, genie_index* ix, const genie_config* cfg, const float* points,
+                          const uint64_t* set_off, const uint64_t* elems, uint64_t n, uint32_t k, uint32_t first_id,
+                          uint32_t out_stride, genie_entry* out, uint32_t* out_len, uint32_t* out_threshold,
+                          genie_batch_stats* stats, char* err, size_t errlen);
+
 /* Builds a device index directly from device tokens (n_points x m, dim = function
  * index): the GPU counterpart of encode_dataset + build_index for LSH data.
  * Postings per key are ascending ids (stable counting sort). */

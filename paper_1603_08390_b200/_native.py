@@ -118,6 +118,9 @@ ENGINE_SYMBOLS = {
     "genie_index_from_tokens_device": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
                                                  C.POINTER(vp), C.c_char_p, C.c_size_t]),
     "genie_index_export": (C.c_int, [vp, u64p, u64p, u32p, C.c_char_p, C.c_size_t]),
+    "genie_lsh_query_batch": (C.c_int, [vp, vp, C.POINTER(Config), f32p, u64p, u64p, C.c_uint64, C.c_uint32,
+                                        C.c_uint32, C.c_uint32, C.POINTER(Entry), u32p, u32p, C.POINTER(BatchStats),
+                                        C.c_char_p, C.c_size_t]),
     "genie_mcix_parse_spans": (C.c_int, [vp, C.c_uint64, u64p, u16p, u64p, C.c_char_p, C.c_size_t]),
     "genie_mcix_serialize_spans": (C.c_int, [C.c_uint32, C.c_uint64, u64p, u16p, u64p, C.c_uint64, u32p, vp, u64p,
                                              C.c_char_p, C.c_size_t]),

@@ -613,6 +613,98 @@ int genie_minhash_encode(genie_encoder* enc, const uint64_t* set_off, const uint
     });
 }
 
+// Query items of encoded points: row q asks for k results with one point
+// item per hash function i (Keyword{dim = i, token = tokens[q m + i]},
+// lsh.hpp:186-195); lo / hi read the token matrix in place.
+__global__ void k_point_items(uint64_t n, uint32_t m, uint32_t k, uint32_t first_id, uint32_t* qid, uint32_t* kk,
+                              uint64_t* item_off, uint16_t* dim) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * m; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t q = i / m;
+        const uint32_t f = static_cast<uint32_t>(i - q * m);
+        dim[i] = static_cast<uint16_t>(f);
+        if (f == 0) {
+            qid[q] = first_id + static_cast<uint32_t>(q);
+            kk[q] = k;
+            item_off[q] = i;
+        }
+        if (i + 1 == n * m) item_off[n] = n * m;
+    }
+}
+
+int genie_lsh_query_batch(genie_encoder* enc, genie_index* ix, const genie_config* cfg_in, const float* points,
+                          const uint64_t* set_off, const uint64_t* elems, uint64_t n, uint32_t k, uint32_t first_id,
+                          uint32_t out_stride, genie_entry* out, uint32_t* out_len, uint32_t* out_threshold,
+                          genie_batch_stats* stats, char* err, size_t errlen) {
+    return guarded(err, errlen, [&]() -> int {
+        const genie_config cfg = cfg_in ? *cfg_in : genie_config_default();
+        validate_config(cfg);
+        if (!enc || !ix) throw Error(GENIE_ERR_CONTRACT, "genie_lsh_query_batch: null encoder or index");
+        if (enc->device != ix->device) throw Error(GENIE_ERR_CONTRACT, "encoder and index on different devices");
+        const genie_lsh_config& c = enc->cfg;
+        const bool sets = c.family == GENIE_LSH_MINHASH;
+        if (n && (sets ? (!set_off || !elems) : !points)) throw Error(GENIE_ERR_CONTRACT, "genie_lsh_query_batch: null input");
+        if (n && (!out || !out_len || !out_threshold)) throw Error(GENIE_ERR_CONTRACT, "genie_lsh_query_batch: null output");
+        if (k == 0) throw Error(GENIE_ERR_CONTRACT, "Query " + std::to_string(first_id) + ": k must be >= 1");
+        if (n >= (1u << 21)) throw Error(GENIE_ERR_CONTRACT, "batch exceeds 2^21 queries");
+        if (n * c.m >= (1ull << 32)) throw Error(GENIE_ERR_CONTRACT, "too many query items");
+        if (n && out_stride < std::min<uint64_t>(k, std::max<uint32_t>(ix->n, 1)))
+            throw Error(GENIE_ERR_CONTRACT, "out_stride must be >= min(k, num_objects)");
+        if (!n) return GENIE_OK;
+        ensure_device(ix->device);
+        cudaStream_t s = ix->stream;
+        const uint32_t Q = static_cast<uint32_t>(n);
+        // 1. inputs up, tokens on the device (never read back)
+        DevBuf<uint32_t>& tok = enc->ws_tokens;
+        tok.reserve(n * c.m);
+        char e2[256];
+        int rc;
+        if (sets) {
+            const uint64_t ne = set_off[n] - set_off[0];
+            std::vector<uint64_t> off(set_off, set_off + n + 1);
+            for (auto& o : off) o -= set_off[0];
+            enc->ws_off.reserve(n + 1);
+            enc->ws_elems.reserve(std::max<uint64_t>(ne, 1));
+            GENIE_CUDA(cudaMemcpyAsync(enc->ws_off.p, off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, s));
+            if (ne) GENIE_CUDA(cudaMemcpyAsync(enc->ws_elems.p, elems + set_off[0], ne * 8, cudaMemcpyHostToDevice, s));
+            rc = genie_minhash_encode_device(enc, enc->ws_off.p, enc->ws_elems.p, n, tok.p, s, e2, sizeof(e2));
+        } else {
+            enc->ws_points.reserve(n * c.dims);
+            GENIE_CUDA(cudaMemcpyAsync(enc->ws_points.p, points, n * c.dims * sizeof(float), cudaMemcpyHostToDevice, s));
+            rc = genie_lsh_encode_device(enc, enc->ws_points.p, n, tok.p, s, e2, sizeof(e2));
+        }
+        if (rc) throw Error(rc, e2);
+        // 2. the batch: one point item per function, lo = hi = the token
+        Workspace& w = ix->ws;
+        w.d_qid.reserve(Q);
+        w.d_k.reserve(Q);
+        w.d_item_off.reserve(Q + 1);
+        w.d_dim.reserve(n * c.m);
+        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n * c.m + 255) / 256, uint64_t(ix->sms) * 16));
+        k_point_items<<<blocks, 256, 0, s>>>(n, c.m, k, first_id, w.d_qid.p, w.d_k.p, w.d_item_off.p, w.d_dim.p);
+        GENIE_CUDA(cudaGetLastError());
+        const uint32_t stride = std::max<uint32_t>(out_stride, 1);
+        w.d_out.reserve(uint64_t(Q) * stride);
+        w.d_out_len.reserve(Q + 1);
+        w.d_out_thr.reserve(Q + 1);
+        // 3. query (re-issued if the workspace had to grow), results down
+        std::string msg;
+        genie_batch_stats local{};
+        rc = GENIE_RETRY;
+        for (int attempt = 0; attempt < 4 && rc == GENIE_RETRY; ++attempt) {
+            launch_batch(ix, cfg, Q, w.d_qid.p, w.d_k.p, w.d_item_off.p, w.d_dim.p, tok.p, tok.p,
+                         static_cast<uint32_t>(n * c.m), k, stride, w.d_out.p, w.d_out_len.p, w.d_out_thr.p, s, false);
+            rc = finish_batch(ix, &local, msg, nullptr);
+        }
+        if (rc != GENIE_OK) throw Error(rc, msg);
+        GENIE_CUDA(cudaMemcpyAsync(out, w.d_out.p, uint64_t(Q) * stride * sizeof(genie_entry), cudaMemcpyDeviceToHost, s));
+        GENIE_CUDA(cudaMemcpyAsync(out_len, w.d_out_len.p, Q * 4, cudaMemcpyDeviceToHost, s));
+        GENIE_CUDA(cudaMemcpyAsync(out_threshold, w.d_out_thr.p, Q * 4, cudaMemcpyDeviceToHost, s));
+        GENIE_CUDA(cudaStreamSynchronize(s));
+        if (stats) *stats = local;
+        return GENIE_OK;
+    });
+}
+
 // encode_dataset + build_index for LSH data, on the device: stable radix sort
 // of (dim*D + token, id) pairs emitted in id order, so every list comes out
 // ascending (index.hpp:207-212, 235).

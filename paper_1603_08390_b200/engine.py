@@ -611,6 +611,37 @@ class Encoder:
                                                     C.c_void_p(d_tokens.data_ptr()), _torch_stream(stream), err,
                                                     len(err)), err)
 
+    def query(self, index: "DeviceIndex", k: int, points: Optional[np.ndarray] = None,
+              set_off: Optional[np.ndarray] = None, elems: Optional[np.ndarray] = None, first_id: int = 0,
+              cfg: Optional[N.Config] = None, stride: Optional[int] = None, out=None, copy: bool = True) -> Results:
+        """encode_query_point + execute_batch in one GPU call (genie_lsh_query_batch):
+        host points (or sets) in, results out; the tokens stay on the device."""
+        if points is not None:
+            pts = np.ascontiguousarray(points, np.float32)
+            n, pp, so, el = pts.shape[0], _ptr(pts, C.c_float), None, None
+        else:
+            so = np.ascontiguousarray(set_off, np.uint64)
+            el = np.ascontiguousarray(elems, np.uint64)
+            n, pp = so.shape[0] - 1, None
+        Q = int(n)
+        stride = int(stride if stride is not None else max(min(k, index.num_objects), 1))
+        if out is not None:
+            ent, ln, thr = out
+        else:
+            ent, ln, thr = np.zeros((Q, stride, 2), np.uint32), np.zeros(Q, np.uint32), np.zeros(Q, np.uint32)
+        stats, err = N.BatchStats(), _errbuf()
+        cfg = cfg if cfg is not None else config()
+        check(self._lib.genie_lsh_query_batch(
+            self._h, index.handle, C.byref(cfg), pp, None if so is None else _ptr(so, C.c_uint64),
+            None if el is None else _ptr(el, C.c_uint64), Q, k, first_id, stride,
+            ent.ctypes.data_as(C.POINTER(N.Entry)), _ptr(ln, C.c_uint32), _ptr(thr, C.c_uint32), C.byref(stats), err,
+            len(err)), err)
+        qid = np.arange(first_id, first_id + Q, dtype=np.uint32)
+        sdict = {f: getattr(stats, f) for f, _ in N.BatchStats._fields_}
+        if not copy:
+            return Results(qid, ent[:, :, 0], ent[:, :, 1], ln, thr, None, None, sdict)
+        return Results(qid, ent[:, :, 0].copy(), ent[:, :, 1].copy(), ln, thr, None, None, sdict)
+
 
 def _mcix_bytes(image) -> bytes:
     if isinstance(image, (bytes, bytearray, memoryview)):

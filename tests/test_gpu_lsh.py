@@ -113,3 +113,36 @@ def test_fp32_mode_disagreements_counted_and_bounded(gpu, oracle, family):
     if family == PSTABLE:  # a disagreement is a neighbouring bucket, never further
         diff = np.abs(exact.astype(np.int64) - fast.astype(np.int64))
         assert int(diff.max(initial=0)) <= 1
+
+
+@pytest.mark.parametrize("family", [PSTABLE, RBH, MINHASH])
+def test_fused_query_path_equals_encode_then_query(gpu, oracle, family):
+    """genie_lsh_query_batch (host points / sets in, tokens kept on the
+    device) == the host encode followed by genie_query_batch."""
+    from paper_1603_08390_b200.engine import point_queries
+
+    if family == PSTABLE:
+        ds = synth.sift(n=60_000, dims=128, queries=96)
+        enc = Encoder(lsh_config(PSTABLE, 237, 128, 3, w=4.0), gpu)
+        toks, qt, kw, k = enc.encode(ds.points), enc.encode(ds.query_points), dict(points=ds.query_points), 100
+        dom = 67
+    elif family == RBH:
+        ds = synth.ocr(n=8_000, dims=784, queries=64)
+        sigma = oracle.kernel_width(ds.points[:2000])
+        enc = Encoder(lsh_config(RBH, 237, 784, 7, sigma=sigma), gpu)
+        toks, qt, kw, k = enc.encode(ds.points), enc.encode(ds.query_points), dict(points=ds.query_points), 1
+        dom = 8192
+    else:
+        ds = synth.sets(n=50_000, queries=128)
+        enc = Encoder(lsh_config(MINHASH, 128, 0, 5, rehash_domain=8192), gpu)
+        toks = enc.encode_sets(ds.set_off, ds.elems)
+        qt = enc.encode_sets(ds.query_set_off, ds.query_elems)
+        kw, k, dom = dict(set_off=ds.query_set_off, elems=ds.query_elems), 100, 8192
+    ix = DeviceIndex.from_csr(csr_from_tokens(toks), device=gpu)
+    want = ix.query(point_queries(qt, k, first_id=7))
+    got = enc.query(ix, k, first_id=7, **kw)
+    assert np.array_equal(got.qid, want.qid)
+    assert np.array_equal(got.length, want.length) and np.array_equal(got.threshold, want.threshold)
+    for q in range(len(got.length)):
+        assert got.row(q) == want.row(q)
+    assert dom > 0
