@@ -662,8 +662,9 @@ def main_genie(args):
     # ---- e2e through the public C-ABI calls with host (pinned) buffers
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
     hout = (pin(np.zeros((Q, stride, 2), np.uint32)), pin(np.zeros(Q, np.uint32)), pin(np.zeros(Q, np.uint32)))
+    # the public host-buffer call; with pinned buffers it replays as one CUDA graph
     e2e_cfg = config(selector=args.selector, tile_bytes=args.tile_bytes, ctas_per_sm=args.ctas_per_sm,
-                     span_chunk=args.span_chunk)
+                     span_chunk=args.span_chunk, graph=not args.no_graph)
     qb = w.batch
     hb = QueryBatch(pin(qb.qid), pin(qb.k), pin(qb.item_off), pin(qb.dim), pin(qb.lo), pin(qb.hi))
 

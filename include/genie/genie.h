@@ -76,7 +76,10 @@ typedef struct {
 /* genie_config.flags: genie_query_batch_device replays the batch pipeline as
  * one CUDA graph, captured on first use and re-captured whenever the batch
  * shape, buffers, stream or workspace change (ignored for the legacy default
- * stream and for k > 8192). */
+ * stream and for k > 8192).  genie_query_batch does the same with the uploads
+ * and read-backs inside the graph when every host buffer is page-locked
+ * (cudaHostAlloc / pinned) and item_off[0] == 0; otherwise it launches
+ * directly. */
 #define GENIE_FLAG_GRAPH 2u
 
 /* mcx::StageTimings (engine.hpp:44-50), measured with CUDA events on the

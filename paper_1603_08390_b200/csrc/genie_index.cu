@@ -400,6 +400,8 @@ void genie_index_destroy(genie_index* ix) {
     cudaSetDevice(ix->device);
     if (ix->stream) cudaStreamSynchronize(ix->stream);
     if (ix->ws.h_status) cudaFreeHost(ix->ws.h_status);
+    if (ix->host_graph) cudaGraphExecDestroy(ix->host_graph);
+    if (ix->h_bounds) cudaFreeHost(ix->h_bounds);
     for (auto& e : ix->ev)
         if (e) cudaEventDestroy(e);
     if (ix->stream) cudaStreamDestroy(ix->stream);

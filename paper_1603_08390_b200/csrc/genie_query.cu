@@ -2926,6 +2926,37 @@ static void segmented_sort_rows(genie_index* ix, uint32_t Q, uint32_t stride, ge
         out, out_len, stride, Q, db.Current(), id_offset);
 }
 
+uint64_t prepare_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, uint32_t total_items, uint32_t max_k,
+                       uint32_t out_stride, cudaStream_t s) {
+    uint32_t tile_bits_w[3];
+    class_tile_bits(ix, cfg, tile_bits_of(cfg), tile_bits_w);
+    reserve_workspace(ix, Q, total_items, max_k, out_stride,
+                      std::min({tile_bits_w[0] * 4, tile_bits_w[1] * 2, tile_bits_w[2]}));
+    ensure_keycuts(ix, tile_bits_w, s);
+    // signature of every device buffer and capacity the batch will use
+    const Workspace& w = ix->ws;
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    auto mixin = [&h](uint64_t v) { h = mix64(h ^ v); };
+    for (const void* ptr : {(const void*)w.q_bound.p, (const void*)w.q_P.p, (const void*)w.q_span_base.p,
+                            (const void*)w.q_cut_base.p, (const void*)w.q_out_base.p, (const void*)w.q_S.p,
+                            (const void*)w.q_W.p, (const void*)w.q_ntiles.p, (const void*)w.q_cap.p,
+                            (const void*)w.q_tile_base.p, (const void*)w.q_rank.p, (const void*)w.q_big.p,
+                            (const void*)w.q_floor.p, (const void*)w.q_plan.p, (const void*)w.it_kb.p,
+                            (const void*)w.it_nk.p, (const void*)w.it_sbase.p, (const void*)w.span_beg.p,
+                            (const void*)w.span_dense.p, (const void*)w.cuts.p, (const void*)w.work_q.p,
+                            (const void*)w.work_t.p, (const void*)w.tile_len.p, (const void*)w.tile_rec.p,
+                            (const void*)w.tile_out.p, (const void*)w.status.p, (const void*)w.d_qid.p,
+                            (const void*)w.d_k.p, (const void*)w.d_item_off.p, (const void*)w.d_dim.p,
+                            (const void*)w.d_lo.p, (const void*)w.d_hi.p, (const void*)w.d_out.p,
+                            (const void*)w.d_out_len.p, (const void*)w.d_out_thr.p, (const void*)ix->keycut[0].p,
+                            (const void*)ix->keycut[1].p, (const void*)ix->keycut[2].p})
+        mixin(reinterpret_cast<uint64_t>(ptr));
+    for (uint64_t v : {uint64_t(w.cap_spans), uint64_t(w.cap_cuts), uint64_t(w.cap_work), uint64_t(w.cap_tout),
+                       uint64_t(ix->keycut_T[0]), uint64_t(ix->keycut_T[1]), uint64_t(ix->keycut_T[2])})
+        mixin(v);
+    return h;
+}
+
 void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const uint32_t* d_qid,
                   const uint32_t* d_k, const uint64_t* d_item_off, const uint16_t* d_dim,
                   const uint32_t* d_lo, const uint32_t* d_hi, uint32_t total_items,
@@ -3049,9 +3080,12 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     // stage events are recorded as external event nodes when captured, so a
     // replayed graph still records them (cudaEventRecordExternal)
     auto enqueue = [&](bool capturing) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (!capturing) GENIE_CUDA(cudaStreamIsCapturing(s, &cs));  // an enclosing capture (host-buffer graphs)
+        const bool external = capturing || cs == cudaStreamCaptureStatusActive;
         auto record = [&](int e) {
-            GENIE_CUDA(capturing ? cudaEventRecordWithFlags(ix->ev[e], s, cudaEventRecordExternal)
-                                 : cudaEventRecord(ix->ev[e], s));
+            GENIE_CUDA(external ? cudaEventRecordWithFlags(ix->ev[e], s, cudaEventRecordExternal)
+                                : cudaEventRecord(ix->ev[e], s));
         };
         if (timed) record(0);
         k_init_status<<<1, 64, 0, s>>>(w.status.p);

@@ -243,6 +243,12 @@ struct genie_index {
     bool last_timed = false;
     genie_config last_cfg{};
     std::shared_ptr<void> graph;  // captured batch pipeline (GENIE_FLAG_GRAPH), genie_query.cu
+    // captured host-buffer batch (genie_query_batch with GENIE_FLAG_GRAPH): H2D, pipeline, D2H
+    cudaGraphExec_t host_graph = nullptr;
+    uint64_t host_graph_key[16] = {};
+    uint64_t host_graph_captures = 0;
+    uint64_t* h_bounds = nullptr;  // pinned staging of the per-query bounds (graph path)
+    uint32_t h_bounds_cap = 0;
 };
 
 namespace genie {
@@ -262,6 +268,12 @@ void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entr
                        uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
                        uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s, bool list_major);
 
+// Host-side set-up of a batch (tile sizes, workspace, cut tables) without any
+// stream work, so the launch that follows can be captured; returns a digest of
+// every device buffer / capacity the batch will use (a graph key).
+uint64_t prepare_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, uint32_t total_items, uint32_t max_k,
+                       uint32_t out_stride, cudaStream_t s);
+
 // Reads the status block (synchronises) and converts it to a status code +
 // message.  Grows the workspace and returns GENIE_RETRY on overflow.
 int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
@@ -280,6 +292,15 @@ inline void validate_config(const genie_config& c) {
     if (c.span_chunk == 0 || c.max_spans_per_task == 0)
         throw Error(GENIE_ERR_CONTRACT, "span_chunk and max_spans_per_task must be positive");
     if (c.selector > GENIE_SELECT_SORT) throw Error(GENIE_ERR_CONTRACT, "unknown selector");
+}
+
+// The O(Q) part of the checks (sizes): the per-item / per-query contract
+// checks run on the device (k_resolve) and, only when it reports a bad
+// input, validate_queries re-derives the reference's exact message.
+inline void validate_offsets(uint32_t Q, const uint64_t* item_off) {
+    if (Q >= (1u << 21)) throw Error(GENIE_ERR_CONTRACT, "batch exceeds 2^21 queries");
+    for (uint32_t q = 0; q < Q; ++q)
+        if (item_off[q + 1] < item_off[q]) throw Error(GENIE_ERR_CONTRACT, "item_off must be non-decreasing");
 }
 
 inline void validate_queries(uint32_t Q, const uint32_t* qid, const uint32_t* k,
