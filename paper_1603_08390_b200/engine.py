@@ -327,10 +327,9 @@ class DeviceIndex:
         err = _errbuf()
         cfg = cfg if cfg is not None else config()
         rc = self._lib.genie_query_batch(
-            self._h, C.byref(cfg), Q, _ptr(batch.qid, C.c_uint32), _ptr(batch.k, C.c_uint32),
-            _ptr(batch.item_off, C.c_uint64), _ptr(batch.dim, C.c_uint16), _ptr(batch.lo, C.c_uint32),
-            _ptr(batch.hi, C.c_uint32), stride, ent.ctypes.data_as(C.POINTER(N.Entry)), _ptr(ln, C.c_uint32),
-            _ptr(thr, C.c_uint32), None if bound is None else _ptr(bound, C.c_uint64),
+            self._h, C.byref(cfg), Q, batch.qid.ctypes.data, batch.k.ctypes.data, batch.item_off.ctypes.data,
+            batch.dim.ctypes.data, batch.lo.ctypes.data, batch.hi.ctypes.data, stride, ent.ctypes.data,
+            ln.ctypes.data, thr.ctypes.data, None if bound is None else bound.ctypes.data,
             C.byref(st) if timings else None, C.byref(stats), err, len(err))
         check(rc, err)
         tdict = {f: getattr(st, f) for f, _ in N.StageNs._fields_} if timings else None
@@ -618,7 +617,7 @@ class Encoder:
         host points (or sets) in, results out; the tokens stay on the device."""
         if points is not None:
             pts = np.ascontiguousarray(points, np.float32)
-            n, pp, so, el = pts.shape[0], _ptr(pts, C.c_float), None, None
+            n, pp, so, el = pts.shape[0], pts.ctypes.data, None, None
         else:
             so = np.ascontiguousarray(set_off, np.uint64)
             el = np.ascontiguousarray(elems, np.uint64)
@@ -632,10 +631,9 @@ class Encoder:
         stats, err = N.BatchStats(), _errbuf()
         cfg = cfg if cfg is not None else config()
         check(self._lib.genie_lsh_query_batch(
-            self._h, index.handle, C.byref(cfg), pp, None if so is None else _ptr(so, C.c_uint64),
-            None if el is None else _ptr(el, C.c_uint64), Q, k, first_id, stride,
-            ent.ctypes.data_as(C.POINTER(N.Entry)), _ptr(ln, C.c_uint32), _ptr(thr, C.c_uint32), C.byref(stats), err,
-            len(err)), err)
+            self._h, index.handle, C.byref(cfg), pp, None if so is None else so.ctypes.data,
+            None if el is None else el.ctypes.data, Q, k, first_id, stride, ent.ctypes.data, ln.ctypes.data,
+            thr.ctypes.data, C.byref(stats), err, len(err)), err)
         qid = np.arange(first_id, first_id + Q, dtype=np.uint32)
         sdict = {f: getattr(stats, f) for f, _ in N.BatchStats._fields_}
         if not copy:
