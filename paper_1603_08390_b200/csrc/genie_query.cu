@@ -948,318 +948,251 @@ __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32
 
 // Dense phase (interleaved layout): every thread owns whole 32-object blocks
 // and initialises their counters as the sum of the query's dense bitmaps
-// (plain 16-byte stores, no atomics, no zeroing pass).  Few lists: each adds
-// its bits lane by lane (W shift-and-mask-adds per 32 objects).  Many lists
-// (nd >= 2W): bit-sliced counting -- a Harley-Seal tree of carry-save adders
-// folds 8 bitmaps at a time into bit planes of the count (about 3 logic ops
-// per list per 32 objects), transposed into counters once per block.  With
-// the gate on it also counts, in registers, the objects reaching each level
-// v in [at0, at0 + kLvl) (Swar::ge + popc), for the c-PQ catch-up below.
+// (plain 16-byte stores, no atomics, no zeroing pass).  The bitmaps of a
+// block are first summed into bit planes of the count (plane i = bit i of
+// every object's count): up to three lists by a full adder lane by lane
+// (dense_lanes); more by carry-save adders, a Harley-Seal tree over 8 lists
+// at a time (dense_planes).  The planes become counter words through a
+// masked-swap transpose (planes_to_words).  With the gate on, the same
+// planes count, in registers, the objects reaching each level v in
+// [at0, at0 + kLvl) for the c-PQ catch-up (dense_gate).
+
+__host__ __device__ constexpr uint32_t swap_mask(int s) {
+    return s == 0 ? 0x55555555u : (s == 1 ? 0x33333333u : (s == 2 ? 0x0f0f0f0fu : 0x00ff00ffu));
+}
+
+// Bit b of plane i (bit i of the count of object b of a 32-object block) ->
+// field j of word m (the counter of object j * W + m: the interleaved
+// layout).  log2(W) levels of masked swaps between words 2^s apart; a pair
+// costs two shifts and two LOP3s, and planes known to be zero (i >= NP) fold.
+template <int W, int NP>
+__device__ __forceinline__ void planes_to_words(const uint32_t (&P)[NP], uint32_t (&X)[W]) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) X[i] = i < NP ? P[i < NP ? i : 0] : 0u;
+#pragma unroll
+    for (int s = 0; (1 << s) < W; ++s) {
+        const int f = 1 << s;
+        const uint32_t m = swap_mask(s);
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (i & f) continue;
+            const uint32_t a = X[i], b = X[i + f];
+            X[i] = (a & m) | ((b << f) & ~m);
+            X[i + f] = ((a >> f) & m) | (b & ~m);
+        }
+    }
+}
+
+// objects of the block whose count (NP planes) is >= v
+template <int NP>
+__device__ __forceinline__ uint32_t planes_ge(const uint32_t (&P)[NP], uint32_t v) {
+    if (v >> NP) return 0u;
+    uint32_t ge = 0, eq = 0xffffffffu;
+#pragma unroll
+    for (int i = NP - 1; i >= 0; --i) {
+        if ((v >> i) & 1u) {
+            eq &= P[i];
+        } else {
+            ge |= eq & P[i];
+            eq &= ~P[i];
+        }
+    }
+    return ge | eq;
+}
+
+// adds c (weight 2^i0) into planes i0.. (ripple carry; a carry out of the top
+// plane cannot happen: counts stay below 2^NP)
+template <int NP>
+__device__ __forceinline__ void plane_add(uint32_t (&P)[NP], uint32_t c, int i0) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        if (i < i0) continue;
+        const uint32_t t = P[i] & c;
+        P[i] ^= c;
+        c = t;
+    }
+}
+
+template <int G>
+__device__ __forceinline__ void ldg_words(const uint32_t* src, uint32_t (&x)[G]) {
+    if constexpr (G == 1) {
+        x[0] = __ldg(src);
+    } else if constexpr (G == 2) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+        x[0] = v.x;
+        x[1] = v.y;
+    } else {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
+        x[0] = v.x;
+        x[1] = v.y;
+        x[2] = v.z;
+        x[3] = v.w;
+    }
+}
+
+template <int W>
+__device__ __forceinline__ void store_block(const ScanSmem& sm, uint32_t blk, const uint32_t (&acc)[W]) {
+    uint4* dst = reinterpret_cast<uint4*>(sm.cnt + blk * W);
+#pragma unroll
+    for (int j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+}
+
+// Many lists (nd > 3, W <= 8): G consecutive blocks per thread (one G-word
+// bitmap load per list), NP planes (NP = W, or fewer when nd < 2^NP).
+template <int W, int NP, int G>
+__device__ __forceinline__ void dense_planes(const BatchParams& p, const ScanSmem& sm, const StageBuf& sb,
+                                             uint32_t bw0, uint32_t nblk, uint32_t nd, uint32_t at0, uint32_t nlv,
+                                             uint32_t (&lv)[kLvl]) {
+    const uint32_t* dslot = sb.dense();
+    for (uint32_t blk = G * threadIdx.x; blk < nblk; blk += G * blockDim.x) {
+        const uint32_t* col = p.bitmaps + bw0 + blk;
+        uint32_t P[G][NP];
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+#pragma unroll
+            for (int i = 0; i < NP; ++i) P[h][i] = 0;
+        uint32_t d = 0;
+        if constexpr (NP >= 4) {
+            for (; d + 8 <= nd; d += 8) {
+                uint32_t a[8][G];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) ldg_words<G>(col + size_t(dslot[d + u]) * p.bitmap_words, a[u]);
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    uint32_t twosA, twosB, foursA, foursB, eights;
+                    csa(twosA, P[h][0], P[h][0], a[0][h], a[1][h]);
+                    csa(twosB, P[h][0], P[h][0], a[2][h], a[3][h]);
+                    csa(foursA, P[h][1], P[h][1], twosA, twosB);
+                    csa(twosA, P[h][0], P[h][0], a[4][h], a[5][h]);
+                    csa(twosB, P[h][0], P[h][0], a[6][h], a[7][h]);
+                    csa(foursB, P[h][1], P[h][1], twosA, twosB);
+                    csa(eights, P[h][2], P[h][2], foursA, foursB);
+                    plane_add<NP>(P[h], eights, 3);  // weight 8
+                }
+            }
+        }
+        if constexpr (NP >= 3) {
+            for (; d + 4 <= nd; d += 4) {
+                uint32_t a[4][G];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ldg_words<G>(col + size_t(dslot[d + u]) * p.bitmap_words, a[u]);
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    uint32_t twosA, twosB, fours;
+                    csa(twosA, P[h][0], P[h][0], a[0][h], a[1][h]);
+                    csa(twosB, P[h][0], P[h][0], a[2][h], a[3][h]);
+                    csa(fours, P[h][1], P[h][1], twosA, twosB);
+                    plane_add<NP>(P[h], fours, 2);  // weight 4
+                }
+            }
+        }
+        for (; d < nd; ++d) {
+            uint32_t a[G];
+            ldg_words<G>(col + size_t(dslot[d]) * p.bitmap_words, a);
+#pragma unroll
+            for (int h = 0; h < G; ++h) plane_add<NP>(P[h], a[h], 0);
+        }
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            if (blk + h >= nblk) break;
+            if (nlv) {
+#pragma unroll
+                for (uint32_t l = 0; l < kLvl; ++l)
+                    if (l < nlv) lv[l] += __popc(planes_ge<NP>(P[h], at0 + l));
+            }
+            uint32_t acc[W];
+            planes_to_words<W, NP>(P[h], acc);
+            store_block<W>(sm, blk + h, acc);
+        }
+    }
+}
+
+// One to three lists (most C2 items): lane-wise, a warp step covers 32 * BPT
+// consecutive blocks and lane l owns blocks base + 32 i (i < BPT), so every
+// bitmap load (one word per lane) and every 16-byte counter store of the warp
+// is contiguous.  Two planes: the lists' sum (XOR) and carry (majority); the
+// level counts are OR (>= 1), the carry (>= 2) and AND (>= 3).
+template <int W, int ND>
+__device__ __forceinline__ void dense_lanes(const BatchParams& p, const ScanSmem& sm, const StageBuf& sb,
+                                            uint32_t bw0, uint32_t nblk, uint32_t at0, uint32_t nlv,
+                                            uint32_t (&lv)[kLvl]) {
+    constexpr uint32_t BPT = W == 4 ? 4 : (W == 8 ? 2 : 1);
+    constexpr int NP = ND == 1 ? 1 : 2;
+    const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const uint32_t* rows[ND];
+#pragma unroll
+    for (int u = 0; u < ND; ++u) rows[u] = p.bitmaps + bw0 + lane + size_t(sb.dense()[u]) * p.bitmap_words;
+    for (uint32_t wt = threadIdx.x >> 5; wt * 32 * BPT < nblk; wt += nwarps) {
+        const uint32_t base = wt * 32 * BPT + lane;
+        const bool full = (wt + 1) * 32 * BPT <= nblk;
+        uint32_t b[ND][BPT];
+#pragma unroll
+        for (int u = 0; u < ND; ++u)
+#pragma unroll
+            for (uint32_t i = 0; i < BPT; ++i)
+                b[u][i] = (full || base + 32 * i < nblk) ? __ldg(rows[u] + wt * 32 * BPT + 32 * i) : 0u;
+#pragma unroll
+        for (uint32_t i = 0; i < BPT; ++i) {
+            uint32_t P[NP];
+            uint32_t ge1, ge3 = 0;
+            if constexpr (ND == 1) {
+                P[0] = ge1 = b[0][i];
+            } else if constexpr (ND == 2) {
+                P[0] = b[0][i] ^ b[1][i];
+                P[1] = b[0][i] & b[1][i];
+                ge1 = b[0][i] | b[1][i];
+            } else {
+                const uint32_t x = b[0][i], y = b[1][i], z = b[2][i];
+                P[0] = x ^ y ^ z;
+                P[1] = (x & y) | (x & z) | (y & z);
+                ge1 = x | y | z;
+                ge3 = x & y & z;
+            }
+            if (full || base + 32 * i < nblk) {
+                uint32_t acc[W];
+                planes_to_words<W, NP>(P, acc);
+                store_block<W>(sm, base + 32 * i, acc);
+            }
+            if (nlv) {
+                const uint32_t ge2 = NP > 1 ? P[NP - 1] : 0u;
+#pragma unroll
+                for (uint32_t l = 0; l < kLvl; ++l) {
+                    if (l < nlv) {
+                        const uint32_t v = at0 + l;
+                        lv[l] += __popc(v == 1 ? ge1 : (v == 2 ? ge2 : (v == 3 ? ge3 : 0u)));
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <int W>
 GENIE_DENSE_FN uint32_t dense_init(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, const StageBuf& sb,
                                uint32_t nd, uint32_t at0, uint32_t nlv, bool& csa_path, long long* t_work = nullptr) {
     using Sw = Swar<W>;
-    constexpr uint32_t BPT = W == 4 ? 4 : (W == 8 ? 2 : 1);  // blocks per thread step (16 words)
+    constexpr uint32_t BPT = W == 4 ? 4 : (W == 8 ? 2 : 1);  // blocks per lane per warp step
     constexpr uint32_t NW = BPT * W;
     const uint32_t bw0 = it.tile_lo >> 5;
     const uint32_t nblk = it.words / W;
     uint32_t lv[kLvl] = {};
     csa_path = false;
     if constexpr (W <= 8) {
-        if (nd >= 2 * W) {
+        if (nd > 3) {
             csa_path = true;
-#if GENIE_CSA_QUAD
-          if constexpr (W == 8) {
-            // four consecutive blocks per thread: one 16-byte bitmap load per list
-            const uint32_t bwq = p.bitmap_words / 4;
-            for (uint32_t blk = 4 * threadIdx.x; blk < nblk; blk += 4 * blockDim.x) {
-                const uint4* col = reinterpret_cast<const uint4*>(p.bitmaps + bw0 + blk);
-                uint32_t P[4][W];
-#pragma unroll
-                for (int i = 0; i < W; ++i) P[0][i] = P[1][i] = P[2][i] = P[3][i] = 0;
-                uint32_t d = 0;
-                for (; d + 4 <= nd; d += 4) {
-                    uint4 a[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) a[u] = __ldg(col + size_t(sb.dense()[d + u]) * bwq);
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        uint32_t x[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) x[u] = h == 0 ? a[u].x : (h == 1 ? a[u].y : (h == 2 ? a[u].z : a[u].w));
-                        uint32_t twosA, twosB, fours;
-                        csa(twosA, P[h][0], P[h][0], x[0], x[1]);
-                        csa(twosB, P[h][0], P[h][0], x[2], x[3]);
-                        csa(fours, P[h][1], P[h][1], twosA, twosB);
-                        uint32_t c = fours;
-#pragma unroll
-                        for (int i = 2; i < W; ++i) {
-                            const uint32_t t = P[h][i] & c;
-                            P[h][i] ^= c;
-                            c = t;
-                        }
-                    }
-                }
-                for (; d < nd; ++d) {
-                    const uint4 a = __ldg(col + size_t(sb.dense()[d]) * bwq);
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        uint32_t c = h == 0 ? a.x : (h == 1 ? a.y : (h == 2 ? a.z : a.w));
-#pragma unroll
-                        for (int i = 0; i < W; ++i) {
-                            const uint32_t t = P[h][i] & c;
-                            P[h][i] ^= c;
-                            c = t;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    if (blk + h >= nblk) break;
-                    if (nlv) {
-#pragma unroll
-                        for (uint32_t l = 0; l < kLvl; ++l) {
-                            if (l < nlv) {
-                                const uint32_t v = at0 + l;
-                                uint32_t ge = 0, eq = 0xffffffffu;
-#pragma unroll
-                                for (int i = W - 1; i >= 0; --i) {
-                                    if ((v >> i) & 1u) {
-                                        eq &= P[h][i];
-                                    } else {
-                                        ge |= eq & P[h][i];
-                                        eq &= ~P[h][i];
-                                    }
-                                }
-                                lv[l] += __popc(ge | eq);
-                            }
-                        }
-                    }
-                    uint32_t acc[W];
-#pragma unroll
-                    for (int m = 0; m < W; ++m) {
-                        uint32_t x = 0;
-#pragma unroll
-                        for (int i = 0; i < W; ++i) x |= ((P[h][i] >> m) & Sw::kOnes) << i;
-                        acc[m] = x;
-                    }
-                    uint4* dst = reinterpret_cast<uint4*>(sm.cnt + (blk + h) * W);
-#pragma unroll
-                    for (int j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-                }
-            }
-          } else
-#elif GENIE_CSA_PAIR
-          if constexpr (W == 8) {
-            // two consecutive blocks per thread: one 8-byte bitmap load per list
-            const uint32_t bwq = p.bitmap_words / 2;
-            for (uint32_t blk = 2 * threadIdx.x; blk < nblk; blk += 2 * blockDim.x) {
-                const uint2* col = reinterpret_cast<const uint2*>(p.bitmaps + bw0 + blk);
-                uint32_t P[2][W];
-#pragma unroll
-                for (int i = 0; i < W; ++i) P[0][i] = P[1][i] = 0;
-                uint32_t d = 0;
-                for (; d + 8 <= nd; d += 8) {
-                    uint2 a[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) a[u] = __ldg(col + size_t(sb.dense()[d + u]) * bwq);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t x[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) x[u] = h ? a[u].y : a[u].x;
-                        uint32_t twosA, twosB, foursA, foursB, eights;
-                        csa(twosA, P[h][0], P[h][0], x[0], x[1]);
-                        csa(twosB, P[h][0], P[h][0], x[2], x[3]);
-                        csa(foursA, P[h][1], P[h][1], twosA, twosB);
-                        csa(twosA, P[h][0], P[h][0], x[4], x[5]);
-                        csa(twosB, P[h][0], P[h][0], x[6], x[7]);
-                        csa(foursB, P[h][1], P[h][1], twosA, twosB);
-                        csa(eights, P[h][2], P[h][2], foursA, foursB);
-                        uint32_t c = eights;
-#pragma unroll
-                        for (int i = 3; i < W; ++i) {
-                            const uint32_t t = P[h][i] & c;
-                            P[h][i] ^= c;
-                            c = t;
-                        }
-                    }
-                }
-                for (; d < nd; ++d) {
-                    const uint2 a = __ldg(col + size_t(sb.dense()[d]) * bwq);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t c = h ? a.y : a.x;
-#pragma unroll
-                        for (int i = 0; i < W; ++i) {
-                            const uint32_t t = P[h][i] & c;
-                            P[h][i] ^= c;
-                            c = t;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (blk + h >= nblk) break;
-                    if (nlv) {
-#pragma unroll
-                        for (uint32_t l = 0; l < kLvl; ++l) {
-                            if (l < nlv) {
-                                const uint32_t v = at0 + l;
-                                uint32_t ge = 0, eq = 0xffffffffu;
-#pragma unroll
-                                for (int i = W - 1; i >= 0; --i) {
-                                    if ((v >> i) & 1u) {
-                                        eq &= P[h][i];
-                                    } else {
-                                        ge |= eq & P[h][i];
-                                        eq &= ~P[h][i];
-                                    }
-                                }
-                                lv[l] += __popc(ge | eq);
-                            }
-                        }
-                    }
-                    uint32_t acc[W];
-#pragma unroll
-                    for (int m = 0; m < W; ++m) {
-                        uint32_t x = 0;
-#pragma unroll
-                        for (int i = 0; i < W; ++i) x |= ((P[h][i] >> m) & Sw::kOnes) << i;
-                        acc[m] = x;
-                    }
-                    uint4* dst = reinterpret_cast<uint4*>(sm.cnt + (blk + h) * W);
-#pragma unroll
-                    for (int j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-                }
-            }
-          } else
-#endif
-            for (uint32_t blk = threadIdx.x; blk < nblk; blk += blockDim.x) {
-                const uint32_t* col = p.bitmaps + bw0 + blk;
-                uint32_t P[W];  // bit planes of the dense count (< 2^W: it is at most the bound)
-#pragma unroll
-                for (int i = 0; i < W; ++i) P[i] = 0;
-                uint32_t d = 0;
-                for (; d + 8 <= nd; d += 8) {
-                    uint32_t a[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) a[u] = __ldg(col + size_t(sb.dense()[d + u]) * p.bitmap_words);
-                    uint32_t twosA, twosB, foursA, foursB, eights;
-                    csa(twosA, P[0], P[0], a[0], a[1]);
-                    csa(twosB, P[0], P[0], a[2], a[3]);
-                    csa(foursA, P[1], P[1], twosA, twosB);
-                    csa(twosA, P[0], P[0], a[4], a[5]);
-                    csa(twosB, P[0], P[0], a[6], a[7]);
-                    csa(foursB, P[1], P[1], twosA, twosB);
-                    csa(eights, P[2], P[2], foursA, foursB);
-                    uint32_t c = eights;  // weight 8: ripple into the planes above
-#pragma unroll
-                    for (int i = 3; i < W; ++i) {
-                        const uint32_t t = P[i] & c;
-                        P[i] ^= c;
-                        c = t;
-                    }
-                }
-                for (; d < nd; ++d) {
-                    uint32_t c = __ldg(col + size_t(sb.dense()[d]) * p.bitmap_words);
-#pragma unroll
-                    for (int i = 0; i < W; ++i) {
-                        const uint32_t t = P[i] & c;
-                        P[i] ^= c;
-                        c = t;
-                    }
-                }
-                if (nlv) {  // objects of the block counting >= v: comparator on the planes
-#pragma unroll
-                    for (uint32_t l = 0; l < kLvl; ++l) {
-                        if (l < nlv) {
-                            const uint32_t v = at0 + l;
-                            uint32_t ge = 0, eq = 0xffffffffu;
-#pragma unroll
-                            for (int i = W - 1; i >= 0; --i) {
-                                if ((v >> i) & 1u) {
-                                    eq &= P[i];
-                                } else {
-                                    ge |= eq & P[i];
-                                    eq &= ~P[i];
-                                }
-                            }
-                            lv[l] += __popc(ge | eq);
-                        }
-                    }
-                }
-                // planes -> interleaved counters: word m, lane l holds object l * W + m
-                uint32_t acc[W];
-#pragma unroll
-                for (int m = 0; m < W; ++m) {
-                    uint32_t x = 0;
-#pragma unroll
-                    for (int i = 0; i < W; ++i) x |= ((P[i] >> m) & Sw::kOnes) << i;
-                    acc[m] = x;
-                }
-                uint4* dst = reinterpret_cast<uint4*>(sm.cnt + blk * W);
-#pragma unroll
-                for (int j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-            }
-            nd = 0;  // done: skip the lane-wise path
+            constexpr int G = W == 8 ? (GENIE_CSA_QUAD ? 4 : (GENIE_CSA_PAIR ? 2 : 1)) : 1;
+            if (nd >= 2 * W) dense_planes<W, W, G>(p, sm, sb, bw0, nblk, nd, at0, nlv, lv);
+            else dense_planes<W, W == 4 ? 3 : 4, G>(p, sm, sb, bw0, nblk, nd, at0, nlv, lv);
+            nd = 0;
         }
     }
-    // Lane-wise path: a warp step covers 32 * BPT consecutive blocks; lane l
-    // owns blocks base + 32 j (j < BPT), so every bitmap load (one word per
-    // lane) and every 16-byte counter store of the warp is contiguous.
+    if (nd == 1) dense_lanes<W, 1>(p, sm, sb, bw0, nblk, at0, nlv, lv);
+    else if (nd == 2) dense_lanes<W, 2>(p, sm, sb, bw0, nblk, at0, nlv, lv);
+    else if (nd == 3) dense_lanes<W, 3>(p, sm, sb, bw0, nblk, at0, nlv, lv);
+    if (nd <= 3) nd = 0;
+    // W = 16 with more than three lists: per-lane adds (counts < 2^15, no carries)
+    if constexpr (W > 8) {
     const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    if (nd && nd <= 3) {
-        // up to three lists (most C2 items): a full adder turns the bitmap
-        // words x, y, z into the two bit planes of the count (sum, carry),
-        // spread into the counter words once; the level counts come from the
-        // same words (count >= 1, 2, 3 is OR, majority, AND)
-        const uint32_t* rows[3];
-#pragma unroll
-        for (uint32_t u = 0; u < 3; ++u) rows[u] = p.bitmaps + bw0 + lane + size_t(sb.dense()[u < nd ? u : 0]) * p.bitmap_words;
-        for (uint32_t wt = threadIdx.x >> 5; wt * 32 * BPT < nblk; wt += nwarps) {
-            const uint32_t base = wt * 32 * BPT + lane;
-            const bool full = (wt + 1) * 32 * BPT <= nblk;
-            uint32_t b[3][BPT];
-#pragma unroll
-            for (uint32_t u = 0; u < 3; ++u) {
-                const uint32_t* src = rows[u] + wt * 32 * BPT;
-#pragma unroll
-                for (uint32_t i = 0; i < BPT; ++i)
-                    b[u][i] = u < nd && (full || base + 32 * i < nblk) ? __ldg(src + 32 * i) : 0u;
-            }
-#pragma unroll
-            for (uint32_t i = 0; i < BPT; ++i) {
-                const uint32_t x = b[0][i], y = b[1][i], z = b[2][i];
-                const uint32_t s0 = x ^ y ^ z, s1 = (x & y) | (x & z) | (y & z);
-                if (full || base + 32 * i < nblk) {
-                    uint32_t acc[W];
-#pragma unroll
-                    for (uint32_t m = 0; m < W; ++m) {
-                        if constexpr (W <= 4) {
-                            acc[m] = ((s0 >> m) & Sw::kOnes) | (((s1 >> m) & Sw::kOnes) << 1);
-                        } else {
-                            acc[m] = ((s0 >> m) & Sw::kOnes) + (((s1 >> m) & Sw::kOnes) << 1);
-                        }
-                    }
-                    uint4* dst = reinterpret_cast<uint4*>(sm.cnt + (base + 32 * i) * W);
-#pragma unroll
-                    for (uint32_t j = 0; j < W; j += 4) dst[j / 4] = make_uint4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-                }
-                if (nlv) {
-                    const uint32_t ge1 = x | y | z, ge3 = x & y & z;
-#pragma unroll
-                    for (uint32_t l = 0; l < kLvl; ++l) {
-                        if (l < nlv) {
-                            const uint32_t v = at0 + l;
-                            lv[l] += __popc(v == 1 ? ge1 : (v == 2 ? s1 : (v == 3 ? ge3 : 0u)));
-                        }
-                    }
-                }
-            }
-        }
-        nd = 0;  // done: skip the general lane-wise path
-    }
     for (uint32_t wt = threadIdx.x >> 5; nd && wt * 32 * BPT < nblk; wt += nwarps) {
         const uint32_t base = wt * 32 * BPT + lane;
         uint32_t acc[NW];
@@ -1311,6 +1244,7 @@ GENIE_DENSE_FN uint32_t dense_init(const BatchParams& p, const ItemCtx& it, cons
                 }
             }
         }
+    }
     }
     uint32_t reach = 0;  // levels at0 + l (l < reach) that some object of this thread's blocks reaches
 #pragma unroll
