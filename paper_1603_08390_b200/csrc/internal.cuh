@@ -107,6 +107,15 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #ifndef GENIE_SPAN_PREFETCH  // L2 prefetch of the next item's posting slices: 0 off, 1 bulk (UBLKPF), 2 per-lane lines
 #define GENIE_SPAN_PREFETCH 2
 #endif
+#ifndef GENIE_STATIC_GROUPS  // <= this many 128-posting groups per scan warp: static split, else guided
+#define GENIE_STATIC_GROUPS 64
+#endif
+#ifndef GENIE_PLANES_LOP  // many-list dense path: transpose through explicit LOP3 selects
+#define GENIE_PLANES_LOP 1
+#endif
+#ifndef GENIE_LANES_LV_SPLIT  // few-list dense path: separate code for items without gate levels (W = 4 / W >= 8)
+#define GENIE_LANES_LV_SPLIT 1
+#endif
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
 #endif
@@ -114,7 +123,8 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #define GENIE_CSA_PAIR 1
 #endif
 constexpr int kScanUnroll = GENIE_SCAN_UNROLL;               // 128-posting groups loaded per warp pass
-constexpr uint32_t kStaticGroups = 64;        // <= this many 128-posting groups per warp: static split
+constexpr bool kLanesLvSplit = GENIE_LANES_LV_SPLIT;
+constexpr uint32_t kStaticGroups = GENIE_STATIC_GROUPS;        // <= this many 128-posting groups per warp: static split
 constexpr uint64_t kEmptySlot = ~0ull;
 constexpr int kMaxDevices = 64;              // per-device host caches (launch attributes)
 
