@@ -211,17 +211,28 @@ void build_dense_containers(genie_index* ix, const uint64_t* h_off) {
         }
     }
     const double dens = dense_density(ix);
+    ix->bitmap_words = ((ix->n + 31) / 32 + 3) & ~3u;  // 16-byte rows
+    // key_dense[j]: word offset of key j's bitmap row in `bitmaps`, or -1.
+    // k_scan adds it to a per-thread pointer as a 32-bit index (one IMAD per
+    // row load), so the rows span at most 2^31 words (8 GB): beyond that the
+    // longest lists keep their bitmaps and the rest stay posting lists.
     std::vector<int32_t> slot(ix->K, -1);
     std::vector<uint64_t> dense_keys;
     if (dens > 0.0 && ix->n >= 1024) {
         for (uint64_t j = 0; j < ix->K; ++j)
-            if (double(h_off[j + 1] - h_off[j]) >= dens * double(ix->n)) {
-                slot[j] = static_cast<int32_t>(dense_keys.size());
-                dense_keys.push_back(j);
-            }
+            if (double(h_off[j + 1] - h_off[j]) >= dens * double(ix->n)) dense_keys.push_back(j);
+        const uint64_t max_rows = ((1ull << 31) - 1) / ix->bitmap_words;
+        if (dense_keys.size() > max_rows) {
+            std::stable_sort(dense_keys.begin(), dense_keys.end(), [&](uint64_t a, uint64_t b) {
+                return h_off[a + 1] - h_off[a] > h_off[b + 1] - h_off[b];
+            });
+            dense_keys.resize(max_rows);
+            std::sort(dense_keys.begin(), dense_keys.end());
+        }
+        for (size_t d = 0; d < dense_keys.size(); ++d)
+            slot[dense_keys[d]] = static_cast<int32_t>(d * ix->bitmap_words);
     }
     ix->n_dense = static_cast<uint32_t>(dense_keys.size());
-    ix->bitmap_words = ((ix->n + 31) / 32 + 3) & ~3u;  // 16-byte rows
     ix->key_dense.reserve(ix->K + 1);
     if (ix->K)
         GENIE_CUDA(cudaMemcpy(ix->key_dense.p, slot.data(), ix->K * sizeof(int32_t), cudaMemcpyHostToDevice));

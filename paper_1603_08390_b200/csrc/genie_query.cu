@@ -55,7 +55,7 @@ struct BatchParams {
     const uint64_t* key_off;
     const uint32_t* postings;
     const uint32_t* dim_mult;
-    const int32_t* key_dense;  // [K] dense-container slot or -1
+    const int32_t* key_dense;  // [K] word offset of the key's bitmap row, or -1 (< 2^31 words)
     const DimRange* dim_range; // [65536] each dim's key range
     const uint32_t* tokmap;    // token maps of gapped dims (DimRange::map_*)
     const uint32_t* keycut[3]; // per width class: precomputed tile cuts of every key (or null)
@@ -85,7 +85,7 @@ struct BatchParams {
     uint32_t ht_slots;
     uint32_t *it_kb, *it_nk, *it_sbase;
     uint64_t* span_beg;
-    int32_t* span_dense;  // [spans] bitmap slot used for the span's list, or -1
+    int32_t* span_dense;  // [spans] word offset of the bitmap row used for the span's list, or -1
     uint32_t* cuts;
     uint32_t *work_q, *work_t;
     uint32_t* tile_len;
@@ -1068,7 +1068,7 @@ __device__ __forceinline__ void dense_planes(const BatchParams& p, const ScanSme
             for (; d + 8 <= nd; d += 8) {
                 uint32_t a[8][G];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) ldg_words<G>(col + size_t(dslot[d + u]) * p.bitmap_words, a[u]);
+                for (int u = 0; u < 8; ++u) ldg_words<G>(col + dslot[d + u], a[u]);
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
                     uint32_t twosA, twosB, foursA, foursB, eights;
@@ -1087,7 +1087,7 @@ __device__ __forceinline__ void dense_planes(const BatchParams& p, const ScanSme
             for (; d + 4 <= nd; d += 4) {
                 uint32_t a[4][G];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) ldg_words<G>(col + size_t(dslot[d + u]) * p.bitmap_words, a[u]);
+                for (int u = 0; u < 4; ++u) ldg_words<G>(col + dslot[d + u], a[u]);
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
                     uint32_t twosA, twosB, fours;
@@ -1100,7 +1100,7 @@ __device__ __forceinline__ void dense_planes(const BatchParams& p, const ScanSme
         }
         for (; d < nd; ++d) {
             uint32_t a[G];
-            ldg_words<G>(col + size_t(dslot[d]) * p.bitmap_words, a);
+            ldg_words<G>(col + dslot[d], a);
 #pragma unroll
             for (int h = 0; h < G; ++h) plane_add<NP>(P[h], a[h], 0);
         }
@@ -1184,7 +1184,7 @@ __device__ __forceinline__ void dense_lanes(const BatchParams& p, const ScanSmem
     uint32_t wt = threadIdx.x >> 5;
     const uint32_t* r[ND];
 #pragma unroll
-    for (int u = 0; u < ND; ++u) r[u] = p.bitmaps + bw0 + size_t(sb.dense()[u]) * p.bitmap_words + wt * STEP + lane;
+    for (int u = 0; u < ND; ++u) r[u] = p.bitmaps + bw0 + sb.dense()[u] + wt * STEP + lane;
     uint4* dst = reinterpret_cast<uint4*>(sm.cnt) + (wt * STEP + lane) * (W / 4);
     const uint32_t nfull = nblk / STEP;
     for (; wt < nfull; wt += nwarps) {
@@ -1239,7 +1239,7 @@ GENIE_DENSE_FN uint32_t dense_init(const BatchParams& p, const ItemCtx& it, cons
             uint32_t b[4][BPT];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint32_t* src = col + size_t(sb.dense()[d + u]) * p.bitmap_words;
+                const uint32_t* src = col + sb.dense()[d + u];
 #pragma unroll
                 for (uint32_t i = 0; i < BPT; ++i) b[u][i] = base + 32 * i < nblk ? __ldg(src + 32 * i) : 0u;
             }
@@ -1251,7 +1251,7 @@ GENIE_DENSE_FN uint32_t dense_init(const BatchParams& p, const ItemCtx& it, cons
                     for (uint32_t m = 0; m < W; ++m) acc[i * W + m] += (b[u][i] >> m) & Sw::kOnes;
         }
         for (; d < nd; ++d) {
-            const uint32_t* src = col + size_t(sb.dense()[d]) * p.bitmap_words;
+            const uint32_t* src = col + sb.dense()[d];
             uint32_t b[BPT];
 #pragma unroll
             for (uint32_t i = 0; i < BPT; ++i) b[i] = base + 32 * i < nblk ? __ldg(src + 32 * i) : 0u;
@@ -1724,7 +1724,7 @@ __device__ __forceinline__ uint32_t stage_warp_finish(const BatchParams& p, cons
                 const int o = __ffs(m) - 1;
                 m &= m - 1;
                 const uint32_t slot = __shfl_sync(0xffffffffu, static_cast<uint32_t>(dslot), o);
-                const char* row = reinterpret_cast<const char*>(p.bitmaps + size_t(slot) * p.bitmap_words + tile_word0);
+                const char* row = reinterpret_cast<const char*>(p.bitmaps + slot + tile_word0);
                 for (uint32_t off = lane * 128; off < tile_bytes; off += 32 * 128)
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(row + off));
             }

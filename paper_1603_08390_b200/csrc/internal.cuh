@@ -240,7 +240,7 @@ struct genie_index {
     bool class_seen[3] = {false, false, false};
     // dense containers: keys whose list covers >= dense_density of the
     // objects also carry a bitmap of n bits (Roaring-style bitmap container)
-    genie::DevBuf<int32_t> key_dense;   // [K] slot in `bitmaps` or -1
+    genie::DevBuf<int32_t> key_dense;   // [K] word offset of the key's row in `bitmaps`, or -1
     genie::DevBuf<uint32_t> bitmaps;    // [n_dense][bitmap_words]
     uint32_t n_dense = 0, bitmap_words = 0;
     uint32_t dense_inv[3] = {0, 0, 0};  // query-time density rule per counter width (W = 4, 8, 16)
