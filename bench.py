@@ -735,7 +735,7 @@ def main_genie(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator, SURVEY.md 8d)",
             "config": {"workload": WORKLOADS[args.workload], "n_objects": w.n, "queries": Q, "k": int(qb.max_k),
                        "selector": ["cpq", "bucket"][min(args.selector, 1)],
-                       "parallelism": f"object-id shards x{world} + NCCL all-gather merge" if world > 1 else "single GPU",
+                       "parallelism": (f"object-id shards x{world} + {args.dist_backend.upper()} all-gather merge" if world > 1 else "single GPU"),
                        "l2": "flushed between timed steps (256 MiB write)",
                        "postings_per_query_mean": round(postings / Q, 1),
                        "generate_s": round(w.gen_s, 2), "index_build_s": round(w.build_s, 2)},
