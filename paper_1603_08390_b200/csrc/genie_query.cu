@@ -995,6 +995,13 @@ __device__ __forceinline__ void planes_to_words(const uint32_t (&P)[NP], uint32_
     }
 }
 
+// consecutive 32-object blocks per thread in the many-list dense path (one
+// G-word bitmap load per list); dense_gate re-reads the same ownership
+template <int W>
+__host__ __device__ constexpr int csa_blocks() {
+    return W == 8 ? (GENIE_CSA_QUAD ? 4 : (GENIE_CSA_PAIR ? 2 : 1)) : (W == 4 ? GENIE_CSA_BLOCKS_W4 : 1);
+}
+
 // objects of the block whose count (NP planes) is >= v
 template <int NP>
 __device__ __forceinline__ uint32_t planes_ge(const uint32_t (&P)[NP], uint32_t v) {
@@ -1209,7 +1216,7 @@ GENIE_DENSE_FN uint32_t dense_init(const BatchParams& p, const ItemCtx& it, cons
     if constexpr (W <= 8) {
         if (nd > 3) {
             csa_path = true;
-            constexpr int G = W == 8 ? (GENIE_CSA_QUAD ? 4 : (GENIE_CSA_PAIR ? 2 : 1)) : 1;
+            constexpr int G = csa_blocks<W>();
             if (nd >= 2 * W) dense_planes<W, W, G>(p, sm, sb, bw0, nblk, nd, at0, nlv, lv);
             else dense_planes<W, W == 4 ? 3 : 4, G>(p, sm, sb, bw0, nblk, nd, at0, nlv, lv);
             nd = 0;
@@ -1339,8 +1346,8 @@ GENIE_DENSE_FN void dense_gate(const ItemCtx& it, const ScanSmem& sm, uint32_t a
         // blocks of this thread: csa path blk = tid + k * blockDim; lane-wise
         // path blk = (warp + k * nwarps) * 32 * BPT + lane + 32 i
         const uint32_t lane = threadIdx.x & 31;
-        constexpr uint32_t kGrp = GENIE_CSA_QUAD ? 4u : (GENIE_CSA_PAIR ? 2u : 1u);  // csa blocks per thread
-        const bool pair = kGrp > 1 && csa_path && W == 8;
+        constexpr uint32_t kGrp = csa_blocks<W>();  // csa blocks per thread
+        const bool pair = kGrp > 1 && csa_path;
         const uint32_t first = pair ? kGrp * threadIdx.x : (csa_path ? threadIdx.x : (threadIdx.x >> 5) * 32 * BPT + lane);
         const uint32_t stride = pair ? kGrp * blockDim.x : (csa_path ? blockDim.x : (blockDim.x >> 5) * 32 * BPT);
         const uint32_t per = pair ? kGrp : (csa_path ? 1u : BPT);

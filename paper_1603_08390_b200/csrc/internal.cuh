@@ -116,6 +116,9 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #ifndef GENIE_LANES_LV_SPLIT  // few-list dense path: separate code for items without gate levels (W = 4 / W >= 8)
 #define GENIE_LANES_LV_SPLIT 1
 #endif
+#ifndef GENIE_CSA_BLOCKS_W4  // W = 4 many-list dense path: blocks per thread
+#define GENIE_CSA_BLOCKS_W4 2
+#endif
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
 #endif
