@@ -119,6 +119,9 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #ifndef GENIE_CSA_BLOCKS_W4  // W = 4 many-list dense path: blocks per thread
 #define GENIE_CSA_BLOCKS_W4 2
 #endif
+#ifndef GENIE_LANES_MAX  // dense lists per item up to which the lane-wise path runs (W <= 8)
+#define GENIE_LANES_MAX 3
+#endif
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
 #endif
