@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -58,7 +59,7 @@ struct BatchParams {
     const int32_t* key_dense;  // [K] word offset of the key's bitmap row, or -1 (< 2^31 words)
     const DimRange* dim_range; // [65536] each dim's key range
     const uint32_t* tokmap;    // token maps of gapped dims (DimRange::map_*)
-    const uint32_t* keycut[3]; // per width class: precomputed tile cuts of every key (or null)
+    const uint32_t* keycut[kClasses]; // per work class: precomputed tile cuts of every key (or null)
     const uint32_t* bitmaps;   // [n_dense][bitmap_words]
     uint32_t bitmap_words, n_dense;
     uint32_t dense_inv[3];  // per width class W = 4, 8, 16: use a bitmap iff len * inv >= n (0: always)
@@ -74,7 +75,13 @@ struct BatchParams {
     const uint32_t* hi;
     // plan
     uint32_t tile_bits;       // counter tile allocated per CTA (bits)
-    uint32_t tile_bits_w[3];  // tile used by width class W = 4, 8, 16 (<= tile_bits)
+    uint32_t tile_bits_w[kClasses];  // tile of class c = tile_bits_w[c] / (4 << c) objects (W = 4, 8, 16:
+                                     // <= tile_bits; hashed class: hash_sub_T x GENIE_HASH_TILES)
+    // hashed sparse class (class 3; hash_slots == 0: off)
+    uint32_t hash_slots;  // open-addressing table slots (power of two) in the counter area
+    uint32_t hash_fill;   // an item takes the table path iff its postings <= hash_fill
+    uint32_t hash_pmax;   // a query joins the class iff P x T / n <= hash_pmax (expected postings per tile)
+    uint32_t hash_sub_T;  // objects of one 8-bit counter sub-tile (the overflow path)
     uint32_t unit;
     uint32_t selector;
     // workspace
@@ -99,7 +106,7 @@ struct BatchParams {
     uint32_t* out_thr;
 };
 
-__device__ __forceinline__ uint32_t wclass(uint32_t W) { return W == 4 ? 0 : (W == 8 ? 1 : 2); }
+__device__ __forceinline__ uint32_t wclass(uint32_t W) { return W == 4 ? 0 : (W == 8 ? 1 : (W == 16 ? 2 : 3)); }
 
 __device__ __forceinline__ uint32_t tile_objs(const BatchParams& p, uint32_t W) {
     return p.tile_bits_w[wclass(W)] / W;
@@ -199,6 +206,15 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
             atomicMin(&p.st[ST_BAD_BOUND], static_cast<unsigned long long>(q));
         } else {
             W = width_for(bnd);
+            // hashed sparse class: counts fit 8 bits, the spans one staging
+            // batch, the W = 8 path would cut the objects into several tiles,
+            // and the query's postings are few for a hashed tile's objects
+            // (expected per tile <= hash_pmax; a tile that still gets more
+            // than the table takes takes the sub-tile path in k_scan)
+            if (W <= 8 && p.hash_slots && p.selector == GENIE_SELECT_CPQ && P > 0 && carry <= kSpanBatch &&
+                i1 - i0 <= kSpanBatch && p.n > tile_objs(p, 8) &&
+                P * (p.tile_bits_w[3] / kHashW) <= uint64_t(p.hash_pmax) * p.n)
+                W = kHashW;
             nt = (P == 0 || p.n == 0) ? 0 : ntiles_for(p.n, p.tile_bits_w[wclass(W)], W);
         }
     }
@@ -216,11 +232,11 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
 // Single CTA: exclusive prefix sums over queries and the width classes.
 __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
     __shared__ unsigned long long sums[32];
-    unsigned long long c_span = 0, c_cut = 0, c_tile = 0, c_out = 0, c_cls = 0;
+    unsigned long long c_span = 0, c_cut = 0, c_tile = 0, c_out = 0, c_cls = 0, c_cls3 = 0;
     uint32_t max_nt = 0;
     for (uint32_t base = 0; base < p.Q; base += blockDim.x) {
         const uint32_t q = base + threadIdx.x;
-        unsigned long long v_span = 0, v_cut = 0, v_tile = 0, v_out = 0, v_cls = 0;
+        unsigned long long v_span = 0, v_cut = 0, v_tile = 0, v_out = 0, v_cls = 0, v_cls3 = 0;
         uint32_t cap = 0, W = 0, nt = 0;
         if (q < p.Q) {
             nt = p.q_ntiles[q];
@@ -228,23 +244,30 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
             if (nt) {
                 const uint32_t T = tile_objs(p, W);
                 const uint32_t kq = p.k[q];
-                cap = min(kq, T);
+                // a hashed tile whose postings overflow the table emits the
+                // top-k of each of its 8-bit sub-tiles (k_scan): up to
+                // ceil(T / hash_sub_T) x k entries
+                cap = W == kHashW ? min(uint32_t(min(uint64_t(kq) * ((T + p.hash_sub_T - 1) / p.hash_sub_T),
+                                                     uint64_t(0xffffffffu))), T)
+                                  : min(kq, T);
                 // single-tile queries read each item's contiguous keyword
                 // range directly (no per-keyword spans / cuts)
                 v_span = nt > 1 ? p.q_S[q] : 0u;
                 v_cut = nt > 1 ? static_cast<unsigned long long>(p.q_S[q]) * (nt + 1) : 0ull;
                 v_tile = nt;
                 v_out = static_cast<unsigned long long>(nt) * cap;
-                v_cls = 1ull << (21 * wclass(W));
+                if (W == kHashW) v_cls3 = 1;
+                else v_cls = 1ull << (21 * wclass(W));
             }
             max_nt = max(max_nt, nt);
         }
-        unsigned long long t_span, t_cut, t_tile, t_out, t_cls;
+        unsigned long long t_span, t_cut, t_tile, t_out, t_cls, t_cls3;
         const unsigned long long e_span = block_exclusive_scan(v_span, sums, t_span);
         const unsigned long long e_cut = block_exclusive_scan(v_cut, sums, t_cut);
         const unsigned long long e_tile = block_exclusive_scan(v_tile, sums, t_tile);
         const unsigned long long e_out = block_exclusive_scan(v_out, sums, t_out);
         const unsigned long long e_cls = block_exclusive_scan(v_cls, sums, t_cls);
+        const unsigned long long e_cls3 = block_exclusive_scan(v_cls3, sums, t_cls3);
         if (q < p.Q) {
             p.q_span_base[q] = c_span + e_span;
             p.q_cut_base[q] = c_cut + e_cut;
@@ -252,7 +275,9 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
             p.q_out_base[q] = c_out + e_out;
             p.q_cap[q] = cap;
             const unsigned long long r = c_cls + e_cls;
-            p.q_rank[q] = nt ? static_cast<uint32_t>((r >> (21 * wclass(W))) & 0x1fffffull) : 0;
+            p.q_rank[q] = !nt ? 0u
+                          : W == kHashW ? static_cast<uint32_t>(c_cls3 + e_cls3)
+                                        : static_cast<uint32_t>((r >> (21 * wclass(W))) & 0x1fffffull);
             QueryPlan pl;
             pl.cut_base = c_cut + e_cut;
             pl.span_base = c_span + e_span;
@@ -276,6 +301,7 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
         c_tile += t_tile;
         c_out += t_out;
         c_cls += t_cls;
+        c_cls3 += t_cls3;
     }
     if (threadIdx.x == 0) {
         p.st[ST_TOTAL_SPANS] = c_span;
@@ -285,6 +311,7 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
         p.st[ST_CLASS0] = c_cls & 0x1fffffull;
         p.st[ST_CLASS1] = (c_cls >> 21) & 0x1fffffull;
         p.st[ST_CLASS2] = (c_cls >> 42) & 0x1fffffull;
+        p.st[ST_CLASS3] = c_cls3;
         if (c_span > p.cap_spans || c_cut > p.cap_cuts || c_tile > p.cap_work ||
             c_out > p.cap_tout)
             p.st[ST_OVERFLOW] = 1;
@@ -306,9 +333,9 @@ __global__ void __launch_bounds__(256) k_worklist(BatchParams p) {
     const uint32_t nt = p.q_ntiles[q];
     if (!nt) return;
     const uint32_t c = wclass(p.q_W[q]);
-    uint64_t cnt[3], ntc[3];
-    for (int i = 0; i < 3; ++i) {
-        cnt[i] = p.st[ST_CLASS0 + i];
+    uint64_t cnt[kClasses], ntc[kClasses];
+    for (int i = 0; i < kClasses; ++i) {
+        cnt[i] = p.st[class_st(i)];
         ntc[i] = p.n ? ntiles_for(p.n, p.tile_bits_w[i], 4u << i) : 0;
     }
     const uint32_t rank = p.q_rank[q];
@@ -358,8 +385,9 @@ __global__ void __launch_bounds__(256) k_cut(BatchParams p) {
             // the list's bitmap replaces its posting scan when the list is dense
             // enough for this query's counter width (bit-sliced / lane-wise adds
             // per 32 objects vs. an atomic per posting)
-            int32_t ds = p.n_dense ? p.key_dense[j] : -1;
-            const uint32_t inv = p.dense_inv[wclass(p.q_W[q])];
+            const uint32_t cls = wclass(p.q_W[q]);  // the hashed class never uses bitmaps
+            int32_t ds = p.n_dense && cls < 3 ? p.key_dense[j] : -1;
+            const uint32_t inv = p.dense_inv[cls < 3 ? cls : 0];
             if (ds >= 0 && inv && uint64_t(len) * inv < p.n) ds = -1;
             p.span_beg[g] = beg;
             p.span_dense[g] = ds;
@@ -501,6 +529,11 @@ enum ScalarSlot {
     SC_NOUT = 3,        // entries emitted by the item
     SC_UCTR = 4,        // guided-scheduling cursor
     SC_T = 7,           // hist_select scratch
+    SC_HTHR = 5,        // hashed items: AT - 1, entries above it, the tie cut (bin, rank in bin, id)
+    SC_HABOVE = 6,
+    SC_HBIN = 8,
+    SC_HNEED = 9,
+    SC_HCUT = 11,
     SC_FLOOR = 10,      // gate start of the item
     SC_PF_ITEM = 13,    // the item the next prepare_item prepares (claimed and resolved), its query and tile
     SC_PF_Q = 14,
@@ -1807,7 +1840,7 @@ __device__ __forceinline__ StageArgs stage_args(const BatchParams& p, const Quer
 // warps that prepare the next item in the W kernel (GENIE_PREP_WARPS_W8 for W >= 8)
 template <int W>
 __device__ __host__ constexpr uint32_t prep_warps() {
-    return W >= 8 ? GENIE_PREP_WARPS_W8 : 1u;
+    return W == kHashW ? GENIE_HASH_PW : (W >= 8 ? GENIE_PREP_WARPS_W8 : 1u);
 }
 struct WorkQueue {  // one width class's items [base, end) of the work list, claimed via st[ctr]
     uint32_t base, end, ctr;
@@ -2033,7 +2066,7 @@ GENIE_PREP_FN void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32
     if (pw == kStager) stage_warp_issue(p, sa, sm.sb(buf), t, 0, nsb);
     uint32_t nq = 0, ntile = 0, a0 = 0;
     unsigned long long raw_claim = ~0ull;
-    const bool gate = (p.selector == GENIE_SELECT_CPQ) && pl.W <= 8;
+    const bool gate = (p.selector == GENIE_SELECT_CPQ) && (pl.W <= 8 || pl.W == kHashW);
 #ifdef GENIE_PHASE_TIMERS
     long long pt2 = 0, pt3 = 0;
 #endif
@@ -2204,6 +2237,359 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
     }
 }
 
+// ------------------------------------------------------ hashed sparse class
+//
+// A query whose postings are few for the objects they spread over (minHash:
+// ~1.5 K postings per 94 K-object W = 8 tile) spends most of a dense item on
+// per-object work -- zeroing the counter tile, the extract scans -- and on the
+// per-item chains (staging 128 slices, barriers).  The hashed class (k_resolve)
+// gives such a query tiles of GENIE_HASH_TILES x the W = 8 tile and counts into
+// an open-addressing table in the counter area instead: one 32-bit slot per
+// touched object, (local id << 8) | count, linear probing; a posting costs one
+// shared CAS (first touch) or CAS + add.  The Count Priority Queue state is
+// then read off the final counts: ZA[v] = #objects counting >= v is a suffix
+// sum of the count histogram, so AT = the first level >= the gate start that
+// fewer than k objects reach (cpq.hpp:374-389), thr = AT - 1, and the tile
+// emits exactly what extract() does (cpq.hpp:307-339): every count > thr,
+// then the first k - above ties at thr in ascending id -- found by a two-level
+// radix selection on the tie ids.  Records and the query floor as in
+// scan_and_select.  An item whose postings exceed the table's fill limit
+// (skewed ids) counts its tile as 8-bit dense sub-tiles of hash_sub_T objects
+// instead and emits each sub-tile's exact top-k (hist_select).
+constexpr uint32_t kEmptyHash = 0xffffffffu;
+constexpr uint32_t kTieBins = 1024;
+static_assert((kScanThreads / 32) * 256 * 4 + kTieBins * 4 <= kHashScratch, "hashed-item scratch");
+
+__device__ __forceinline__ uint32_t atom_cas_shared(uint32_t addr, uint32_t cmp, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(addr), "r"(cmp), "r"(v));
+    return old;
+}
+__device__ __forceinline__ void red_add_shared(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
+// One posting: count object `local` in the table at shared address `tab`.
+__device__ __forceinline__ void hash_count(uint32_t tab, uint32_t hmask, uint32_t hshift, uint32_t local) {
+    const uint32_t key = local << 8;
+    uint32_t h = (local * 0x9E3779B1u) >> hshift;
+    for (;;) {
+        const uint32_t a = tab + h * 4;
+        const uint32_t old = atom_cas_shared(a, kEmptyHash, key | 1u);
+        if (old == kEmptyHash) return;
+        if ((old & ~0xffu) == key) {
+            red_add_shared(a, 1u);
+            return;
+        }
+        h = (h + 1) & hmask;
+    }
+}
+
+// A warp's contiguous run [r0, r1) of the item's staged postings (across its
+// slices, as scan_compact), lane l taking r0 + l + 32 j.  SUB = false: count
+// into the table; SUB = true: 8-bit dense counters of the objects
+// [lo, lo + n) (linear layout), other ids skipped.
+template <bool SUB>
+__device__ __forceinline__ void hashed_scan(const uint32_t* __restrict__ postings, const StageBuf& sb, uint32_t nsb,
+                                            uint32_t r0, uint32_t r1, uint32_t lo, uint32_t n, uint32_t base,
+                                            uint32_t hmask, uint32_t hshift) {
+    constexpr int UNR = GENIE_HASH_UNR;
+    if (r0 >= r1) return;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t* pp = sb.ppref();
+    uint32_t si;
+    {
+        const uint32_t r = min(r0 + lane, r1 - 1);
+        uint32_t a = 0, b = nsb;
+        while (a < b) {
+            const uint32_t m = (a + b) >> 1;
+            if (pp[m] <= r) a = m + 1;
+            else b = m;
+        }
+        si = a - 1;
+    }
+    for (uint32_t r00 = r0; r00 < r1; r00 += 32 * UNR) {
+        uint32_t x[UNR];
+        uint32_t ok = 0;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t r = r00 + u * 32 + lane;
+            x[u] = 0;
+            if (r < r1) {
+                while (pp[si + 1] <= r) ++si;
+                x[u] = __ldg(postings + sb.beg()[si] + (r - pp[si]));
+                ok |= 1u << u;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            if (!((ok >> u) & 1u)) continue;
+            const uint32_t d = x[u] - lo;
+            if constexpr (SUB) {
+                if (d < n) red_add_shared(base + (d >> 2) * 4, 1u << ((d & 3u) * 8));
+            } else {
+                hash_count(base, hmask, hshift, d);
+            }
+        }
+    }
+}
+
+// The tile's exact top-k from the table (see above).
+__device__ void hashed_select(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm, uint32_t H) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t* tab = sm.cnt;
+    uint32_t* hsub = sm.cnt + H;                       // per-warp 256-bin count histograms
+    uint32_t* tbin = hsub + (kScanThreads / 32) * 256;  // tie bins
+    const uint4* t4 = reinterpret_cast<const uint4*>(tab);
+#ifdef GENIE_PHASE_TIMERS
+    const long long hs0 = clock64();
+#endif
+    // 1. count histogram (counts 1..3, the bulk, tallied in registers)
+    {
+        uint32_t n1 = 0, n2 = 0, n3 = 0;
+        uint32_t* hw = hsub + warp * 256;
+        for (uint32_t i = threadIdx.x; i < H / 4; i += kScanThreads) {
+            const uint4 v = t4[i];
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (w[e] == kEmptyHash) continue;
+                const uint32_t c = w[e] & 0xffu;
+                n1 += c == 1;
+                n2 += c == 2;
+                n3 += c == 3;
+                if (c > 3) atomicAdd(&hw[c], 1u);
+            }
+        }
+        n1 = warp_sum(n1);
+        n2 = warp_sum(n2);
+        n3 = warp_sum(n3);
+        if (lane == 0) {
+            hw[1] += n1;
+            hw[2] += n2;
+            hw[3] += n3;
+        }
+    }
+    __syncthreads();
+#ifdef GENIE_PHASE_TIMERS
+    const long long hs1 = clock64();
+#endif
+    // 2. ZA[v] = #objects counting >= v, the histogram's suffix sums (threads
+    // 0..255: bin 255 - t, warp scans + the lower warps' totals), then AT =
+    // the first level >= the gate start that fewer than k objects reach
+    {
+        const uint32_t t = threadIdx.x;
+        uint32_t v = 0;
+        if (t < 256)
+            for (uint32_t w = 0; w < kScanThreads / 32; ++w) v += hsub[w * 256 + (255 - t)];
+        const uint32_t incl = warp_inclusive_scan(v);
+        if (lane == 31) sm.sums[warp] = incl;
+        __syncthreads();
+        if (t < 256) {
+            uint32_t add = 0;
+            for (uint32_t w = 0; w < warp; ++w) add += static_cast<uint32_t>(sm.sums[w]);
+            sm.za[255 - t] = incl + add;
+        }
+        __syncthreads();
+        const uint32_t floor = sm.scal[SC_FLOOR], a0 = floor > 1 ? floor : 1u;
+        if (t < 256 && t >= a0 && (t > it.bound || sm.za[t] < it.kq)) atomicMin(&sm.scal[SC_HTHR], t);
+        __syncthreads();
+        if (t == 0) {
+            const uint32_t at = min(sm.scal[SC_HTHR], it.bound + 1);
+            sm.scal[SC_HTHR] = at - 1;
+            sm.scal[SC_HABOVE] = at <= 255 ? sm.za[at] : 0u;
+        }
+    }
+    __syncthreads();
+#ifdef GENIE_PHASE_TIMERS
+    const long long ht1 = clock64();
+    if (threadIdx.x == 0) {
+        atomicAdd(&p.st[ST_P_WAIT], static_cast<unsigned long long>(hs1 - hs0));
+        atomicAdd(&p.st[ST_P_ISSUE], static_cast<unsigned long long>(ht1 - hs1));
+    }
+#endif
+    const uint32_t thr = sm.scal[SC_HTHR], above = sm.scal[SC_HABOVE], floor = sm.scal[SC_FLOOR];
+    ItemCtx itr = it;
+    itr.rec_b = max((thr > 0 && thr >= floor) ? thr : floor, 1u);
+    if (threadIdx.x == 0) p.tile_rec[uint64_t(it.slot) * kRecWords] = itr.rec_b;
+    const bool ties = thr > 0 && thr >= floor;  // then ZA[thr] >= k > above: ties fill the rest
+    const uint32_t need = ties ? it.kq - above : 0u;
+    const uint32_t lbits = 32 - __clz(max(it.tile_n - 1, 1u));  // <= 20 bits (host caps the tile)
+    const uint32_t shift = lbits > 10 ? lbits - 10 : 0u;
+    // 3. counts > thr out; tie bins by the high id bits
+    for (uint32_t i = threadIdx.x; i < H / 4; i += kScanThreads) {
+        const uint4 v = t4[i];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (w[e] == kEmptyHash) continue;
+            const uint32_t c = w[e] & 0xffu;
+            if (c > thr) emit(p, itr, sm, w[e] >> 8, c);
+            else if (ties && c == thr) atomicAdd(&tbin[(w[e] >> 8) >> shift], 1u);
+        }
+    }
+    __syncthreads();
+#ifdef GENIE_PHASE_TIMERS
+    const long long ht2 = clock64();
+    if (threadIdx.x == 0) atomicAdd(&p.st[ST_T_DENSE], static_cast<unsigned long long>(ht2 - ht1));
+#endif
+    if (!ties) return;
+    // 4. the bin holding the need-th smallest tie id, and the rank inside it
+    auto find_rank = [&](uint32_t want, uint32_t slot_bin, uint32_t slot_rank) {
+        if (warp == 0) {
+            uint32_t s = 0;  // lane l: bins 32 l .. 32 l + 31, read rotated (no bank conflicts)
+            for (uint32_t j = 0; j < kTieBins / 32; ++j) s += tbin[lane * (kTieBins / 32) + ((j + lane) & 31)];
+            const uint32_t incl = warp_inclusive_scan(s);
+            uint32_t cum = incl - s;
+            if (cum < want && want <= incl) {
+                for (uint32_t j = 0; j < kTieBins / 32; ++j) {
+                    const uint32_t v = tbin[lane * (kTieBins / 32) + j];
+                    if (cum + v >= want) {
+                        sm.scal[slot_bin] = lane * (kTieBins / 32) + j;
+                        sm.scal[slot_rank] = want - cum;
+                        break;
+                    }
+                    cum += v;
+                }
+            }
+        }
+        __syncthreads();
+    };
+    find_rank(need, SC_HBIN, SC_HNEED);
+    const uint32_t B = sm.scal[SC_HBIN];
+    uint32_t cut = B << shift;  // the need-th smallest tie id
+    if (shift) {
+        // 5. ids are distinct: flag the low parts of bin B's ties, pick the rank
+        const uint32_t need2 = sm.scal[SC_HNEED];
+        for (uint32_t i = threadIdx.x; i < kTieBins; i += kScanThreads) tbin[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < H / 4; i += kScanThreads) {
+            const uint4 v = t4[i];
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (w[e] != kEmptyHash && (w[e] & 0xffu) == thr && ((w[e] >> 8) >> shift) == B)
+                    tbin[(w[e] >> 8) & ((1u << shift) - 1u)] = 1u;
+        }
+        __syncthreads();
+        find_rank(need2, SC_HCUT, SC_HNEED);
+        cut |= sm.scal[SC_HCUT];
+    }
+    // 6. ties with id <= cut: exactly `need` of them
+    for (uint32_t i = threadIdx.x; i < H / 4; i += kScanThreads) {
+        const uint4 v = t4[i];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (w[e] != kEmptyHash && (w[e] & 0xffu) == thr && (w[e] >> 8) <= cut) emit(p, itr, sm, w[e] >> 8, thr);
+    }
+    if (threadIdx.x == 0) atomicMax(&p.q_floor[it.q], thr);
+#ifdef GENIE_PHASE_TIMERS
+    if (threadIdx.x == 0) {
+        atomicAdd(&p.st[ST_T_GATE], 1ull);
+        atomicAdd(&p.st[ST_T_STAGE], static_cast<unsigned long long>(clock64() - ht2));
+    }
+#endif
+}
+
+// Overflow path: the tile as 8-bit dense sub-tiles, each one's exact top-k
+// (up to ceil(T / hash_sub_T) x k entries: the class's tile capacity).
+__device__ void hashed_sub_tiles(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm0, const StageBuf& sb,
+                                 uint32_t nsb, uint32_t ptot) {
+    ScanSmem sm = sm0;
+    const uint32_t nwarps = kScanThreads / 32, warp = threadIdx.x >> 5;
+    const uint32_t share = (ptot + nwarps - 1) / nwarps;
+    const uint32_t r0 = min(ptot, warp * share), r1 = min(ptot, r0 + share);
+    for (uint32_t lo = 0; lo < it.tile_n; lo += p.hash_sub_T) {
+        ItemCtx is = it;
+        is.tile_lo = it.tile_lo + lo;
+        is.tile_n = min(p.hash_sub_T, it.tile_n - lo);
+        is.words = ((is.tile_n + 31) >> 5) * 8;
+        is.gate = false;
+        is.ht_cap = kHtSlots;
+        sm.ht = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sm.cnt) + ((is.words + 15) & ~15u) * 4);
+        uint4* c4 = reinterpret_cast<uint4*>(sm.cnt);
+        for (uint32_t i = threadIdx.x; i < (is.words + 3) / 4; i += kScanThreads) c4[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        hashed_scan<true>(p.postings, sb, nsb, r0, r1, is.tile_lo, is.tile_n, smem_u32(sm.cnt), 0, 0);
+        __syncthreads();
+        hist_select<8, false>(p, is, sm);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) atomicAdd(&p.st[ST_FALLBACK], 1ull);
+}
+
+__device__ void process_item_hashed(const BatchParams& p, const ScanSmem& sm, uint32_t b, const WorkQueue& total) {
+    constexpr uint32_t PW = prep_warps<kHashW>();
+    const ItemDesc& d = sm.desc[b];
+    ItemCtx it;
+    it.q = d.q;
+    it.t = d.t;
+    it.kq = d.kq;
+    it.bound = d.bound;
+    const uint32_t T = tile_objs(p, kHashW);
+    it.tile_lo = it.t * T;
+    it.tile_n = min(T, p.n - it.tile_lo);
+    it.words = 0;
+    it.cap = d.cap;
+    it.slot = d.tile_slot;
+    it.out_base = d.out_base;
+    it.gate = true;
+    it.ht_cap = 0;
+    const uint32_t nsb = min(kSpanBatch, d.S), ptot = d.ptot;
+    const uint32_t H = p.hash_slots;
+    const bool fast = ptot <= p.hash_fill;  // block-uniform
+#ifdef GENIE_PHASE_TIMERS
+    const long long t0 = clock64();
+#endif
+    if (fast) {
+        uint4* t4 = reinterpret_cast<uint4*>(sm.cnt);
+        for (uint32_t i = threadIdx.x; i < H / 4; i += kScanThreads) t4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+        uint4* h4 = reinterpret_cast<uint4*>(sm.cnt + H);
+        for (uint32_t i = threadIdx.x; i < ((kScanThreads / 32) * 256 + kTieBins) / 4; i += kScanThreads)
+            h4[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (threadIdx.x == 0) {
+        sm.scal[SC_FLOOR] = d.a0;
+        sm.scal[SC_NOUT] = 0;
+        sm.scal[SC_HTHR] = 0xffffffffu;
+    }
+    __syncthreads();
+#ifdef GENIE_PHASE_TIMERS
+    const long long t1 = clock64();
+#endif
+    // warps 0 .. PW-1 prepare the next item while the others count this one
+    if (threadIdx.x < 32 * PW) {
+        prepare_item<PW>(p, sm, b ^ 1u, total);
+    } else if (fast) {
+        const uint32_t nwarps = kScanThreads / 32 - PW, warp = (threadIdx.x >> 5) - PW;
+        const uint32_t share = (ptot + nwarps - 1) / nwarps;
+        const uint32_t r0 = min(ptot, warp * share), r1 = min(ptot, r0 + share);
+        hashed_scan<false>(p.postings, sm.sb(b), nsb, r0, r1, it.tile_lo, 0, smem_u32(sm.cnt), H - 1,
+                           1u + __clz(H));
+    }
+    __syncthreads();
+#ifdef GENIE_PHASE_TIMERS
+    const long long t2 = clock64();
+#endif
+#if GENIE_HASH_NOSELECT  // timing experiment only: results are not produced
+    if (false) hashed_select(p, it, sm, H);
+#else
+    if (fast) hashed_select(p, it, sm, H);
+#endif
+    else if (!fast) hashed_sub_tiles(p, it, sm, sm.sb(b), nsb, ptot);
+    __syncthreads();
+    if (threadIdx.x == 0) p.tile_len[it.slot] = sm.scal[SC_NOUT];
+#ifdef GENIE_PHASE_TIMERS
+    if (threadIdx.x == 0) {
+        atomicAdd(&p.st[ST_T_SETUP], static_cast<unsigned long long>(t1 - t0));
+        atomicAdd(&p.st[ST_T_SCAN], static_cast<unsigned long long>(t2 - t1));
+        atomicAdd(&p.st[ST_T_EXTRACT], static_cast<unsigned long long>(clock64() - t2));
+        atomicAdd(&p.st[ST_T_WMAX], static_cast<unsigned long long>(ptot));
+    }
+#endif
+}
+
 // One persistent kernel per counter width W (its own register allocation):
 // the CTAs drain the W class's slice of the work list (k_worklist orders the
 // list class-major), a launch per class.
@@ -2213,10 +2599,10 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     extern __shared__ __align__(16) uint8_t smem[];
     const ScanSmem sm = carve(smem, p.ht_slots, tile_bytes);
     if (p.st[ST_OVERFLOW]) return;
-    constexpr uint32_t c = W == 4 ? 0 : (W == 8 ? 1 : 2);
+    constexpr uint32_t c = W == 4 ? 0 : (W == 8 ? 1 : (W == 16 ? 2 : 3));
     WorkQueue total{0, 0, kWorkCtr[c]};
     for (uint32_t i = 0; i <= c; ++i) {
-        const uint32_t items = static_cast<uint32_t>(p.st[ST_CLASS0 + i]) *
+        const uint32_t items = static_cast<uint32_t>(p.st[class_st(i)]) *
                                (p.n ? ntiles_for(p.n, p.tile_bits_w[i], 4u << i) : 0u);
         total.base = total.end;
         total.end += items;
@@ -2258,7 +2644,8 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     for (uint32_t iter = 0;; ++iter) {
         const uint32_t b = iter & 1u;
         if (!sm.desc[b].valid) break;
-        process_item<W>(p, sm, b, total);
+        if constexpr (W == kHashW) process_item_hashed(p, sm, b, total);
+        else process_item<W>(p, sm, b, total);
     }
 }
 
@@ -2629,9 +3016,9 @@ __global__ void k_keycut(const uint64_t* key_off, const uint32_t* postings, uint
 
 // Builds the table of every width class the index has been queried with
 // (class_seen, from the previous batches' status) at the batch's tile sizes.
-static void ensure_keycuts(genie_index* ix, const uint32_t (&tile_bits_w)[3], cudaStream_t s) {
+static void ensure_keycuts(genie_index* ix, const uint32_t (&tile_bits_w)[kClasses], cudaStream_t s) {
     if (!ix->K || !ix->n) return;
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c < kClasses; ++c) {
         const uint32_t T = tile_bits_w[c] / (4u << c);
         if (!ix->class_seen[c] || ix->keycut_T[c] == T) continue;
         const uint32_t nt = (ix->n + T - 1) / T;
@@ -2827,8 +3214,8 @@ static uint32_t tile_bits_of(const genie_config& cfg) {
 // tile share.  The cap snaps to 64 / 48 / 32 KB (C3: 64 KB, +23 %; measured
 // non-power-of-two sizes lose up to 12 %).  W = 4 tiles hold at most as many
 // objects as the cap.  Explicit tile_bytes apply to every class unchanged.
-static uint32_t class_tile_bits(const genie_index* ix, const genie_config& cfg, uint32_t tile_bits,
-                                uint32_t (&out)[3]) {
+static uint32_t class_tile_bits_dense(const genie_index* ix, const genie_config& cfg, uint32_t tile_bits,
+                                      uint32_t (&out)[kClasses]) {
     for (int c = 0; c < 3; ++c) out[c] = tile_bits;
     if (cfg.tile_bytes || ix->n == 0) return tile_bits;
     static thread_local int dev_cached = -1;
@@ -2853,6 +3240,43 @@ static uint32_t class_tile_bits(const genie_index* ix, const genie_config& cfg, 
     out[0] = std::min<uint32_t>(alloc, static_cast<uint32_t>(std::max(objs * 4.0, double(alloc) / 2)) & ~1023u);
     out[1] = alloc;
     out[2] = alloc;
+    return alloc;
+}
+
+static uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
+}
+
+// Hashed sparse class (k_scan<kHashW>): the table takes the largest power of
+// two of slots the counter area holds next to its scratch; the class's tile
+// is GENIE_HASH_TILES 8-bit sub-tiles of the allocation (<= 2^20 objects: the
+// tie selection's id radix).  Knobs (read per batch): GENIE_HASH_TILES (0: the
+// class is off), GENIE_HASH_LOAD_PCT, GENIE_HASH_FILL_PCT.  Results do not
+// depend on them.
+struct HashPlan {
+    uint32_t slots = 0, fill = 0, pmax = 0, sub_T = 0, tile_objs = 1024;
+};
+static HashPlan hash_plan(uint32_t tile_bits) {
+    HashPlan h;
+    const uint32_t tile_bytes = tile_bits / 8;
+    const uint32_t nsub = env_u32("GENIE_HASH_TILES", GENIE_HASH_TILES);
+    h.sub_T = tile_bytes & ~1023u;
+    if (nsub == 0 || tile_bytes < kHashScratch + 4096 * 4 || h.sub_T == 0) return h;
+    const uint32_t room = (tile_bytes - kHashScratch) / 4;
+    h.slots = 1u << (31 - __builtin_clz(room));
+    h.fill = static_cast<uint32_t>(uint64_t(h.slots) * std::min<uint32_t>(env_u32("GENIE_HASH_FILL_PCT", GENIE_HASH_FILL_PCT), 90) / 100);
+    h.pmax = static_cast<uint32_t>(uint64_t(h.slots) * env_u32("GENIE_HASH_LOAD_PCT", GENIE_HASH_LOAD_PCT) / 100);
+    h.tile_objs = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(nsub) * h.sub_T, 1u << 20));
+    return h;
+}
+
+static uint32_t class_tile_bits(const genie_index* ix, const genie_config& cfg, uint32_t tile_bits,
+                                uint32_t (&out)[kClasses], HashPlan* hp = nullptr) {
+    const uint32_t alloc = class_tile_bits_dense(ix, cfg, tile_bits, out);
+    const HashPlan h = hash_plan(alloc);
+    out[3] = h.tile_objs * kHashW;
+    if (hp) *hp = h;
     return alloc;
 }
 
@@ -2907,8 +3331,9 @@ static void segmented_sort_rows(genie_index* ix, uint32_t Q, uint32_t stride, ge
 
 uint64_t prepare_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, uint32_t total_items, uint32_t max_k,
                        uint32_t out_stride, cudaStream_t s) {
-    uint32_t tile_bits_w[3];
-    class_tile_bits(ix, cfg, tile_bits_of(cfg), tile_bits_w);
+    uint32_t tile_bits_w[kClasses];
+    HashPlan hp;
+    class_tile_bits(ix, cfg, tile_bits_of(cfg), tile_bits_w, &hp);
     reserve_workspace(ix, Q, total_items, max_k, out_stride,
                       std::min({tile_bits_w[0] * 4, tile_bits_w[1] * 2, tile_bits_w[2]}));
     ensure_keycuts(ix, tile_bits_w, s);
@@ -2928,10 +3353,12 @@ uint64_t prepare_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, uin
                             (const void*)w.d_k.p, (const void*)w.d_item_off.p, (const void*)w.d_dim.p,
                             (const void*)w.d_lo.p, (const void*)w.d_hi.p, (const void*)w.d_out.p,
                             (const void*)w.d_out_len.p, (const void*)w.d_out_thr.p, (const void*)ix->keycut[0].p,
-                            (const void*)ix->keycut[1].p, (const void*)ix->keycut[2].p})
+                            (const void*)ix->keycut[1].p, (const void*)ix->keycut[2].p, (const void*)ix->keycut[3].p})
         mixin(reinterpret_cast<uint64_t>(ptr));
     for (uint64_t v : {uint64_t(w.cap_spans), uint64_t(w.cap_cuts), uint64_t(w.cap_work), uint64_t(w.cap_tout),
-                       uint64_t(ix->keycut_T[0]), uint64_t(ix->keycut_T[1]), uint64_t(ix->keycut_T[2])})
+                       uint64_t(ix->keycut_T[0]), uint64_t(ix->keycut_T[1]), uint64_t(ix->keycut_T[2]),
+                       uint64_t(ix->keycut_T[3]), uint64_t(tile_bits_w[3]), uint64_t(hp.slots), uint64_t(hp.fill),
+                       uint64_t(hp.pmax), uint64_t(hp.sub_T)})
         mixin(v);
     return h;
 }
@@ -2943,8 +3370,9 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
                   uint32_t* d_out_thr, cudaStream_t s, bool timed, uint32_t extra_offset) {
     (void)d_qid;
     const uint32_t id_offset = ix->id_offset + extra_offset;  // reported ids are local + id_offset
-    uint32_t tile_bits_w[3];
-    const uint32_t tile_bits = class_tile_bits(ix, cfg, tile_bits_of(cfg), tile_bits_w);
+    uint32_t tile_bits_w[kClasses];
+    HashPlan hp;
+    const uint32_t tile_bits = class_tile_bits(ix, cfg, tile_bits_of(cfg), tile_bits_w, &hp);
     const uint32_t tile_bytes = tile_bits / 8;
     reserve_workspace(ix, Q, total_items, max_k, out_stride,
                       std::min({tile_bits_w[0] * 4, tile_bits_w[1] * 2, tile_bits_w[2]}));
@@ -2970,7 +3398,11 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.lo = d_lo;
     p.hi = d_hi;
     p.tile_bits = tile_bits;
-    for (int c = 0; c < 3; ++c) p.tile_bits_w[c] = tile_bits_w[c];
+    for (int c = 0; c < kClasses; ++c) p.tile_bits_w[c] = tile_bits_w[c];
+    p.hash_slots = hp.slots;
+    p.hash_fill = hp.fill;
+    p.hash_pmax = hp.pmax;
+    p.hash_sub_T = hp.sub_T;
     // span_chunk is the reference's chunk (ids per task chunk, engine.hpp:40);
     // a scan warp claims a quarter of one at a time (guided self-scheduling)
     uint32_t unit = cfg.span_chunk ? cfg.span_chunk / 4 : kDefaultUnit;
@@ -3000,7 +3432,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.key_dense = ix->key_dense.p;
     p.dim_range = ix->dim_range.p;
     p.tokmap = ix->tokmap.p;
-    for (int c = 0; c < 3; ++c)
+    for (int c = 0; c < kClasses; ++c)
         p.keycut[c] = ix->keycut_T[c] == tile_bits_w[c] / (4u << c) ? ix->keycut[c].p : nullptr;
     p.bitmaps = ix->bitmaps.p;
     p.bitmap_words = ix->bitmap_words;
@@ -3034,6 +3466,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         GENIE_CUDA(cudaFuncSetAttribute(k_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         GENIE_CUDA(cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         GENIE_CUDA(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        GENIE_CUDA(cudaFuncSetAttribute(k_scan<kHashW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         ac.scan_smem = smem;
     }
     if (!ac.merge_set) {
@@ -3081,6 +3514,10 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
             k_scan<8><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             k_scan<16><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             launches += 3;
+            if (p.hash_slots) {  // the hashed sparse class is enabled (GENIE_HASH_TILES)
+                k_scan<kHashW><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+                ++launches;
+            }
             if (timed) record(2);
             // one small CTA per query: after the floors prune them, unions are a
             // few k entries, so all queries merge concurrently; larger unions
@@ -3161,8 +3598,8 @@ int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
     GENIE_CUDA(cudaStreamSynchronize(ix->stream));
     GENIE_CUDA(cudaGetLastError());
     const unsigned long long* h = ix->ws.h_status;
-    for (int c = 0; c < 3; ++c)
-        if (h[ST_CLASS0 + c]) ix->class_seen[c] = true;  // its cut table is built before the next batch
+    for (int c = 0; c < kClasses; ++c)
+        if (h[class_st(c)]) ix->class_seen[c] = true;  // its cut table is built before the next batch
     if (stats) {
         stats->postings = h[ST_TOTAL_POSTINGS];
         stats->work_items = h[ST_TOTAL_WORK];

@@ -122,6 +122,22 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #ifndef GENIE_LANES_MAX  // dense lists per item up to which the lane-wise path runs (W <= 8)
 #define GENIE_LANES_MAX 3
 #endif
+#ifndef GENIE_HASH_TILES  // hashed sparse class: object tile = this many W = 8 counter tiles (0: class off)
+#define GENIE_HASH_TILES 0  // measured slower than the dense W = 8 tiles on C4 (1.37 M vs 2.0 M q/s): off
+#endif
+#ifndef GENIE_HASH_LOAD_PCT  // ... admits a query whose expected postings per tile fill <= this % of the table
+#define GENIE_HASH_LOAD_PCT 50
+#endif
+#ifndef GENIE_HASH_FILL_PCT  // ... an item takes the table path while its postings fill <= this % of it
+#define GENIE_HASH_FILL_PCT 75
+#endif
+#ifndef GENIE_HASH_PW  // ... warps preparing the next item (1 or 2)
+#define GENIE_HASH_PW 2
+#endif
+#ifndef GENIE_HASH_UNR  // ... posting loads per lane in flight
+#define GENIE_HASH_UNR 4
+#endif
+constexpr uint32_t kHashScratch = 20u << 10;  // per-warp count histograms + tie bins after the table
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
 #endif
@@ -174,9 +190,19 @@ enum StatusWord : int {
     ST_P_ISSUE = 35,
     ST_P_GATE = 36,
     ST_P_STAGE = 37,
+    ST_CLASS3 = 38,     // queries of the hashed sparse class (kHashW)
+    ST_WORK_CTR3 = 39,  // its scan queue cursor
     ST_WORDS = 40
 };
-constexpr uint32_t kWorkCtr[3] = {ST_WORK_CTR, ST_WORK_CTR1, ST_WORK_CTR2};
+// Work classes: counter widths W = 4, 8, 16 (dense counter tiles) and the
+// hashed sparse class (class 3, pseudo-width kHashW = 32: a query whose
+// postings are few for the object range counts into a shared-memory
+// open-addressing table instead of a dense counter tile).  W = 4 << class.
+constexpr int kClasses = 4;
+constexpr uint32_t kHashW = 32;
+constexpr uint32_t kWorkCtr[kClasses] = {ST_WORK_CTR, ST_WORK_CTR1, ST_WORK_CTR2, ST_WORK_CTR3};
+// status word holding the number of queries of class c
+__host__ __device__ constexpr uint32_t class_st(int c) { return c < 3 ? ST_CLASS0 + c : ST_CLASS3; }
 
 // Per-batch device scratch, grown on demand (never shrinks).
 struct Workspace {
@@ -241,9 +267,9 @@ struct genie_index {
     // per width class: every key's position of each object-tile boundary
     // (keycut[c][j * (nt + 1) + b], tiles of keycut_T[c] objects), built once
     // the class has been queried; k_cut then reads cuts instead of searching
-    genie::DevBuf<uint32_t> keycut[3];
-    uint32_t keycut_T[3] = {0, 0, 0};
-    bool class_seen[3] = {false, false, false};
+    genie::DevBuf<uint32_t> keycut[genie::kClasses];
+    uint32_t keycut_T[genie::kClasses] = {0, 0, 0, 0};
+    bool class_seen[genie::kClasses] = {false, false, false, false};
     // dense containers: keys whose list covers >= dense_density of the
     // objects also carry a bitmap of n bits (Roaring-style bitmap container)
     genie::DevBuf<int32_t> key_dense;   // [K] word offset of the key's row in `bitmaps`, or -1

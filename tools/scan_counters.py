@@ -68,7 +68,7 @@ def capture(workloads):
         rep = outdir / f"scan_{w}"
         # the batch's width class: W = 4 (tweets, adult) or 8 (sift, ocr, minhash); the other
         # classes' k_scan launches exit at once
-        wcls = 4 if w in ("tweets", "adult") else (32 if w == "minhash" else 8)
+        wcls = 4 if w in ("tweets", "adult") else 8
         cmd = ["ncu", "--set", "full", "--metrics", ",".join(METRICS), "--clock-control", "none",
                "--import-source", "on", "--kernel-name-base", "demangled", "-k", f"regex:k_scan<\\(int\\){wcls}>",
                "--launch-skip", "3", "--launch-count", "1",
