@@ -1082,6 +1082,62 @@ __device__ __forceinline__ void ldg_words(const uint32_t* src, uint32_t (&x)[G])
     }
 }
 
+// G bitmap words of each of N lists whose row offsets sit at slot[0..N)
+// (16-byte shared loads of the offsets measured no faster)
+template <int N, int G>
+__device__ __forceinline__ void ldg_lists(const uint32_t* col, const uint32_t* slot, uint32_t (&a)[N][G]) {
+#pragma unroll
+    for (int u = 0; u < N; ++u) ldg_words<G>(col + slot[u], a[u]);
+}
+
+// 16 lists into planes 0..3 (ones, twos, fours, eights accumulate there);
+// the weight-16 carry is returned in s16 for the caller to place.
+template <int NP, int G>
+__device__ __forceinline__ void hs16(uint32_t (&P)[G][NP], const uint32_t* col, const uint32_t* slot,
+                                     uint32_t (&s16)[G]) {
+    uint32_t eA[G];
+    {
+        uint32_t a[8][G];
+        ldg_lists<8, G>(col, slot, a);
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            uint32_t twosA, twosB, foursA, foursB;
+            csa(twosA, P[h][0], P[h][0], a[0][h], a[1][h]);
+            csa(twosB, P[h][0], P[h][0], a[2][h], a[3][h]);
+            csa(foursA, P[h][1], P[h][1], twosA, twosB);
+            csa(twosA, P[h][0], P[h][0], a[4][h], a[5][h]);
+            csa(twosB, P[h][0], P[h][0], a[6][h], a[7][h]);
+            csa(foursB, P[h][1], P[h][1], twosA, twosB);
+            csa(eA[h], P[h][2], P[h][2], foursA, foursB);
+        }
+    }
+    uint32_t a[8][G];
+    ldg_lists<8, G>(col, slot + 8, a);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        uint32_t twosA, twosB, foursA, foursB, eB;
+        csa(twosA, P[h][0], P[h][0], a[0][h], a[1][h]);
+        csa(twosB, P[h][0], P[h][0], a[2][h], a[3][h]);
+        csa(foursA, P[h][1], P[h][1], twosA, twosB);
+        csa(twosA, P[h][0], P[h][0], a[4][h], a[5][h]);
+        csa(twosB, P[h][0], P[h][0], a[6][h], a[7][h]);
+        csa(foursB, P[h][1], P[h][1], twosA, twosB);
+        csa(eB, P[h][2], P[h][2], foursA, foursB);
+        csa(s16[h], P[h][3], P[h][3], eA[h], eB);
+    }
+}
+
+// 32 lists into planes 0..4; the weight-32 carry is returned in s32.
+template <int NP, int G>
+__device__ __forceinline__ void hs32(uint32_t (&P)[G][NP], const uint32_t* col, const uint32_t* slot,
+                                     uint32_t (&s32)[G]) {
+    uint32_t sA[G], sB[G];
+    hs16<NP, G>(P, col, slot, sA);
+    hs16<NP, G>(P, col, slot + 16, sB);
+#pragma unroll
+    for (int h = 0; h < G; ++h) csa(s32[h], P[h][4], P[h][4], sA[h], sB[h]);
+}
+
 template <int W>
 __device__ __forceinline__ void store_block(const ScanSmem& sm, uint32_t blk, const uint32_t (&acc)[W]) {
     uint4* dst = reinterpret_cast<uint4*>(sm.cnt + blk * W);
@@ -1104,11 +1160,47 @@ __device__ __forceinline__ void dense_planes(const BatchParams& p, const ScanSme
 #pragma unroll
             for (int i = 0; i < NP; ++i) P[h][i] = 0;
         uint32_t d = 0;
+#if GENIE_CSA16
+        if constexpr (NP >= 7 && GENIE_CSA64) {
+            // 64 lists: two 32-list trees whose weight-32 carries meet plane 5
+            for (; d + 64 <= nd; d += 64) {
+                uint32_t sA[G], sB[G];
+                hs32<NP, G>(P, col, dslot + d, sA);
+                hs32<NP, G>(P, col, dslot + d + 32, sB);
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    uint32_t t64;
+                    csa(t64, P[h][5], P[h][5], sA[h], sB[h]);
+                    plane_add<NP>(P[h], t64, 6);  // weight 64
+                }
+            }
+        }
+        if constexpr (NP >= 6 && GENIE_CSA32) {
+            // 32 lists: two 16-list trees whose weight-16 carries meet plane 4
+            for (; d + 32 <= nd; d += 32) {
+                uint32_t s32[G];
+                hs32<NP, G>(P, col, dslot + d, s32);
+#pragma unroll
+                for (int h = 0; h < G; ++h) plane_add<NP>(P[h], s32[h], 5);  // weight 32
+            }
+        }
+        if constexpr (NP >= 5) {
+            // Harley-Seal over 16 lists: two 8-list halves whose weight-8
+            // carries meet plane 3 in one more CSA, so only the weight-16
+            // carry ripples (planes 4..NP-1) -- 38 logic ops per 16 lists and
+            // block instead of 2 x 24
+            for (; d + 16 <= nd; d += 16) {
+                uint32_t s16[G];
+                hs16<NP, G>(P, col, dslot + d, s16);
+#pragma unroll
+                for (int h = 0; h < G; ++h) plane_add<NP>(P[h], s16[h], 4);  // weight 16
+            }
+        }
+#endif
         if constexpr (NP >= 4) {
             for (; d + 8 <= nd; d += 8) {
                 uint32_t a[8][G];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) ldg_words<G>(col + dslot[d + u], a[u]);
+                ldg_lists<8, G>(col, dslot + d, a);
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
                     uint32_t twosA, twosB, foursA, foursB, eights;
@@ -1126,8 +1218,7 @@ __device__ __forceinline__ void dense_planes(const BatchParams& p, const ScanSme
         if constexpr (NP >= 3) {
             for (; d + 4 <= nd; d += 4) {
                 uint32_t a[4][G];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) ldg_words<G>(col + dslot[d + u], a[u]);
+                ldg_lists<4, G>(col, dslot + d, a);
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
                     uint32_t twosA, twosB, fours;

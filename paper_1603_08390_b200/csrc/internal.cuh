@@ -138,6 +138,15 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #define GENIE_HASH_UNR 4
 #endif
 constexpr uint32_t kHashScratch = 20u << 10;  // per-warp count histograms + tie bins after the table
+#ifndef GENIE_CSA16  // many-list dense path (>= 5 planes): 16-list Harley-Seal steps before the 8-list ones
+#define GENIE_CSA16 1
+#endif
+#ifndef GENIE_CSA32  // ... and (>= 6 planes) 32-list steps before those
+#define GENIE_CSA32 1
+#endif
+#ifndef GENIE_CSA64  // ... and (>= 7 planes) 64-list steps before those
+#define GENIE_CSA64 1
+#endif
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
 #endif
