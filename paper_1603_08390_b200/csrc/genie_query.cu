@@ -82,6 +82,10 @@ struct BatchParams {
     uint32_t hash_fill;   // an item takes the table path iff its postings <= hash_fill
     uint32_t hash_pmax;   // a query joins the class iff P x T / n <= hash_pmax (expected postings per tile)
     uint32_t hash_sub_T;  // objects of one 8-bit counter sub-tile (the overflow path)
+    uint32_t hash_dmax;   // ... and iff P x (W = 8 tile) / n <= hash_dmax (dense items would be overhead-bound)
+    uint32_t hash_min_items;  // the class runs only with at least this many items (k_plan), else its
+                              // queries go back to their dense width
+    uint32_t hash_launch;     // k_scan<kHashW> is launched in this batch (else every query is folded back)
     uint32_t unit;
     uint32_t selector;
     // workspace
@@ -207,12 +211,15 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
         } else {
             W = width_for(bnd);
             // hashed sparse class: counts fit 8 bits, the spans one staging
-            // batch, the W = 8 path would cut the objects into several tiles,
-            // and the query's postings are few for a hashed tile's objects
-            // (expected per tile <= hash_pmax; a tile that still gets more
-            // than the table takes takes the sub-tile path in k_scan)
+            // batch, the W = 8 path would cut the objects into several tiles
+            // that each get few postings (expected <= hash_dmax: such items
+            // are bound by their fixed per-item work), and the query's
+            // postings are few for a hashed tile's objects (expected per tile
+            // <= hash_pmax; a tile that still gets more than the table takes
+            // takes the sub-tile path in k_scan)
             if (W <= 8 && p.hash_slots && p.selector == GENIE_SELECT_CPQ && P > 0 && carry <= kSpanBatch &&
                 i1 - i0 <= kSpanBatch && p.n > tile_objs(p, 8) &&
+                P * tile_objs(p, 8) <= uint64_t(p.hash_dmax) * p.n &&
                 P * (p.tile_bits_w[3] / kHashW) <= uint64_t(p.hash_pmax) * p.n)
                 W = kHashW;
             nt = (P == 0 || p.n == 0) ? 0 : ntiles_for(p.n, p.tile_bits_w[wclass(W)], W);
@@ -232,8 +239,26 @@ __global__ void __launch_bounds__(256) k_resolve(BatchParams p) {
 // Single CTA: exclusive prefix sums over queries and the width classes.
 __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
     __shared__ unsigned long long sums[32];
+    __shared__ uint32_t s_hash_items;
     unsigned long long c_span = 0, c_cut = 0, c_tile = 0, c_out = 0, c_cls = 0, c_cls3 = 0;
     uint32_t max_nt = 0;
+    // The hashed class is its own k_scan launch after the dense classes: with
+    // too few items to occupy the GPU it would only add a tail (a handful of
+    // sparse queries in a dense batch), so its queries then go back to their
+    // dense width (results do not depend on the class)
+    if (threadIdx.x == 0) s_hash_items = 0;
+    __syncthreads();
+    if (p.hash_slots) {
+        uint32_t mine = 0;
+        for (uint32_t q = threadIdx.x; q < p.Q; q += blockDim.x)
+            if (p.q_W[q] == kHashW) mine += p.q_ntiles[q];
+        mine = warp_sum(mine);
+        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_hash_items, mine);
+    }
+    __syncthreads();
+    const bool want = s_hash_items && s_hash_items >= p.hash_min_items;
+    const bool demote = !(want && p.hash_launch);
+    if (threadIdx.x == 0) p.st[ST_HASH_WANT] = want ? 1ull : 0ull;
     for (uint32_t base = 0; base < p.Q; base += blockDim.x) {
         const uint32_t q = base + threadIdx.x;
         unsigned long long v_span = 0, v_cut = 0, v_tile = 0, v_out = 0, v_cls = 0, v_cls3 = 0;
@@ -241,6 +266,13 @@ __global__ void __launch_bounds__(1024) k_plan(BatchParams p) {
         if (q < p.Q) {
             nt = p.q_ntiles[q];
             W = p.q_W[q];
+            if (W == kHashW && demote) {
+                const uint64_t qb = p.q_bound[q];
+                W = width_for(qb < 1 ? 1 : qb);
+                nt = ntiles_for(p.n, p.tile_bits_w[wclass(W)], W);
+                p.q_W[q] = W;
+                p.q_ntiles[q] = nt;
+            }
             if (nt) {
                 const uint32_t T = tile_objs(p, W);
                 const uint32_t kq = p.k[q];
@@ -2330,11 +2362,12 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
 
 // ------------------------------------------------------ hashed sparse class
 //
-// A query whose postings are few for the objects they spread over (minHash:
-// ~1.5 K postings per 94 K-object W = 8 tile) spends most of a dense item on
-// per-object work -- zeroing the counter tile, the extract scans -- and on the
-// per-item chains (staging 128 slices, barriers).  The hashed class (k_resolve)
-// gives such a query tiles of GENIE_HASH_TILES x the W = 8 tile and counts into
+// A query whose postings are few for the objects they spread over (tens to a
+// few hundred postings per 94 K-object W = 8 tile: sparse sets over tens of
+// millions of objects) spends almost all of a dense item on fixed per-item
+// work -- the prepare chain, zeroing the counter tile, the extract scans,
+// barriers.  The hashed class (k_resolve, GENIE_HASH_DENSE_MAX) gives such a
+// query tiles of GENIE_HASH_TILES x the W = 8 tile (2^20 objects) and counts into
 // an open-addressing table in the counter area instead: one 32-bit slot per
 // touched object, (local id << 8) | count, linear probing; a posting costs one
 // shared CAS (first touch) or CAS + add.  The Count Priority Queue state is
@@ -3343,10 +3376,10 @@ static uint32_t env_u32(const char* name, uint32_t dflt) {
 // two of slots the counter area holds next to its scratch; the class's tile
 // is GENIE_HASH_TILES 8-bit sub-tiles of the allocation (<= 2^20 objects: the
 // tie selection's id radix).  Knobs (read per batch): GENIE_HASH_TILES (0: the
-// class is off), GENIE_HASH_LOAD_PCT, GENIE_HASH_FILL_PCT.  Results do not
-// depend on them.
+// class is off), GENIE_HASH_DENSE_MAX, GENIE_HASH_LOAD_PCT, GENIE_HASH_FILL_PCT.
+// Results do not depend on them.
 struct HashPlan {
-    uint32_t slots = 0, fill = 0, pmax = 0, sub_T = 0, tile_objs = 1024;
+    uint32_t slots = 0, fill = 0, pmax = 0, sub_T = 0, dmax = 0, tile_objs = 1024;
 };
 static HashPlan hash_plan(uint32_t tile_bits) {
     HashPlan h;
@@ -3358,6 +3391,7 @@ static HashPlan hash_plan(uint32_t tile_bits) {
     h.slots = 1u << (31 - __builtin_clz(room));
     h.fill = static_cast<uint32_t>(uint64_t(h.slots) * std::min<uint32_t>(env_u32("GENIE_HASH_FILL_PCT", GENIE_HASH_FILL_PCT), 90) / 100);
     h.pmax = static_cast<uint32_t>(uint64_t(h.slots) * env_u32("GENIE_HASH_LOAD_PCT", GENIE_HASH_LOAD_PCT) / 100);
+    h.dmax = env_u32("GENIE_HASH_DENSE_MAX", GENIE_HASH_DENSE_MAX);
     h.tile_objs = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(nsub) * h.sub_T, 1u << 20));
     return h;
 }
@@ -3449,7 +3483,7 @@ uint64_t prepare_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, uin
     for (uint64_t v : {uint64_t(w.cap_spans), uint64_t(w.cap_cuts), uint64_t(w.cap_work), uint64_t(w.cap_tout),
                        uint64_t(ix->keycut_T[0]), uint64_t(ix->keycut_T[1]), uint64_t(ix->keycut_T[2]),
                        uint64_t(ix->keycut_T[3]), uint64_t(tile_bits_w[3]), uint64_t(hp.slots), uint64_t(hp.fill),
-                       uint64_t(hp.pmax), uint64_t(hp.sub_T)})
+                       uint64_t(hp.pmax), uint64_t(hp.sub_T), uint64_t(hp.dmax)})
         mixin(v);
     return h;
 }
@@ -3494,6 +3528,8 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     p.hash_fill = hp.fill;
     p.hash_pmax = hp.pmax;
     p.hash_sub_T = hp.sub_T;
+    p.hash_dmax = hp.dmax;
+    p.hash_min_items = 0;  // set with the scan grid below
     // span_chunk is the reference's chunk (ids per task chunk, engine.hpp:40);
     // a scan warp claims a quarter of one at a time (guided self-scheduling)
     uint32_t unit = cfg.span_chunk ? cfg.span_chunk / 4 : kDefaultUnit;
@@ -3577,6 +3613,12 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
         }
         per_sm = ac.scan_occ;
     }
+    // two items per scan CTA at least, or the hashed class is folded back (k_plan;
+    // GENIE_HASH_MIN_ITEMS overrides)
+    p.hash_min_items = env_u32("GENIE_HASH_MIN_ITEMS", 2 * static_cast<uint32_t>(sms) * per_sm);
+    // launched when the previous batch on this index wanted it (a dense batch
+    // pays no empty launch; GENIE_HASH_LAUNCH=1 forces it)
+    p.hash_launch = hp.slots && (ix->hash_wanted || env_u32("GENIE_HASH_LAUNCH", 0)) ? 1u : 0u;
     const MergeSrc m = tile_merge_src(ix, Q, d_k, out_stride, d_out, d_out_len, d_out_thr, id_offset);
     const bool big_rows = max_k > kSortCap;  // CUB segmented sort (allocates): never captured
 
@@ -3605,7 +3647,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
             k_scan<8><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             k_scan<16><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             launches += 3;
-            if (p.hash_slots) {  // the hashed sparse class is enabled (GENIE_HASH_TILES)
+            if (p.hash_launch) {  // the hashed sparse class (GENIE_HASH_TILES; see hash_wanted)
                 k_scan<kHashW><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
                 ++launches;
             }
@@ -3691,6 +3733,7 @@ int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
     const unsigned long long* h = ix->ws.h_status;
     for (int c = 0; c < kClasses; ++c)
         if (h[class_st(c)]) ix->class_seen[c] = true;  // its cut table is built before the next batch
+    if (!h[ST_OVERFLOW]) ix->hash_wanted = h[ST_HASH_WANT] != 0;
     if (stats) {
         stats->postings = h[ST_TOTAL_POSTINGS];
         stats->work_items = h[ST_TOTAL_WORK];

@@ -122,8 +122,11 @@ constexpr uint32_t kCompactFillInv = GENIE_COMPACT_FILL_INV;
 #ifndef GENIE_LANES_MAX  // dense lists per item up to which the lane-wise path runs (W <= 8)
 #define GENIE_LANES_MAX 3
 #endif
-#ifndef GENIE_HASH_TILES  // hashed sparse class: object tile = this many W = 8 counter tiles (0: class off)
-#define GENIE_HASH_TILES 0  // measured slower than the dense W = 8 tiles on C4 (1.37 M vs 2.0 M q/s): off
+#ifndef GENIE_HASH_TILES  // hashed sparse class: object tile = this many W = 8 counter tiles, <= 2^20 objects (0: off)
+#define GENIE_HASH_TILES 11
+#endif
+#ifndef GENIE_HASH_DENSE_MAX  // ... taken by queries with at most this many expected postings per W = 8 tile
+#define GENIE_HASH_DENSE_MAX 512  // (C4: ~1 500, dense tiles faster; 30-400: hashed 1.4-4.3x faster)
 #endif
 #ifndef GENIE_HASH_LOAD_PCT  // ... admits a query whose expected postings per tile fill <= this % of the table
 #define GENIE_HASH_LOAD_PCT 50
@@ -201,7 +204,8 @@ enum StatusWord : int {
     ST_P_STAGE = 37,
     ST_CLASS3 = 38,     // queries of the hashed sparse class (kHashW)
     ST_WORK_CTR3 = 39,  // its scan queue cursor
-    ST_WORDS = 40
+    ST_HASH_WANT = 40,  // the batch had enough hashed-class items to launch the class (next batch's hint)
+    ST_WORDS = 41
 };
 // Work classes: counter widths W = 4, 8, 16 (dense counter tiles) and the
 // hashed sparse class (class 3, pseudo-width kHashW = 32: a query whose
@@ -279,6 +283,9 @@ struct genie_index {
     genie::DevBuf<uint32_t> keycut[genie::kClasses];
     uint32_t keycut_T[genie::kClasses] = {0, 0, 0, 0};
     bool class_seen[genie::kClasses] = {false, false, false, false};
+    // the last batch had enough hashed-class items: launch k_scan<kHashW> in
+    // the next one (until then its queries run on dense tiles; results equal)
+    bool hash_wanted = false;
     // dense containers: keys whose list covers >= dense_density of the
     // objects also carry a bitmap of n bits (Roaring-style bitmap container)
     genie::DevBuf<int32_t> key_dense;   // [K] word offset of the key's row in `bitmaps`, or -1

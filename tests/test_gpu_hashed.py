@@ -2,11 +2,12 @@
 whose postings are few for the objects they spread over count into a
 shared-memory open-addressing table over tiles of GENIE_HASH_TILES x the
 W = 8 tile, with the c-PQ threshold read off the final counts and a radix
-selection of the tie ids.  The class is off by default (measured slower than
-the dense W = 8 tiles on C4); these tests switch it on through
-its knobs and compare every case with the CPU oracle (cpq.hpp:307-339 extract
-semantics, engine.hpp:158-177 merge), across knob values, which must not
-change results."""
+selection of the tie ids.  By default it takes only queries with at most
+GENIE_HASH_DENSE_MAX expected postings per W = 8 tile (ultra-sparse: there it
+is 1.4-4.3x faster; at C4's ~1 500 the dense tiles win); these
+tests also switch it on through its knobs for denser queries and compare every
+case with the CPU oracle (cpq.hpp:307-339 extract semantics,
+engine.hpp:158-177 merge), across knob values, which must not change results."""
 import os
 
 import numpy as np
@@ -25,7 +26,8 @@ def assert_same(got, want, label):
         assert got.row(q) == want.row(q), f"{label} q{q}"
 
 
-HASH_ON = {"GENIE_HASH_TILES": 4}
+# the class on for queries it would not take by default (C4-like density)
+HASH_ON = {"GENIE_HASH_TILES": 4, "GENIE_HASH_DENSE_MAX": 1 << 20, "GENIE_HASH_MIN_ITEMS": 0, "GENIE_HASH_LAUNCH": 1}
 
 
 class env:
@@ -84,19 +86,20 @@ def test_hashed_multi_tile_equals_oracle(multi_tile):
     with env(**HASH_ON):
         got = ix.query(qb)
     assert_same(got, want, "hashed")
-    # the class engaged: 3 hashed tiles per query instead of 10 W = 8 tiles
+    # the class engaged (its minimum batch share waived): 3 hashed tiles per
+    # query instead of 10 W = 8 tiles
     assert got.stats["work_items"] < len(qb) * 4
     assert got.stats["fallback_tiles"] == 0
-    # off by default
+    # by default this density (~1 500 postings per W = 8 tile) stays on dense tiles
     assert ix.query(qb).stats["work_items"] == len(qb) * 10
 
 
 @pytest.mark.parametrize("knobs", [
-    {"GENIE_HASH_TILES": 0},           # class off (the default): W = 8 dense tiles
-    {"GENIE_HASH_TILES": 4, "GENIE_HASH_FILL_PCT": 0},  # every hashed item through the 8-bit sub-tile path
-    {"GENIE_HASH_TILES": 1},           # hashed tiles of one W = 8 tile
-    {"GENIE_HASH_TILES": 9, "GENIE_HASH_LOAD_PCT": 100, "GENIE_HASH_FILL_PCT": 90},  # 2^20-object tile cap
-    {"GENIE_HASH_TILES": 4, "GENIE_HASH_LOAD_PCT": 5},  # admission threshold: a mix of classes
+    {"GENIE_HASH_TILES": 0},           # class off: W = 8 dense tiles
+    {**HASH_ON, "GENIE_HASH_FILL_PCT": 0},  # every hashed item through the 8-bit sub-tile path
+    {**HASH_ON, "GENIE_HASH_TILES": 1},  # hashed tiles of one W = 8 tile
+    {**HASH_ON, "GENIE_HASH_TILES": 11, "GENIE_HASH_LOAD_PCT": 100, "GENIE_HASH_FILL_PCT": 90},  # 2^20 objects
+    {**HASH_ON, "GENIE_HASH_LOAD_PCT": 5},  # admission threshold: a mix of classes
 ])
 def test_hashed_knobs_are_result_invariant(multi_tile, knobs):
     csr, ix, qb, want = multi_tile
@@ -153,4 +156,49 @@ def test_hashed_ranges_and_gate_floors(gpu, oracle):
         got = ix.query(qb)
     want = oracle.index(csr).execute(qb)
     assert_same(got, want, "ranges")
+    ix.close()
+
+
+def sparse_sets(n, live, m, domain, queries, rng):
+    """`live` objects spread over n ids (ultra-sparse lists)."""
+    ids = np.sort(rng.choice(n, size=live, replace=False)).astype(np.uint32)
+    toks = rng.integers(0, domain, size=(live, m), dtype=np.uint32)
+    flat = ((np.arange(m, dtype=np.uint64)[None, :] << np.uint64(32)) | toks.astype(np.uint64)).reshape(-1)
+    oid = np.repeat(ids, m)
+    order = np.argsort(flat, kind="stable")
+    sk, sid = flat[order], oid[order]
+    uniq, starts = np.unique(sk, return_index=True)
+    off = np.concatenate([starts.astype(np.uint64), np.array([sk.shape[0]], np.uint64)])
+    qt = toks[rng.integers(0, live, size=queries)].copy()
+    flip = rng.random(qt.shape) < 0.5
+    qt[flip] = rng.integers(0, domain, size=int(flip.sum()), dtype=np.uint32)
+    return CSR(n, uniq, off, sid), qt
+
+
+def test_hashed_class_by_default_on_ultra_sparse(gpu, oracle):
+    # 400K sets over 12M ids: ~65 postings per W = 8 tile -> hashed 2^20-object
+    # tiles by default (12 per query instead of 126 dense tiles)
+    rng = np.random.default_rng(21)
+    csr, qt = sparse_sets(12_000_000, 400_000, 32, 2048, 64, rng)
+    qb = point_queries(qt, 100)
+    ix = DeviceIndex.from_csr(csr, device=gpu)
+    want = oracle.index(csr).execute(qb)
+    # the first batch on the index runs dense tiles and flags the class; the
+    # class's kernel is launched from the next batch on
+    first = ix.query(qb)
+    assert first.stats["work_items"] == len(qb) * 126
+    assert_same(first, want, "ultra-sparse, first batch")
+    got = ix.query(qb)
+    assert got.stats["work_items"] == len(qb) * 12
+    assert_same(got, want, "ultra-sparse")
+    with env(GENIE_HASH_TILES=0):
+        dense = ix.query(qb)
+    assert dense.stats["work_items"] == len(qb) * 126
+    assert_same(dense, want, "ultra-sparse dense tiles")
+    # a few such queries in a batch (fewer hashed items than two per scan CTA)
+    # go back to dense tiles instead of a separate, mostly idle launch
+    few = qb.slice(0, 8)
+    got_few = ix.query(few)
+    assert got_few.stats["work_items"] == len(few) * 126
+    assert_same(got_few, oracle.index(csr).execute(few), "few ultra-sparse")
     ix.close()
