@@ -343,8 +343,9 @@ int genie_merge_topk(int device, uint32_t Q, uint32_t L, const genie_entry* in, 
         d_out.reserve(uint64_t(Q) * stride);
         d_olen.reserve(Q + 1);
         d_othr.reserve(Q + 1);
+        // host lists (mcx::merge_topk) may come in any order: no list floors
         launch_list_merge(&tmp, Q, L, d_in.p, d_len.p, in_stride, d_k.p, stride, d_out.p, d_olen.p,
-                          d_othr.p, max_k, tmp.stream, false);
+                          d_othr.p, max_k, tmp.stream, false, false);
         std::string msg;
         const int rc = finish_batch(&tmp, nullptr, msg, nullptr);
         if (rc != GENIE_OK) throw Error(rc, msg);

@@ -2787,6 +2787,7 @@ struct MergeSrc {
     const uint32_t* tile_len;
     const genie_entry* tile_out;
     const uint32_t* q_floor;  // per-query floor (tile mode) or null
+    int sorted_lists;         // mode 1: every list is ordered by (count desc, id asc) (list floors apply)
     // mode 1: list l of query q at in + q * in_q + l * in_l, length in_len[q * len_q + l * len_l]
     uint32_t L;
     const genie_entry* in;
@@ -2827,18 +2828,41 @@ __global__ void __launch_bounds__(THREADS) k_merge(MergeSrc m, uint32_t cap) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
     __shared__ unsigned long long sums[32];
-    __shared__ uint32_t s_flag, s_pos;
+    __shared__ uint32_t s_flag, s_pos, s_lfloor, s_total;
     __shared__ uint32_t s_scratch[256 + 8];
     // a workspace overflow skipped k_worklist..k_scan: tile_len / tile_out
     // hold nothing of this batch (the host grows the workspace and retries)
     if (m.st[ST_OVERFLOW]) return;
+    // list merges: the duplicate-id set lives in the upper half of the buffer
+    uint32_t* dset = reinterpret_cast<uint32_t*>(keys + cap / 2);
+    const uint32_t dslots = cap;  // u32 slots in cap / 2 keys (a power of two)
     for (uint32_t q = blockIdx.x; q < m.Q; q += gridDim.x) {
         const uint32_t L = nlists_of(m, q);
         const uint32_t kq = m.k[q];
         // Gather the union, dropping entries below the query's floor: the
         // floor is the k-th count of some tile, so at least k entries sit at
         // or above it and nothing below can make the merged top-k.
-        const uint32_t floor = m.q_floor ? m.q_floor[q] : 0u;
+        uint32_t floor = m.q_floor ? m.q_floor[q] : 0u;
+        // List merges (rows of partitions / shards, each sorted by count desc,
+        // id asc): the floor is the largest k-th count over the rows, by the
+        // same argument; every id still goes through the duplicate-id set, so
+        // the ContractError verdict covers the whole union (engine.hpp:165-172)
+        bool lset = false;
+        if (m.mode == 1) {
+            if (threadIdx.x == 0) s_lfloor = 0, s_total = 0, s_flag = 0;
+            __syncthreads();
+            for (uint32_t l = threadIdx.x; l < L; l += blockDim.x) {
+                const genie_entry* bb;
+                uint32_t ll;
+                list_of(m, q, l, bb, ll);
+                atomicAdd(&s_total, ll);
+                if (kq && ll >= kq) atomicMax(&s_lfloor, bb[kq - 1].count);
+            }
+            for (uint32_t i = threadIdx.x; i < dslots; i += blockDim.x) dset[i] = 0xffffffffu;
+            __syncthreads();
+            lset = 2 * s_total <= dslots;  // block-uniform
+            if (lset && m.sorted_lists) floor = s_lfloor;
+        }
         if (threadIdx.x == 0) s_pos = 0;
         __syncthreads();
         {
@@ -2851,19 +2875,34 @@ __global__ void __launch_bounds__(THREADS) k_merge(MergeSrc m, uint32_t cap) {
                     const uint32_t e = e0 + lane;
                     genie_entry x{0, 0};
                     if (e < ll) x = bb[e];
+                    if (lset && e < ll) {  // duplicate-id set (list merges)
+                        uint32_t h = (x.id * 0x9E3779B1u) & (dslots - 1);
+                        for (;;) {
+                            const uint32_t old = atomicCAS(&dset[h], 0xffffffffu, x.id);
+                            if (old == 0xffffffffu) break;
+                            if (old == x.id) {
+                                s_flag = 1;
+                                break;
+                            }
+                            h = (h + 1) & (dslots - 1);
+                        }
+                    }
                     const bool keep = e < ll && x.count >= floor;
                     const uint32_t mask = __ballot_sync(0xffffffffu, keep);
                     uint32_t base = 0;
                     if (lane == 0 && mask) base = atomicAdd(&s_pos, static_cast<uint32_t>(__popc(mask)));
                     base = __shfl_sync(0xffffffffu, base, 0);
                     const uint32_t pos = base + __popc(mask & ((1u << lane) - 1u));
-                    if (keep && pos < cap) keys[pos] = order_key(x.id, x.count);
+                    if (keep && pos < (lset ? cap / 2 : cap)) keys[pos] = order_key(x.id, x.count);
                 }
             }
         }
         __syncthreads();
         const uint32_t filled = s_pos;
-        if (filled > cap) {  // large union: radix selection path (k_merge_big)
+        if (lset) {
+            if (s_flag && threadIdx.x == 0) atomicMin(&m.st[ST_MERGE_DUP], (unsigned long long)q);
+        }
+        if (filled > (lset ? cap / 2 : cap)) {  // large union: radix selection path (k_merge_big)
             if (threadIdx.x == 0) {
                 m.q_big[q] = 1;
                 atomicAdd(&m.st[ST_MERGE_BIG], 1ull);
@@ -2876,7 +2915,36 @@ __global__ void __launch_bounds__(THREADS) k_merge(MergeSrc m, uint32_t cap) {
         while (N < filled) N <<= 1;
         for (uint32_t i = filled + threadIdx.x; i < N; i += blockDim.x) keys[i] = ~0ull;
         __syncthreads();
-        if (m.mode == 1 && filled > 1) {
+        uint32_t H = 1;  // slots of the duplicate-id set (list merges)
+        while (H < 2 * filled) H <<= 1;
+        if (lset) {
+            // checked while gathering
+        } else if (m.mode == 1 && filled > 1 && N + H / 2 <= cap) {
+            // duplicate ids across lists are a ContractError (engine.hpp:165-172):
+            // every id goes into an open-addressing set in the shared memory
+            // after the union (>= 2 slots per entry), a second insert of an id
+            // is the duplicate -- the same verdict as the reference's sort by id
+            uint32_t* set = reinterpret_cast<uint32_t*>(keys + N);
+            for (uint32_t i = threadIdx.x; i < H; i += blockDim.x) set[i] = 0xffffffffu;
+            if (threadIdx.x == 0) s_flag = 0;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < filled; i += blockDim.x) {
+                const uint32_t id = key_id(keys[i]);
+                uint32_t h = (id * 0x9E3779B1u) & (H - 1);
+                for (;;) {
+                    const uint32_t old = atomicCAS(&set[h], 0xffffffffu, id);
+                    if (old == 0xffffffffu) break;
+                    if (old == id) {
+                        s_flag = 1;
+                        break;
+                    }
+                    h = (h + 1) & (H - 1);
+                }
+            }
+            __syncthreads();
+            if (s_flag && threadIdx.x == 0) atomicMin(&m.st[ST_MERGE_DUP], (unsigned long long)q);
+            __syncthreads();
+        } else if (m.mode == 1 && filled > 1) {
             // duplicate ids across lists are a ContractError (engine.hpp:165-172)
             for (uint32_t i = threadIdx.x; i < filled; i += blockDim.x) {
                 const uint64_t k0 = keys[i];
@@ -3775,7 +3843,7 @@ int finish_batch(genie_index* ix, genie_batch_stats* stats, std::string& msg,
 void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
                        const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
                        uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
-                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s, bool list_major) {
+                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s, bool list_major, bool sorted_lists) {
     Workspace& w = ix->ws;
     if (!w.status.p) {
         w.status.reserve(ST_WORDS);
@@ -3796,6 +3864,7 @@ void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entr
     m.in_l = list_major ? uint64_t(Q) * in_stride : in_stride;
     m.len_q = list_major ? 1 : L;
     m.len_l = list_major ? Q : 1;
+    m.sorted_lists = sorted_lists ? 1 : 0;
     m.k = d_k;
     m.Q = Q;
     m.id_offset = 0;
@@ -3817,7 +3886,14 @@ void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entr
     }
     const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(Q, ix->sms * 4));
     if (Q) {
-        k_merge<kMergeThreads><<<grid, kMergeThreads, msmem, s>>>(m, kSortCap);
+        // unions that fit the small merge (the per-shard rows of a multi-GPU
+        // batch: L x k entries) take one 128-thread CTA per query, as the
+        // batch's tile merge does; larger ones the 512-thread CTAs
+        if (uint64_t(L) * std::max<uint32_t>(max_k, 1) <= kMergeSmallCap)
+            k_merge<kMergeSmallThreads><<<Q, kMergeSmallThreads, kMergeSmallCap * sizeof(uint64_t), s>>>(
+                m, kMergeSmallCap);
+        else
+            k_merge<kMergeThreads><<<grid, kMergeThreads, msmem, s>>>(m, kSortCap);
         k_merge_big<<<grid, kMergeThreads, msmem, s>>>(m);
         if (max_k > kSortCap) segmented_sort_rows(ix, Q, out_stride, d_out, d_out_len, 0, s);
     }

@@ -324,7 +324,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
 void launch_list_merge(genie_index* ix, uint32_t Q, uint32_t L, const genie_entry* d_in,
                        const uint32_t* d_in_len, uint32_t in_stride, const uint32_t* d_k,
                        uint32_t out_stride, genie_entry* d_out, uint32_t* d_out_len,
-                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s, bool list_major);
+                       uint32_t* d_out_thr, uint32_t max_k, cudaStream_t s, bool list_major, bool sorted_lists = true);
 
 // Host-side set-up of a batch (tile sizes, workspace, cut tables) without any
 // stream work, so the launch that follows can be captured; returns a digest of
