@@ -747,7 +747,8 @@ struct ItemCtx {
     uint32_t q, t, kq, bound, tile_lo, tile_n, words, ht_cap, cap, slot;
     uint32_t rec_b;  // base level of the tile's record (every emitted entry counts >= rec_b)
     uint64_t out_base;
-    bool gate;
+    bool gate;   // Selector::cpq semantics: tile records, query floor
+    bool admit;  // ... and the scan-time c-PQ gate (admissions); else the tile's exact histogram select
 };
 
 // The c-PQ admission path (cpq.hpp:294-301): the new value passed the
@@ -1709,7 +1710,7 @@ template <int W, bool IL>
 __device__ __forceinline__ void scan_group_range(const BatchParams& p, const ItemCtx& it, const ScanSmem& sm,
                                                  const StageBuf& sb, uint32_t nsb, uint32_t G, uint32_t g0,
                                                  uint32_t g1, uint32_t stride = 1) {
-    if (it.gate) scan_warp_groups<W, true, IL>(p.postings, it, sm, sb, nsb, G, g0, g1, stride);
+    if (it.admit) scan_warp_groups<W, true, IL>(p.postings, it, sm, sb, nsb, G, g0, g1, stride);
     else scan_warp_groups<W, false, IL>(p.postings, it, sm, sb, nsb, G, g0, g1, stride);
 }
 
@@ -1728,7 +1729,7 @@ __device__ void scan_groups(const BatchParams& p, const ItemCtx& it, const ScanS
         // contiguous shares of ceil(ptot / nwarps) (32-bit arithmetic)
         const uint32_t share = (ptot + nwarps - 1) / nwarps;
         const uint32_t r0 = min(ptot, warp * share), r1 = min(ptot, r0 + share);
-        if (it.gate) scan_compact<W, true, IL>(p.postings, it, sm, sb, nsb, r0, r1);
+        if (it.admit) scan_compact<W, true, IL>(p.postings, it, sm, sb, nsb, r0, r1);
         else scan_compact<W, false, IL>(p.postings, it, sm, sb, nsb, r0, r1);
         return;
     }
@@ -2016,7 +2017,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
     }
 #endif
     // ---- select: the tile's exact top-k
-    if (it.gate && !sm.scal[SC_OVF]) {
+    if (it.admit && !sm.scal[SC_OVF]) {
         uint32_t a = sm.scal[SC_AT];  // every thread finishes AT (cpq.hpp:383-389)
         while (a <= it.bound && sm.za[a] >= it.kq) ++a;
         const uint32_t thr = a - 1;  // cpq.hpp:310-311
@@ -2063,7 +2064,7 @@ __device__ void scan_and_select(const BatchParams& p, const ItemCtx& it, const S
             if (threadIdx.x == 0) atomicMax(&p.q_floor[it.q], thr);
         }
     } else {
-        if (it.gate && threadIdx.x == 0) atomicAdd(&p.st[ST_FALLBACK], 1ull);
+        if (it.admit && threadIdx.x == 0) atomicAdd(&p.st[ST_FALLBACK], 1ull);
         const uint32_t T_t = hist_select<W, IL>(p, it, sm);
         if (it.gate && T_t > 0 && threadIdx.x == 0) atomicMax(&p.q_floor[it.q], T_t);
     }
@@ -2257,7 +2258,7 @@ GENIE_PREP_FN void prepare_item(const BatchParams& p, const ScanSmem& sm, uint32
     __syncwarp();
 }
 
-template <int W>
+template <int W, bool FH>
 __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t b, const WorkQueue& total) {
 #ifdef GENIE_PHASE_TIMERS
     const long long t_begin = clock64();
@@ -2277,6 +2278,15 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
     it.slot = d.tile_slot;
     it.out_base = d.out_base;
     it.gate = (p.selector == GENIE_SELECT_CPQ) && W <= 8;
+    // An item whose gate starts at zero (a query's first tile: no floor, no
+    // lower-tile records) admits in bulk until AT climbs; on a small tile
+    // (<= kFirstHistWords counter words, e.g. C1's one-tile queries) it is
+    // cheaper to count without the gate and take the exact histogram select
+    // (records and floor as usual: C1 1.38 M -> 2.0 M q/s); on large tiles
+    // the histogram's pass over every counter costs more (C2 -21 %)
+    // (FH: the k_scan<4> instance launched for indexes of at most kFirstHistWords
+    // x 32 / 4 objects; every other instance keeps the gate: admit == gate)
+    it.admit = FH ? it.gate && !(d.a0 <= 1 && it.words <= kFirstHistWords) : it.gate;
     // The table sits right after the item's counters (whole 16-word steps of
     // dense_init): p.ht_slots slots, or -- for a query's first tile, whose
     // gate starts low without lower-tile records and admits in bulk (one-tile
@@ -2296,7 +2306,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
 
     // setup (cpq.hpp:281-292): empty table and ZA, AT at the gate start
     // (gate_start); counters zeroed unless the dense phase writes them
-    if (it.gate) {
+    if (it.admit) {
         uint4* ht4 = reinterpret_cast<uint4*>(sm.ht);
         for (uint32_t i = threadIdx.x; i < it.ht_cap / 2; i += blockDim.x) ht4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
         for (uint32_t i = threadIdx.x; i <= it.bound; i += blockDim.x) sm.za[i] = 0;
@@ -2332,7 +2342,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
     if (nd) {
         const uint32_t at0 = sm.scal[SC_AT];
         const uint32_t dmax = min(nd, it.bound);
-        const uint32_t nlv = (it.gate && at0 <= dmax) ? min(dmax - at0 + 1, kLvl) : 0u;
+        const uint32_t nlv = (it.admit && at0 <= dmax) ? min(dmax - at0 + 1, kLvl) : 0u;
 #ifdef GENIE_PHASE_TIMERS
         const long long t_d = clock64();
 #endif
@@ -2344,7 +2354,7 @@ __device__ void process_item(const BatchParams& p, const ScanSmem& sm0, uint32_t
 #else
         const uint32_t reach = dense_init<W>(p, it, sm, sm.sb(b), nd, at0, nlv, csa_path);
 #endif
-        if (it.gate && at0 <= dmax) dense_gate<W>(it, sm, at0, dmax, nlv, reach, csa_path);
+        if (it.admit && at0 <= dmax) dense_gate<W>(it, sm, at0, dmax, nlv, reach, csa_path);
 #ifdef GENIE_PHASE_TIMERS
         if (threadIdx.x == 0) {
             atomicAdd(&p.st[ST_T_DENSE], static_cast<unsigned long long>(clock64() - t_d));
@@ -2659,6 +2669,7 @@ __device__ void process_item_hashed(const BatchParams& p, const ScanSmem& sm, ui
     it.slot = d.tile_slot;
     it.out_base = d.out_base;
     it.gate = true;
+    it.admit = false;
     it.ht_cap = 0;
     const uint32_t nsb = min(kSpanBatch, d.S), ptot = d.ptot;
     const uint32_t H = p.hash_slots;
@@ -2717,7 +2728,7 @@ __device__ void process_item_hashed(const BatchParams& p, const ScanSmem& sm, ui
 // One persistent kernel per counter width W (its own register allocation):
 // the CTAs drain the W class's slice of the work list (k_worklist orders the
 // list class-major), a launch per class.
-template <int W>
+template <int W, bool FH = false>
 __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
     k_scan(BatchParams p, uint32_t tile_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -2769,7 +2780,7 @@ __global__ void __launch_bounds__(kScanThreads, kScanCtasPerSm)
         const uint32_t b = iter & 1u;
         if (!sm.desc[b].valid) break;
         if constexpr (W == kHashW) process_item_hashed(p, sm, b, total);
-        else process_item<W>(p, sm, b, total);
+        else process_item<W, FH>(p, sm, b, total);
     }
 }
 
@@ -3659,6 +3670,7 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
     DeviceAttrCache& ac = attr_cache(ix->device);
     if (ac.scan_smem < smem) {
         GENIE_CUDA(cudaFuncSetAttribute(k_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        GENIE_CUDA(cudaFuncSetAttribute(k_scan<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         GENIE_CUDA(cudaFuncSetAttribute(k_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         GENIE_CUDA(cudaFuncSetAttribute(k_scan<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         GENIE_CUDA(cudaFuncSetAttribute(k_scan<kHashW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -3711,7 +3723,12 @@ void launch_batch(genie_index* ix, const genie_config& cfg, uint32_t Q, const ui
             launches += 4;
             if (timed) record(1);
             // one launch per width class (an empty class's CTAs exit at once)
-            k_scan<4><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+            // small indexes (one W = 4 tile of <= kFirstHistWords counter words):
+            // the instance whose gate-less first tiles take the histogram select
+            if (uint64_t(ix->n) * 4 <= uint64_t(kFirstHistWords) * 32)
+                k_scan<4, true><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
+            else
+                k_scan<4><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             k_scan<8><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             k_scan<16><<<sms * per_sm, kScanThreads, smem, s>>>(p, tile_bytes);
             launches += 3;

@@ -150,6 +150,10 @@ constexpr uint32_t kHashScratch = 20u << 10;  // per-warp count histograms + tie
 #ifndef GENIE_CSA64  // ... and (>= 7 planes) 64-list steps before those
 #define GENIE_CSA64 1
 #endif
+#ifndef GENIE_FIRST_HIST_WORDS  // items whose c-PQ gate starts at zero, on tiles of at most this many
+#define GENIE_FIRST_HIST_WORDS 8192  // counter words: no admissions, exact histogram select (0: never)
+#endif
+constexpr uint32_t kFirstHistWords = GENIE_FIRST_HIST_WORDS;
 #ifndef GENIE_CSA_QUAD
 #define GENIE_CSA_QUAD 0
 #endif

@@ -70,7 +70,7 @@ def capture(workloads):
         # classes' k_scan launches exit at once
         wcls = 4 if w in ("tweets", "adult") else 8
         cmd = ["ncu", "--set", "full", "--metrics", ",".join(METRICS), "--clock-control", "none",
-               "--import-source", "on", "--kernel-name-base", "demangled", "-k", f"regex:k_scan<\\(int\\){wcls}>",
+               "--import-source", "on", "--kernel-name-base", "demangled", "-k", f"regex:k_scan<\\(int\\){wcls},",
                "--launch-skip", "3", "--launch-count", "1",
                "-f", "-o", str(rep), sys.executable, str(ROOT / "bench.py"), "--workload", w, "--steps", "1",
                "--warmup", "3", "--no-cpu-baseline"]
